@@ -1,0 +1,137 @@
+"""ctypes binding of libtnl.so (include/tnl.h) — the only route to compute.
+
+There is no CPU fallback: if the library or a GPU is missing, every compute
+entry point raises ``DeviceError``. Loading the library itself needs only the
+CUDA runtime, so CPU-only test boxes can check the exported symbols.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import DeviceError, NumericsError, RankError, ShapeError, UnsupportedError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtnl.so")
+
+TNL_OK, TNL_ERR_SHAPE, TNL_ERR_RANK, TNL_ERR_NUMERICS, TNL_ERR_CUDA, TNL_ERR_UNSUPPORTED, TNL_ERR_ARG = range(7)
+FAMILY_CODE = {"dense": 0, "tucker": 1, "tt": 2, "tr": 3}
+TNL_F64, TNL_F32, TNL_BF16 = 0, 1, 2
+PLAN_AUTO, PLAN_CUT, PLAN_CHAIN, PLAN_GENERIC, PLAN_NO_DECODE = 0, 1, 2, 4, 8
+PLAN_NAMES = {PLAN_CUT: "cut", PLAN_CHAIN: "chain", PLAN_GENERIC: "generic", 0: "none"}
+MAX_MODES = 6
+
+# Every symbol include/tnl.h declares (checked by tests/test_abi.py).
+EXPORTED = (
+    "tnl_abi_version",
+    "tnl_last_error",
+    "tnl_plan_create",
+    "tnl_plan_create_rows",
+    "tnl_plan_destroy",
+    "tnl_plan_query",
+    "tnl_workspace_size",
+    "tnl_forward",
+    "tnl_forward_host",
+    "tnl_reconstruct",
+    "tnl_launch_count",
+)
+
+
+class LayerDesc(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_int32),
+        ("ndim", ctypes.c_int32),
+        ("row_mode_count", ctypes.c_int32),
+        ("src_dtype", ctypes.c_int32),
+        ("mode_shape", ctypes.c_int64 * MAX_MODES),
+        ("ranks", ctypes.c_int64 * (MAX_MODES + 1)),
+        ("arrays", ctypes.c_void_p * (MAX_MODES + 1)),
+    ]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int64),
+        ("cols", ctypes.c_int64),
+        ("r_cut", ctypes.c_int64),
+        ("param_count", ctypes.c_int64),
+        ("chain_flops_per_token", ctypes.c_int64),
+        ("cut_flops_per_token", ctypes.c_int64),
+        ("dense_flops_per_token", ctypes.c_int64),
+        ("weight_bytes", ctypes.c_int64),
+        ("decode_weight_bytes", ctypes.c_int64),
+        ("compute_dtype", ctypes.c_int32),
+        ("plan_large", ctypes.c_int32),
+        ("plan_small", ctypes.c_int32),
+        ("decode_max_m", ctypes.c_int32),
+        ("row_begin", ctypes.c_int64),
+        ("row_end", ctypes.c_int64),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib_path() -> str:
+    return LIB_PATH
+
+
+def load():
+    """Load libtnl.so once; raises DeviceError (no fallback) when it is absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2602_01613_b200.build` "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        lib.tnl_abi_version.restype = ctypes.c_int
+        lib.tnl_last_error.restype = ctypes.c_char_p
+        lib.tnl_plan_create.argtypes = [ctypes.POINTER(LayerDesc), ctypes.c_int32, i64, ctypes.c_int32, ctypes.POINTER(P)]
+        lib.tnl_plan_create_rows.argtypes = [
+            ctypes.POINTER(LayerDesc), ctypes.c_int32, i64, ctypes.c_int32, i64, i64, ctypes.POINTER(P)]
+        lib.tnl_plan_destroy.argtypes = [P]
+        lib.tnl_plan_query.argtypes = [P, ctypes.POINTER(PlanInfo)]
+        lib.tnl_workspace_size.argtypes = [P, i64, ctypes.POINTER(ctypes.c_size_t)]
+        lib.tnl_forward.argtypes = [P, P, i64, i64, P, i64, P, ctypes.c_size_t, P]
+        lib.tnl_forward_host.argtypes = [P, P, i64, P, P]
+        lib.tnl_reconstruct.argtypes = [P, P, i64, ctypes.c_int32, P]
+        lib.tnl_launch_count.argtypes = [ctypes.c_int32]
+        lib.tnl_launch_count.restype = i64
+        for name in ("tnl_plan_create", "tnl_plan_create_rows", "tnl_plan_destroy", "tnl_plan_query",
+                     "tnl_workspace_size", "tnl_forward", "tnl_forward_host", "tnl_reconstruct"):
+            getattr(lib, name).restype = ctypes.c_int
+        if lib.tnl_abi_version() != 1:
+            raise DeviceError(f"libtnl ABI {lib.tnl_abi_version()} != 1")
+        _lib = lib
+        return lib
+
+
+def check(status: int) -> None:
+    """Map a tnl_status onto the reference exception classes (errors.py:8-21)."""
+    if status == TNL_OK:
+        return
+    msg = (load().tnl_last_error() or b"").decode(errors="replace")
+    if status == TNL_ERR_SHAPE:
+        raise ShapeError(msg)
+    if status == TNL_ERR_RANK:
+        raise RankError(msg)
+    if status == TNL_ERR_NUMERICS:
+        raise NumericsError(msg)
+    if status == TNL_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    if status == TNL_ERR_ARG:
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(load().tnl_launch_count(1 if reset else 0))

@@ -1,0 +1,153 @@
+// generic.cu — CUDA-core strided batched contraction (see generic.cuh).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "generic.cuh"
+
+namespace tnl {
+
+namespace {
+
+constexpr int TI = 64, TJ = 64, TP = 16;
+
+template <typename T>
+__device__ __forceinline__ float ld_as_float(const T* p);
+template <>
+__device__ __forceinline__ float ld_as_float<float>(const float* p) {
+  return __ldg(p);
+}
+template <>
+__device__ __forceinline__ float ld_as_float<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+
+template <typename TA, typename TB, typename TC>
+__global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tiles_i,
+                                                           int64_t tiles_j) {
+  __shared__ float sA[TP][TI + 4];
+  __shared__ float sB[TP][TJ + 4];
+  const int64_t tile = blockIdx.x;
+  const int64_t tj = tile % tiles_j;
+  const int64_t ti = (tile / tiles_j) % tiles_i;
+  const int64_t bb = tile / (tiles_j * tiles_i);
+  const int64_t b2 = bb % s.b2;
+  const int64_t b1 = bb / s.b2;
+  const TA* A = static_cast<const TA*>(s.A) + b1 * s.sa1 + b2 * s.sa2;
+  const TB* B = static_cast<const TB*>(s.B) + b1 * s.sb1 + b2 * s.sb2;
+  TC* C = static_cast<TC*>(s.C) + b1 * s.sc1 + b2 * s.sc2;
+
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t i0 = ti * TI, j0 = tj * TJ;
+  float acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+
+  for (int64_t p0 = 0; p0 < s.P; p0 += TP) {
+    // A tile: TI x TP, B tile: TP x TJ  (256 threads, 4 elements each)
+    for (int e = threadIdx.x; e < TI * TP; e += 256) {
+      int ii, pp;
+      if (s.sap == 1) {  // contiguous along p: let consecutive threads walk p
+        pp = e % TP;
+        ii = e / TP;
+      } else {
+        ii = e % TI;
+        pp = e / TI;
+      }
+      const int64_t gi = i0 + ii, gp = p0 + pp;
+      sA[pp][ii] = (gi < s.I && gp < s.P) ? ld_as_float(A + gi * s.sai + gp * s.sap) : 0.f;
+    }
+    for (int e = threadIdx.x; e < TP * TJ; e += 256) {
+      int jj, pp;
+      if (s.sbj == 1) {
+        jj = e % TJ;
+        pp = e / TJ;
+      } else {
+        pp = e % TP;
+        jj = e / TP;
+      }
+      const int64_t gj = j0 + jj, gp = p0 + pp;
+      sB[pp][jj] = (gj < s.J && gp < s.P) ? ld_as_float(B + gp * s.sbp + gj * s.sbj) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int pp = 0; pp < TP; ++pp) {
+      float a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = sA[pp][ty * 4 + q];
+        b[q] = sB[pp][tx * 4 + q];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int64_t gi = i0 + ty * 4 + x;
+    if (gi >= s.I) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int64_t gj = j0 + tx * 4 + y;
+      if (gj >= s.J) continue;
+      TC* dst = C + gi * s.sci + gj * s.scj;
+      if constexpr (sizeof(TC) == 4) {
+        if (s.accumulate)
+          *dst += acc[x][y];
+        else
+          *dst = acc[x][y];
+      } else {
+        *dst = __float2bfloat16_rn(acc[x][y]);
+      }
+    }
+  }
+}
+
+template <typename TA, typename TB>
+int launch_c(const GStep& s, int64_t tiles_i, int64_t tiles_j, int64_t blocks, cudaStream_t st) {
+  if (s.c_dt == DT_F32)
+    generic_step_kernel<TA, TB, float><<<(unsigned)blocks, 256, 0, st>>>(s, tiles_i, tiles_j);
+  else
+    generic_step_kernel<TA, TB, __nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(s, tiles_i,
+                                                                                 tiles_j);
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
+template <typename TA>
+int launch_b(const GStep& s, int64_t ti, int64_t tj, int64_t blocks, cudaStream_t st) {
+  if (s.b_dt == DT_F32) return launch_c<TA, float>(s, ti, tj, blocks, st);
+  return launch_c<TA, __nv_bfloat16>(s, ti, tj, blocks, st);
+}
+
+}  // namespace
+
+int launch_generic_step(const GStep& in, cudaStream_t stream) {
+  GStep s = in;
+  if (s.I <= 0 || s.J <= 0 || s.b1 <= 0 || s.b2 <= 0) return 0;
+  // Fold b2 then b1 into I when the operand strides are compatible.
+  auto fold = [&](int64_t& bcount, int64_t& sa, int64_t& sb, int64_t& sc) {
+    if (bcount > 1 && sb == 0 && sa == s.sai * s.I && sc == s.sci * s.I) {
+      s.I *= bcount;
+      bcount = 1;
+      sa = sb = sc = 0;
+    }
+  };
+  fold(s.b2, s.sa2, s.sb2, s.sc2);
+  if (s.b2 == 1) fold(s.b1, s.sa1, s.sb1, s.sc1);
+  if (s.P <= 0) return 0;
+  const int64_t tiles_i = (s.I + TI - 1) / TI, tiles_j = (s.J + TJ - 1) / TJ;
+  const int64_t blocks = tiles_i * tiles_j * s.b1 * s.b2;
+  if (blocks > 0x7fffffffLL) return (int)cudaErrorInvalidConfiguration;
+  if (s.a_dt == DT_F32) return launch_b<float>(s, tiles_i, tiles_j, blocks, stream);
+  return launch_b<__nv_bfloat16>(s, tiles_i, tiles_j, blocks, stream);
+}
+
+}  // namespace tnl

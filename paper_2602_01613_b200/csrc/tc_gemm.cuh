@@ -1,0 +1,37 @@
+// tc_gemm.cuh — tcgen05/TMEM/TMA GEMM step: D[i][j] = sum_k A[i][k] * B[j][k].
+//
+// A ("M side", 128-row tiles) and B ("N side", BN-row tiles) are bf16 K-major
+// matrices described by 2-D TMA tensor maps (128B swizzle, 64-element K boxes).
+// D accumulates in fp32 in TMEM and is written to out[i*ldo_i + j*ldo_j] as
+// bf16, fp32, or fp32 atomic adds (split-K). Used for every dense contraction
+// step of the bf16 plans: merged-cut (X.B_in^T, T.A_out^T), the Tucker-2 chain
+// (X.U1, T1.G^T, T2.U0^T) and dense layers; in "swap-AB" form (A = weight
+// panel, B = activations) for small-M decode.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tnl {
+
+enum TcOutMode : int32_t { TC_OUT_BF16 = 0, TC_OUT_F32_ATOMIC = 1, TC_OUT_F32 = 2 };
+
+struct TcGemmArgs {
+  int32_t M, N, K;
+  int32_t kb_per_split;  // K blocks (of 64) per blockIdx.z
+  void* out;
+  int64_t ldo_i, ldo_j;
+  int32_t out_mode;
+};
+
+// Encodes a 2-D bf16 K-major tensor map: `rows` rows of `k` elements with a
+// row pitch of `ld` elements, boxes of 64 (K) x box_rows. Returns 0 on success.
+int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t k, int64_t rows, int64_t ld,
+                   int box_rows);
+
+// bn in {16,32,64,128,256}; splits >= 1 (grid.z). Returns cudaError_t as int.
+int launch_tc_gemm(const CUtensorMap& a, const CUtensorMap& b, const TcGemmArgs& args, int bn,
+                   int splits, bool pdl, cudaStream_t stream);
+
+}  // namespace tnl

@@ -1,0 +1,1204 @@
+// tnl_api.cu — C-ABI (include/tnl.h) + host planner for the TN-linear layer.
+//
+// Reference anchors (arxiv/paper_2602_01613, /root/reference/pkg/src/minima):
+//   validate            tn_decompositions.py:97-126   -> validate_desc
+//   matrix_shape/ranks  tn_decompositions.py:82-95    -> Plan::rows/cols, cut_rank
+//   reconstruct         tn_decompositions.py:346-361  -> tnl_reconstruct (chain on identity)
+//   layer_to_matrix @ x tn_decompositions.py:364 + sensitivity.py:156 -> tnl_forward
+//   param_count         tn_decompositions.py:368-374  -> tnl_plan_query
+//   errors              errors.py:8-21                -> tnl_status + tnl_last_error
+//
+// Plans. Every layer factorises through its cut bond (row modes first,
+// tn_decompositions.py:59-63): y = A_out (B_in x). The planner keeps
+//   * GENERIC: the core-by-core chain as CUDA-core strided steps (exact fp32);
+//   * CUT    : B_in (r_cut x cols) and A_out (rows x r_cut) pre-contracted once
+//              at plan time, forward = two tcgen05 GEMM steps;
+//   * CHAIN  : Tucker-2 as three tcgen05 GEMM steps (U_in, G, U_out);
+//   * DENSE  : one tcgen05 GEMM step.
+// bf16 plans use the tensor-core steps; fp32 plans use GENERIC.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tnl.h"
+#include "common.cuh"
+#include "generic.cuh"
+#include "tc_gemm.cuh"
+
+namespace tnl {
+
+static thread_local int64_t g_launches = 0;
+void count_launch(int64_t n) { g_launches += n; }
+int64_t launch_count(bool reset) {
+  int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+static thread_local std::string g_err;
+
+static tnl_status fail(tnl_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (cudaError_t)(expr);                                               \
+    if (_e != cudaSuccess)                                                              \
+      return fail(TNL_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+static inline int64_t prod(const int64_t* a, int lo, int hi) {
+  int64_t p = 1;
+  for (int i = lo; i < hi; ++i) p *= a[i];
+  return p;
+}
+static inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// small device kernels
+// ---------------------------------------------------------------------------
+__global__ void f32_to_bf16_2d(const float* __restrict__ src, int64_t lds, __nv_bfloat16* dst,
+                               int64_t ldd, int64_t rows, int64_t cols) {
+  int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / cols, c = e % cols;
+    dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+  }
+}
+__global__ void identity_f32(float* dst, int64_t rows, int64_t cols, int64_t offset) {
+  // dst[r][c] = (c == r + offset)
+  int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / cols, c = e % cols;
+    dst[e] = (c == r + offset) ? 1.f : 0.f;
+  }
+}
+__global__ void copy_2d_any(const void* src, int s_dt, int64_t s_r, int64_t s_c, void* dst, int d_dt,
+                            int64_t d_r, int64_t d_c, int64_t rows, int64_t cols) {
+  int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / cols, c = e % cols;
+    float v = s_dt == DT_F32 ? static_cast<const float*>(src)[r * s_r + c * s_c]
+                             : __bfloat162float(static_cast<const __nv_bfloat16*>(src)[r * s_r + c * s_c]);
+    if (d_dt == DT_F32)
+      static_cast<float*>(dst)[r * d_r + c * d_c] = v;
+    else
+      static_cast<__nv_bfloat16*>(dst)[r * d_r + c * d_c] = __float2bfloat16_rn(v);
+  }
+}
+static int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+
+// ---------------------------------------------------------------------------
+// Plan
+// ---------------------------------------------------------------------------
+enum Segment { SEG_FULL = 0, SEG_INPUT = 1, SEG_OUTPUT = 2 };
+
+struct Operand {
+  const void* p;
+  int32_t dt;
+  int64_t s_m, s_c;  // element strides: token, feature
+};
+
+struct TmapKey {
+  const void* p;
+  int64_t k, rows, ld;
+  int box;
+  bool operator==(const TmapKey& o) const {
+    return p == o.p && k == o.k && rows == o.rows && ld == o.ld && box == o.box;
+  }
+};
+
+}  // namespace tnl
+
+struct tnl_plan {
+  int32_t family = 0, d = 0, rm = 0, compute_dtype = TNL_F32, flags = 0;
+  int64_t ms[TNL_MAX_MODES] = {0};
+  int64_t rk[TNL_MAX_MODES + 1] = {0};
+  int64_t rows = 0, cols = 0, row_begin = 0, row_end = 0;
+  int64_t r_cut = 0, r_pad = 0, param_count = 0;
+  int64_t chain_flops = 0, cut_flops = 0;
+  bool tucker_cut_in = true;  // Tucker: cut = prod R_in (else prod R_out)
+  int device = 0;
+  // device arena
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  // generic fp32 cores (device, permuted layouts; see build_steps)
+  std::vector<float*> gcore;  // TT/TR: per core; Tucker: [0]=core, [1+k]=factor k; dense: [0]
+  // bf16 tensor-core panels
+  __nv_bfloat16* bin = nullptr;   // (r_pad x cols)
+  __nv_bfloat16* aout = nullptr;  // (rows_local x r_pad)
+  __nv_bfloat16* u1t = nullptr;   // Tucker-2 chain: (R1p x cols)
+  __nv_bfloat16* gmat = nullptr;  //                 (R0p x R1p)
+  __nv_bfloat16* u0 = nullptr;    //                 (rows_local x R0p)
+  int64_t r0p = 0, r1p = 0;
+  __nv_bfloat16* wdense = nullptr;  // dense (rows_local x cols)
+  float* gen_w_out = nullptr;       // generic dense rows slice (fp32) for sharded generic plans
+  int32_t plan_large = TNL_PLAN_GENERIC, plan_small = TNL_PLAN_GENERIC;
+  int32_t decode_max_m = 0;
+  int64_t max_state = 0;  // generic chain: max intermediate elements per token
+  // host staging for tnl_forward_host
+  int64_t max_m = 0;
+  void* stage_x = nullptr;
+  void* stage_y = nullptr;
+  void* stage_ws = nullptr;
+  size_t stage_ws_bytes = 0;
+  // tensor-map cache
+  std::mutex tm_mu;
+  std::vector<std::pair<tnl::TmapKey, CUtensorMap>> tm_cache;
+};
+
+namespace tnl {
+
+// Returns 0 and fills *m (by value: cache entries may move on insertion).
+static int get_tmap(tnl_plan* P, CUtensorMap* m, const void* p, int64_t k, int64_t rows,
+                    int64_t ld, int box) {
+  TmapKey key{p, k, rows, ld, box};
+  std::lock_guard<std::mutex> g(P->tm_mu);
+  for (auto& e : P->tm_cache)
+    if (e.first == key) {
+      *m = e.second;
+      return 0;
+    }
+  int err = make_tmap_bf16(m, p, k, rows, ld, box);
+  if (err) return err;
+  if (P->tm_cache.size() >= 64) P->tm_cache.erase(P->tm_cache.begin());
+  P->tm_cache.emplace_back(key, *m);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Validation: tn_decompositions.py:97-126 (same checks, same messages)
+// ---------------------------------------------------------------------------
+static tnl_status validate_desc(const tnl_layer_desc* L) {
+  if (!L) return fail(TNL_ERR_ARG, "null layer descriptor");
+  const int d = L->ndim;
+  if (d < 2 || d > TNL_MAX_MODES)
+    return fail(TNL_ERR_SHAPE, "mode shape length must be in [2, %d], got %d", TNL_MAX_MODES, d);
+  for (int k = 0; k < d; ++k)
+    if (L->mode_shape[k] < 1)
+      return fail(TNL_ERR_SHAPE, "all mode sizes must be >= 1, got %lld",
+                  (long long)L->mode_shape[k]);
+  if (!(1 <= L->row_mode_count && L->row_mode_count < d))
+    return fail(TNL_ERR_SHAPE, "row_mode_count %d invalid for %d modes", L->row_mode_count, d);
+  if (L->src_dtype != TNL_F64 && L->src_dtype != TNL_F32 && L->src_dtype != TNL_BF16)
+    return fail(TNL_ERR_ARG, "unknown source dtype %d", L->src_dtype);
+  switch (L->family) {
+    case TNL_FAMILY_DENSE:
+      if (!L->arrays[0]) return fail(TNL_ERR_SHAPE, "dense layer must hold its matricized payload");
+      break;
+    case TNL_FAMILY_TUCKER:
+      if (!L->arrays[0]) return fail(TNL_ERR_SHAPE, "tucker layer needs a core and one factor per mode");
+      for (int k = 0; k < d; ++k) {
+        if (!L->arrays[1 + k])
+          return fail(TNL_ERR_SHAPE, "tucker layer needs a core and one factor per mode");
+        if (L->ranks[k] < 1) return fail(TNL_ERR_RANK, "ranks must be >= 1");
+      }
+      break;
+    case TNL_FAMILY_TT:
+    case TNL_FAMILY_TR:
+      for (int k = 0; k < d; ++k) {
+        if (!L->arrays[k]) return fail(TNL_ERR_SHAPE, "%s layer needs %d cores",
+                                       L->family == TNL_FAMILY_TT ? "tt" : "tr", d);
+        if (L->ranks[k] < 1 || L->ranks[k + 1] < 1) return fail(TNL_ERR_RANK, "ranks must be >= 1");
+      }
+      if (L->family == TNL_FAMILY_TT && (L->ranks[0] != 1 || L->ranks[d] != 1))
+        return fail(TNL_ERR_SHAPE, "tt boundary ranks must be 1");
+      if (L->family == TNL_FAMILY_TR && L->ranks[d] != L->ranks[0])
+        return fail(TNL_ERR_SHAPE, "tr closing bond mismatch");
+      break;
+    default:
+      return fail(TNL_ERR_SHAPE, "unknown family %d", L->family);
+  }
+  return TNL_OK;
+}
+
+// host conversion of one source array to float (with optional bf16 rounding)
+static float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+static void load_host(const tnl_layer_desc* L, int idx, int64_t n, bool round, std::vector<float>& out) {
+  out.resize(n);
+  const void* src = L->arrays[idx];
+  for (int64_t e = 0; e < n; ++e) {
+    float v;
+    if (L->src_dtype == TNL_F64)
+      v = (float)static_cast<const double*>(src)[e];
+    else if (L->src_dtype == TNL_F32)
+      v = static_cast<const float*>(src)[e];
+    else {
+      uint16_t b = static_cast<const uint16_t*>(src)[e];
+      uint32_t u = (uint32_t)b << 16;
+      memcpy(&v, &u, 4);
+    }
+    out[e] = round ? bf16_round(v) : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic chain step construction (torch orientation, token-major states)
+// ---------------------------------------------------------------------------
+struct ChainIO {
+  Operand in;   // x (FULL/INPUT) or cut state (OUTPUT)
+  Operand out;  // y (FULL/OUTPUT) or cut state (INPUT)
+  float* ws[2];
+};
+
+static GStep mk(int64_t b1, int64_t b2, int64_t I, int64_t P, int64_t J) {
+  GStep s;
+  memset(&s, 0, sizeof s);
+  s.b1 = b1;
+  s.b2 = b2;
+  s.I = I;
+  s.P = P;
+  s.J = J;
+  s.a_dt = s.b_dt = s.c_dt = DT_F32;
+  return s;
+}
+
+// States (per token), TT/TR with closure size r0 (1 for TT):
+//   input after core k : [alpha][pre(k)][b_k]        pre(k) = prod ms[rm..k-1]
+//   cut                : [alpha][b_rm]   (kappa = alpha*b_rm + b)
+//   output after core k: [alpha][a_k][post(k)]       post(k) = prod ms[k..rm-1]
+//   y                  : [i_0][post(1)]
+// Device core layouts (gcore): last core permuted to [alpha][j][c]; core 0
+// permuted to [i0][(alpha, a)]; the others natural (b, n, c).
+static void steps_ttr(const tnl_plan* P, int seg, int64_t M, const ChainIO& io,
+                      std::vector<GStep>& out) {
+  const int d = P->d, rm = P->rm;
+  const int64_t* ms = P->ms;
+  const int64_t* r = P->rk;  // bonds: core k is (r[k], ms[k], r[k+1])
+  const int64_t r0 = r[0];
+  int wsi = 0;
+  // current state operand description
+  const void* cur = nullptr;
+  int cur_dt = DT_F32;
+  auto next_ws = [&]() { float* p = io.ws[wsi]; wsi ^= 1; return p; };
+  if (seg == SEG_FULL || seg == SEG_INPUT) {
+    // k = d-1: state[m][alpha][pre][c] = sum_j x[m][pre][j] D[c][j][alpha]
+    {
+      const int k = d - 1;
+      const int64_t pre = prod(ms, rm, k), n = ms[k], c = r[k];
+      GStep s = mk(M, r0, pre, n, c);
+      s.A = io.in.p;
+      s.a_dt = io.in.dt;
+      s.sa1 = io.in.s_m;
+      s.sa2 = 0;
+      s.sai = n * io.in.s_c;
+      s.sap = io.in.s_c;
+      s.B = P->gcore[k];
+      s.sb1 = 0;
+      s.sb2 = n * c;
+      s.sbp = c;
+      s.sbj = 1;
+      const bool last = (k == rm) && seg == SEG_INPUT;
+      if (last) {  // cut state [alpha][c] -> out operand kappa = alpha*c + b
+        s.C = const_cast<void*>(io.out.p);
+        s.c_dt = io.out.dt;
+        s.sc1 = io.out.s_m;
+        s.sc2 = c * io.out.s_c;
+        s.sci = 0;
+        s.scj = io.out.s_c;
+      } else {
+        float* w = next_ws();
+        s.C = w;
+        s.sc1 = r0 * pre * c;
+        s.sc2 = pre * c;
+        s.sci = c;
+        s.scj = 1;
+        cur = w;
+      }
+      out.push_back(s);
+    }
+    for (int k = d - 2; k >= rm; --k) {
+      const int64_t pre = prod(ms, rm, k), n = ms[k], c = r[k + 1], b = r[k];
+      GStep s = mk(M, r0, pre, n * c, b);
+      s.A = cur;
+      s.a_dt = DT_F32;
+      s.sa1 = r0 * pre * n * c;
+      s.sa2 = pre * n * c;
+      s.sai = n * c;
+      s.sap = 1;
+      s.B = P->gcore[k];
+      s.sbp = 1;
+      s.sbj = n * c;
+      const bool last = (k == rm) && seg == SEG_INPUT;
+      if (last) {
+        s.C = const_cast<void*>(io.out.p);
+        s.c_dt = io.out.dt;
+        s.sc1 = io.out.s_m;
+        s.sc2 = b * io.out.s_c;
+        s.sci = 0;
+        s.scj = io.out.s_c;
+      } else {
+        float* w = next_ws();
+        s.C = w;
+        s.sc1 = r0 * pre * b;
+        s.sc2 = pre * b;
+        s.sci = b;
+        s.scj = 1;
+        cur = w;
+      }
+      out.push_back(s);
+    }
+    if (seg == SEG_INPUT) return;
+  }
+  // output side; state [m][alpha][a][post], cut has a = r[rm], post = 1
+  int64_t a = r[rm], post = 1;
+  int64_t s_m, s_alpha, s_a, s_post;
+  if (seg == SEG_OUTPUT) {
+    cur = io.in.p;
+    cur_dt = io.in.dt;
+    s_m = io.in.s_m;
+    s_alpha = a * io.in.s_c;
+    s_a = io.in.s_c;
+    s_post = 0;
+  } else {
+    cur_dt = DT_F32;
+    s_m = r0 * a;
+    s_alpha = a;
+    s_a = 1;
+    s_post = 0;
+  }
+  for (int k = rm - 1; k >= 1; --k) {
+    const int64_t n = ms[k], ap = r[k];  // core (ap, n, a)
+    GStep s = mk(M, r0, ap * n, a, post);
+    s.A = P->gcore[k];
+    s.sai = a;
+    s.sap = 1;
+    s.B = cur;
+    s.b_dt = cur_dt;
+    s.sb1 = s_m;
+    s.sb2 = s_alpha;
+    s.sbp = s_a;
+    s.sbj = post > 1 ? s_post : 1;
+    float* w = next_ws();
+    s.C = w;
+    s.sc1 = r0 * ap * n * post;
+    s.sc2 = ap * n * post;
+    s.sci = post;
+    s.scj = 1;
+    out.push_back(s);
+    cur = w;
+    cur_dt = DT_F32;
+    post *= n;
+    a = ap;
+    s_m = r0 * a * post;
+    s_alpha = a * post;
+    s_a = post;
+    s_post = 1;
+  }
+  // core 0: y[m][i0][post] = sum_{(alpha,a)} G0p[i0][(alpha,a)] U[m][alpha][a][post]
+  {
+    const int64_t n0 = ms[0];
+    GStep s = mk(M, 1, n0, r0 * a, post);
+    s.A = P->gcore[0];
+    s.sai = r0 * a;
+    s.sap = 1;
+    s.B = cur;
+    s.b_dt = cur_dt;
+    s.sb1 = s_m;
+    s.sbp = s_a;  // (alpha, a) composite: alpha stride == a * s_a
+    s.sbj = post > 1 ? s_post : 1;
+    s.C = const_cast<void*>(io.out.p);
+    s.c_dt = io.out.dt;
+    s.sc1 = io.out.s_m;
+    s.sci = post * io.out.s_c;
+    s.scj = io.out.s_c;
+    out.push_back(s);
+  }
+}
+
+// Tucker: factors U_k (n_k x R_k), core G (R_0..R_{d-1}) as (Rout x Rin).
+static void steps_tucker(const tnl_plan* P, int seg, int64_t M, const ChainIO& io,
+                         std::vector<GStep>& out) {
+  const int d = P->d, rm = P->rm;
+  const int64_t* ms = P->ms;
+  const int64_t* R = P->rk;
+  const int64_t Rin = prod(R, rm, d), Rout = prod(R, 0, rm);
+  int wsi = 0;
+  auto next_ws = [&]() { float* p = io.ws[wsi]; wsi ^= 1; return p; };
+  const bool cut_in = P->tucker_cut_in;
+  // state description: [m][dims...] contiguous per token, with feature stride sf
+  const void* cur = nullptr;
+  int cur_dt = DT_F32;
+  int64_t cur_sm = 0, cur_sf = 1;
+  const bool do_in = (seg == SEG_FULL || seg == SEG_INPUT);
+  const bool do_core = seg == SEG_FULL || (seg == SEG_INPUT && !cut_in) || (seg == SEG_OUTPUT && cut_in);
+  const bool do_out = (seg == SEG_FULL || seg == SEG_OUTPUT);
+  // which step is the final one of this segment
+  int total = (do_in ? d - rm : 0) + (do_core ? 1 : 0) + (do_out ? rm : 0);
+  int idx = 0;
+  if (seg == SEG_OUTPUT || !do_in) {
+    cur = io.in.p;
+    cur_dt = io.in.dt;
+    cur_sm = io.in.s_m;
+    cur_sf = io.in.s_c;
+  } else {
+    cur = io.in.p;
+    cur_dt = io.in.dt;
+    cur_sm = io.in.s_m;
+    cur_sf = io.in.s_c;
+  }
+  auto dst = [&](GStep& s, int64_t per_token) {
+    ++idx;
+    if (idx == total) {
+      s.C = const_cast<void*>(io.out.p);
+      s.c_dt = io.out.dt;
+      return std::make_pair(io.out.s_m, io.out.s_c);
+    }
+    float* w = next_ws();
+    s.C = w;
+    s.c_dt = DT_F32;
+    return std::make_pair(per_token, (int64_t)1);
+  };
+  if (do_in) {
+    // state[m][pre_n][n_k][post_R] -> [m][pre_n][R_k][post_R], k = d-1 .. rm
+    for (int k = d - 1; k >= rm; --k) {
+      const int64_t pre = prod(ms, rm, k), n = ms[k], Rk = R[k], post = prod(R, k + 1, d);
+      GStep s = mk(M, pre, Rk, n, post);
+      s.A = P->gcore[1 + k];
+      s.sai = 1;
+      s.sap = Rk;  // A[i=R][p=j] = U[j][R]
+      s.B = cur;
+      s.b_dt = cur_dt;
+      s.sb1 = cur_sm;
+      s.sb2 = n * post * cur_sf;
+      s.sbp = post * cur_sf;
+      s.sbj = cur_sf;
+      auto o = dst(s, pre * Rk * post);
+      s.sc1 = o.first;
+      s.sc2 = Rk * post * o.second;
+      s.sci = post * o.second;
+      s.scj = o.second;
+      out.push_back(s);
+      cur = s.C;
+      cur_dt = s.c_dt;
+      cur_sm = o.first;
+      cur_sf = o.second;
+    }
+  }
+  if (do_core) {
+    GStep s = mk(1, 1, M, Rin, Rout);
+    s.A = cur;
+    s.a_dt = cur_dt;
+    s.sai = cur_sm;
+    s.sap = cur_sf;
+    s.B = P->gcore[0];
+    s.sbp = 1;
+    s.sbj = Rin;
+    auto o = dst(s, Rout);
+    s.sci = o.first;
+    s.scj = o.second;
+    out.push_back(s);
+    cur = s.C;
+    cur_dt = s.c_dt;
+    cur_sm = o.first;
+    cur_sf = o.second;
+  }
+  if (do_out) {
+    for (int k = 0; k < rm; ++k) {
+      const int64_t pre = prod(ms, 0, k), n = ms[k], Rk = R[k], post = prod(R, k + 1, rm);
+      GStep s = mk(M, pre, n, Rk, post);
+      s.A = P->gcore[1 + k];
+      s.sai = Rk;
+      s.sap = 1;
+      s.B = cur;
+      s.b_dt = cur_dt;
+      s.sb1 = cur_sm;
+      s.sb2 = Rk * post * cur_sf;
+      s.sbp = post * cur_sf;
+      s.sbj = cur_sf;
+      auto o = dst(s, pre * n * post);
+      s.sc1 = o.first;
+      s.sc2 = n * post * o.second;
+      s.sci = post * o.second;
+      s.scj = o.second;
+      out.push_back(s);
+      cur = s.C;
+      cur_dt = s.c_dt;
+      cur_sm = o.first;
+      cur_sf = o.second;
+    }
+  }
+}
+
+static void steps_dense(const tnl_plan* P, int64_t M, const ChainIO& io, std::vector<GStep>& out) {
+  GStep s = mk(1, 1, M, P->cols, P->rows);
+  s.A = io.in.p;
+  s.a_dt = io.in.dt;
+  s.sai = io.in.s_m;
+  s.sap = io.in.s_c;
+  s.B = P->gcore[0];
+  s.sbp = 1;
+  s.sbj = P->cols;
+  s.C = const_cast<void*>(io.out.p);
+  s.c_dt = io.out.dt;
+  s.sci = io.out.s_m;
+  s.scj = io.out.s_c;
+  out.push_back(s);
+}
+
+static void build_steps(const tnl_plan* P, int seg, int64_t M, const ChainIO& io,
+                        std::vector<GStep>& out) {
+  if (P->family == TNL_FAMILY_TT || P->family == TNL_FAMILY_TR)
+    steps_ttr(P, seg, M, io, out);
+  else if (P->family == TNL_FAMILY_TUCKER)
+    steps_tucker(P, seg, M, io, out);
+  else
+    steps_dense(P, M, io, out);
+}
+
+static int64_t max_state_per_token(const tnl_plan* P) {
+  const int d = P->d, rm = P->rm;
+  const int64_t* ms = P->ms;
+  const int64_t* r = P->rk;
+  int64_t mx = 1;
+  if (P->family == TNL_FAMILY_TT || P->family == TNL_FAMILY_TR) {
+    const int64_t r0 = r[0];
+    for (int k = d - 1; k >= rm; --k) mx = std::max(mx, r0 * prod(ms, rm, k) * r[k]);
+    int64_t post = 1;
+    for (int k = rm - 1; k >= 1; --k) {
+      post *= ms[k];
+      mx = std::max(mx, r0 * r[k] * post);
+    }
+  } else if (P->family == TNL_FAMILY_TUCKER) {
+    for (int k = d - 1; k >= rm; --k) mx = std::max(mx, prod(ms, rm, k) * prod(r, k, d));
+    mx = std::max(mx, prod(r, 0, rm));
+    for (int k = 0; k < rm; ++k) mx = std::max(mx, prod(ms, 0, k + 1) * prod(r, k + 1, rm));
+  }
+  return mx;
+}
+
+static int run_steps(const std::vector<GStep>& steps, cudaStream_t st) {
+  for (const auto& s : steps) {
+    int e = launch_generic_step(s, st);
+    if (e) return e;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Flop accounting (SPEC.md:465-473 currency; SURVEY App. A canonical order)
+// ---------------------------------------------------------------------------
+static int64_t chain_flops(const tnl_plan* P) {
+  const int d = P->d, rm = P->rm;
+  const int64_t* ms = P->ms;
+  const int64_t* r = P->rk;
+  int64_t f = 0;
+  if (P->family == TNL_FAMILY_DENSE) return 2 * P->rows * P->cols;
+  if (P->family == TNL_FAMILY_TUCKER) {
+    std::vector<int64_t> cur(ms + rm, ms + d);
+    for (int k = d - 1; k >= rm; --k) {
+      int64_t p = 1;
+      for (auto v : cur) p *= v;
+      f += 2 * p * r[k];
+      cur[k - rm] = r[k];
+    }
+    f += 2 * prod(r, 0, rm) * prod(r, rm, d);
+    std::vector<int64_t> c2(r, r + rm);
+    for (int k = 0; k < rm; ++k) {
+      int64_t p = 1;
+      for (auto v : c2) p *= v;
+      f += 2 * p * ms[k];
+      c2[k] = ms[k];
+    }
+    return f;
+  }
+  const int64_t r0 = r[0];
+  for (int k = rm; k < d; ++k) {
+    int64_t mult = (k != d - 1 && r0 > 1) ? r0 : 1;
+    f += 2 * prod(ms, rm, k) * ms[k] * r[k + 1] * r[k] * mult;
+  }
+  for (int k = 0; k < rm; ++k) {
+    int64_t mult = (k != 0 && r0 > 1) ? r0 : 1;
+    f += 2 * prod(ms, k + 1, rm) * r[k + 1] * ms[k] * r[k] * mult;
+  }
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// Device-side panel construction (fp32 generic steps on identity inputs)
+// ---------------------------------------------------------------------------
+static tnl_status alloc_arena(tnl_plan* P, size_t bytes) {
+  CUDA_TRY(cudaMalloc(&P->arena, bytes));
+  P->arena_bytes = bytes;
+  CUDA_TRY(cudaMemset(P->arena, 0, bytes));
+  return TNL_OK;
+}
+
+// Computes the fp32 (rows_out x K) matrix  OUT[i][kappa] for SEG_OUTPUT
+// (A_out restricted to [row_begin,row_end)) or OUT[kappa][j] for SEG_INPUT (B_in),
+// by running the segment's chain on identity inputs in chunks.
+static tnl_status build_panel_f32(tnl_plan* P, int seg, float* out, cudaStream_t st) {
+  const int64_t K = P->r_cut;
+  const int64_t n_in = (seg == SEG_INPUT) ? P->cols : K;       // identity size
+  const int64_t chunk = std::min<int64_t>(n_in, 512);
+  float *eye = nullptr, *ws0 = nullptr, *ws1 = nullptr, *tmp = nullptr;
+  const int64_t ms_tok = std::max<int64_t>(max_state_per_token(P), 1);
+  const int64_t out_feats = (seg == SEG_INPUT) ? K : P->rows;
+  CUDA_TRY(cudaMalloc(&eye, sizeof(float) * chunk * n_in));
+  CUDA_TRY(cudaMalloc(&ws0, sizeof(float) * chunk * ms_tok));
+  CUDA_TRY(cudaMalloc(&ws1, sizeof(float) * chunk * ms_tok));
+  CUDA_TRY(cudaMalloc(&tmp, sizeof(float) * chunk * out_feats));
+  tnl_status st_ret = TNL_OK;
+  for (int64_t c0 = 0; c0 < n_in && st_ret == TNL_OK; c0 += chunk) {
+    const int64_t m = std::min(chunk, n_in - c0);
+    identity_f32<<<grid_for(m * n_in), 256, 0, st>>>(eye, m, n_in, c0);
+    ChainIO io;
+    io.in = Operand{eye, DT_F32, n_in, 1};
+    io.out = Operand{tmp, DT_F32, out_feats, 1};
+    io.ws[0] = ws0;
+    io.ws[1] = ws1;
+    std::vector<GStep> steps;
+    build_steps(P, seg, m, io, steps);
+    if (run_steps(steps, st)) st_ret = fail(TNL_ERR_CUDA, "panel build launch failed");
+    // tmp[mm][f]: SEG_INPUT -> B_in[f][c0+mm]; SEG_OUTPUT -> A_out[f-row_begin][c0+mm]
+    if (seg == SEG_INPUT) {
+      copy_2d_any<<<grid_for(m * K), 256, 0, st>>>(tmp, DT_F32, K, 1, out + c0, DT_F32, 1, P->cols,
+                                                   m, K);
+    } else {
+      const int64_t nr = P->row_end - P->row_begin;
+      copy_2d_any<<<grid_for(m * nr), 256, 0, st>>>(tmp + P->row_begin, DT_F32, P->rows, 1,
+                                                    out + c0, DT_F32, 1, K, m, nr);
+    }
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(eye);
+  cudaFree(ws0);
+  cudaFree(ws1);
+  cudaFree(tmp);
+  if (st_ret == TNL_OK) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(TNL_ERR_CUDA, "panel build: %s", cudaGetErrorString(e));
+  }
+  return st_ret;
+}
+
+// ---------------------------------------------------------------------------
+// tnl_plan_create
+// ---------------------------------------------------------------------------
+static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, int64_t max_m,
+                              int32_t flags, int64_t row_begin, int64_t row_end, tnl_plan** out) {
+  if (!out) return fail(TNL_ERR_ARG, "null output pointer");
+  *out = nullptr;
+  tnl_status vs = validate_desc(L);
+  if (vs != TNL_OK) return vs;
+  if (compute_dtype != TNL_F32 && compute_dtype != TNL_BF16)
+    return fail(TNL_ERR_ARG, "compute dtype must be TNL_F32 or TNL_BF16");
+  std::unique_ptr<tnl_plan> P(new tnl_plan());
+  P->family = L->family;
+  P->d = L->ndim;
+  P->rm = L->row_mode_count;
+  P->compute_dtype = compute_dtype;
+  P->flags = flags;
+  for (int k = 0; k < P->d; ++k) P->ms[k] = L->mode_shape[k];
+  for (int k = 0; k <= P->d; ++k) P->rk[k] = L->ranks[k];
+  const int d = P->d, rm = P->rm;
+  P->rows = prod(P->ms, 0, rm);
+  P->cols = prod(P->ms, rm, d);
+  if (row_begin == 0 && row_end == 0) row_end = P->rows;
+  if (!(0 <= row_begin && row_begin < row_end && row_end <= P->rows))
+    return fail(TNL_ERR_SHAPE, "row range [%lld, %lld) outside %lld rows", (long long)row_begin,
+                (long long)row_end, (long long)P->rows);
+  P->row_begin = row_begin;
+  P->row_end = row_end;
+  CUDA_TRY(cudaGetDevice(&P->device));
+  const bool bf16 = compute_dtype == TNL_BF16;
+  const int64_t* ms = P->ms;
+  const int64_t* r = P->rk;
+
+  // ---- load cores to host fp32, permute into generic layouts ----
+  std::vector<std::vector<float>> host;  // generic layouts
+  int64_t pc = 0;
+  if (P->family == TNL_FAMILY_DENSE) {
+    std::vector<float> w;
+    load_host(L, 0, P->rows * P->cols, bf16, w);
+    pc = P->rows * P->cols;
+    host.push_back(std::move(w));
+    P->r_cut = std::min(P->rows, P->cols);
+  } else if (P->family == TNL_FAMILY_TUCKER) {
+    std::vector<float> g;
+    load_host(L, 0, prod(r, 0, d), bf16, g);
+    pc += (int64_t)g.size();
+    host.push_back(std::move(g));
+    for (int k = 0; k < d; ++k) {
+      std::vector<float> u;
+      load_host(L, 1 + k, ms[k] * r[k], bf16, u);
+      pc += (int64_t)u.size();
+      host.push_back(std::move(u));
+    }
+    const int64_t Rin = prod(r, rm, d), Rout = prod(r, 0, rm);
+    P->tucker_cut_in = Rin <= Rout;
+    P->r_cut = std::min(Rin, Rout);
+  } else {
+    const int64_t r0 = r[0];
+    for (int k = 0; k < d; ++k) {
+      std::vector<float> c;
+      const int64_t a = r[k], n = ms[k], b = r[k + 1];
+      load_host(L, k, a * n * b, bf16, c);
+      pc += (int64_t)c.size();
+      if (k == d - 1) {  // [alpha][j][c] = D[c][j][alpha]
+        std::vector<float> p(c.size());
+        for (int64_t cc = 0; cc < a; ++cc)
+          for (int64_t j = 0; j < n; ++j)
+            for (int64_t al = 0; al < b; ++al) p[(al * n + j) * a + cc] = c[(cc * n + j) * b + al];
+        c.swap(p);
+      } else if (k == 0) {  // [i0][(alpha, a)] = G0[alpha][i0][a]
+        std::vector<float> p(c.size());
+        for (int64_t al = 0; al < a; ++al)
+          for (int64_t i = 0; i < n; ++i)
+            for (int64_t aa = 0; aa < b; ++aa) p[i * (a * b) + al * b + aa] = c[(al * n + i) * b + aa];
+        c.swap(p);
+      }
+      host.push_back(std::move(c));
+    }
+    // d == 1 never (d >= 2). If d-1 == 0 impossible.
+    P->r_cut = r0 * r[rm];
+  }
+  P->param_count = pc;
+  P->chain_flops = chain_flops(P.get());
+  P->cut_flops = 2 * P->r_cut * (P->rows + P->cols);
+  P->max_state = max_state_per_token(P.get());
+  P->r_pad = round_up(P->r_cut, 16);
+
+  // ---- choose plans ----
+  const bool tc_ok = bf16 && (P->cols % 8 == 0) && !(flags & TNL_PLAN_GENERIC);
+  const int64_t rows_local = P->row_end - P->row_begin;
+  const bool tucker2 = P->family == TNL_FAMILY_TUCKER && d == 2;
+  int32_t large = TNL_PLAN_GENERIC;
+  if (tc_ok) {
+    if (P->family == TNL_FAMILY_DENSE)
+      large = TNL_PLAN_CUT;  // single GEMM (W plays A_out, identity cut)
+    else if ((flags & TNL_PLAN_CHAIN) && tucker2)
+      large = TNL_PLAN_CHAIN;
+    else
+      large = TNL_PLAN_CUT;
+  }
+  P->plan_large = large;
+  P->plan_small = large;
+  P->decode_max_m = 0;
+
+  // ---- device arena: generic cores + panels ----
+  size_t bytes = 0;
+  std::vector<size_t> off;
+  for (auto& h : host) {
+    off.push_back(bytes);
+    bytes += round_up((int64_t)h.size() * 4, 256);
+  }
+  size_t off_bin = 0, off_aout = 0, off_u1 = 0, off_g = 0, off_u0 = 0, off_w = 0;
+  const bool dense = P->family == TNL_FAMILY_DENSE;
+  if (large == TNL_PLAN_CUT && !dense) {
+    off_bin = bytes;
+    bytes += round_up(P->r_pad * P->cols * 2, 256);
+    off_aout = bytes;
+    bytes += round_up(rows_local * P->r_pad * 2, 256);
+  }
+  if (large == TNL_PLAN_CUT && dense) {
+    off_w = bytes;
+    bytes += round_up(rows_local * P->cols * 2, 256);
+  }
+  if (large == TNL_PLAN_CHAIN) {
+    P->r1p = round_up(r[1], 16);
+    P->r0p = round_up(r[0], 16);
+    off_u1 = bytes;
+    bytes += round_up(P->r1p * P->cols * 2, 256);
+    off_g = bytes;
+    bytes += round_up(P->r0p * P->r1p * 2, 256);
+    off_u0 = bytes;
+    bytes += round_up(rows_local * P->r0p * 2, 256);
+  }
+  tnl_status as = alloc_arena(P.get(), bytes);
+  if (as != TNL_OK) return as;
+  char* base = static_cast<char*>(P->arena);
+  for (size_t i = 0; i < host.size(); ++i) {
+    float* dptr = reinterpret_cast<float*>(base + off[i]);
+    CUDA_TRY(cudaMemcpy(dptr, host[i].data(), host[i].size() * 4, cudaMemcpyHostToDevice));
+    P->gcore.push_back(dptr);
+  }
+  cudaStream_t st = 0;
+  if (large == TNL_PLAN_CUT && dense) {
+    P->wdense = reinterpret_cast<__nv_bfloat16*>(base + off_w);
+    copy_2d_any<<<grid_for(rows_local * P->cols), 256, 0, st>>>(
+        P->gcore[0] + P->row_begin * P->cols, DT_F32, P->cols, 1, P->wdense, DT_BF16, P->cols, 1,
+        rows_local, P->cols);
+  } else if (large == TNL_PLAN_CUT) {
+    P->bin = reinterpret_cast<__nv_bfloat16*>(base + off_bin);
+    P->aout = reinterpret_cast<__nv_bfloat16*>(base + off_aout);
+    float *fb = nullptr, *fa = nullptr;
+    CUDA_TRY(cudaMalloc(&fb, sizeof(float) * P->r_cut * P->cols));
+    CUDA_TRY(cudaMalloc(&fa, sizeof(float) * rows_local * P->r_cut));
+    tnl_status s1 = build_panel_f32(P.get(), SEG_INPUT, fb, st);
+    tnl_status s2 = s1 == TNL_OK ? build_panel_f32(P.get(), SEG_OUTPUT, fa, st) : s1;
+    if (s2 == TNL_OK) {
+      copy_2d_any<<<grid_for(P->r_cut * P->cols), 256, 0, st>>>(fb, DT_F32, P->cols, 1, P->bin,
+                                                                DT_BF16, P->cols, 1, P->r_cut,
+                                                                P->cols);
+      copy_2d_any<<<grid_for(rows_local * P->r_cut), 256, 0, st>>>(
+          fa, DT_F32, P->r_cut, 1, P->aout, DT_BF16, P->r_pad, 1, rows_local, P->r_cut);
+    }
+    cudaStreamSynchronize(st);
+    cudaFree(fb);
+    cudaFree(fa);
+    if (s2 != TNL_OK) return s2;
+  } else if (large == TNL_PLAN_CHAIN) {
+    // Tucker-2: U1^T (R1p x cols), G (R0p x R1p), U0 rows (rows_local x R0p)
+    P->u1t = reinterpret_cast<__nv_bfloat16*>(base + off_u1);
+    P->gmat = reinterpret_cast<__nv_bfloat16*>(base + off_g);
+    P->u0 = reinterpret_cast<__nv_bfloat16*>(base + off_u0);
+    copy_2d_any<<<grid_for(r[1] * P->cols), 256, 0, st>>>(P->gcore[2], DT_F32, 1, r[1], P->u1t,
+                                                          DT_BF16, P->cols, 1, r[1], P->cols);
+    copy_2d_any<<<grid_for(r[0] * r[1]), 256, 0, st>>>(P->gcore[0], DT_F32, r[1], 1, P->gmat,
+                                                       DT_BF16, P->r1p, 1, r[0], r[1]);
+    copy_2d_any<<<grid_for(rows_local * r[0]), 256, 0, st>>>(
+        P->gcore[1] + P->row_begin * r[0], DT_F32, r[0], 1, P->u0, DT_BF16, P->r0p, 1, rows_local,
+        r[0]);
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+
+  // ---- host staging for tnl_forward_host ----
+  P->max_m = max_m;
+  if (max_m > 0) {
+    const size_t es = bf16 ? 2 : 4;
+    CUDA_TRY(cudaMalloc(&P->stage_x, es * max_m * P->cols));
+    CUDA_TRY(cudaMalloc(&P->stage_y, es * max_m * rows_local));
+  }
+  *out = P.release();
+  return TNL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+static constexpr int64_t kSwapMaxM = 64;  // tokens: swap-AB (weights on the M side) below this
+
+static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b0, size_t* o_b1) {
+  size_t bytes = 0;
+  auto take = [&](size_t n) {
+    size_t o = bytes;
+    bytes += round_up((int64_t)n, 256);
+    return o;
+  };
+  const int64_t rows_local = P->row_end - P->row_begin;
+  if (P->plan_large == TNL_PLAN_GENERIC) {
+    *o_b0 = take(sizeof(float) * M * P->max_state);
+    *o_b1 = take(sizeof(float) * M * P->max_state);
+    // sharded generic plans compute full rows into a temp y
+    *o_f32 = (rows_local != P->rows) ? take(sizeof(float) * M * P->rows) : 0;
+    return bytes;
+  }
+  int64_t kmax = P->r_pad;
+  if (P->plan_large == TNL_PLAN_CHAIN) kmax = std::max(P->r0p, P->r1p);
+  *o_f32 = take(sizeof(float) * M * kmax);
+  *o_b0 = take(2 * M * kmax);
+  *o_b1 = take(2 * M * kmax);
+  return bytes;
+}
+
+static int pick_bn(int64_t n) {
+  if (n <= 16) return 16;
+  if (n <= 32) return 32;
+  if (n <= 64) return 64;
+  if (n <= 128) return 128;
+  return 256;
+}
+
+// one tensor-core GEMM step, either orientation.
+//   normal : out[m][n] = sum_k X[m][k] W[n][k]   (X: tokens, M-side)
+//   swapped: same result, W on the M side (tokens on N) -> split-K fp32 atomics
+//            when out_f32 != nullptr, else direct bf16 store.
+static tnl_status tc_step(tnl_plan* P, const void* X, int64_t ldx, const void* W, int64_t ldw,
+                          int64_t M, int64_t N, int64_t K, void* out, int64_t ldo, bool out_f32,
+                          bool swapped, int splits, cudaStream_t st) {
+  int err = 0;
+  CUtensorMap ta, tb;
+  TcGemmArgs a;
+  a.K = (int32_t)K;
+  const int total_kb = (int)((K + 63) / 64);
+  if (!swapped) {
+    const int bn = pick_bn(N);
+    if ((err = get_tmap(P, &ta, X, K, M, ldx, 128)))
+      return fail(TNL_ERR_CUDA, "tensor map (activations) failed: %d", err);
+    if ((err = get_tmap(P, &tb, W, K, N, ldw, bn)))
+      return fail(TNL_ERR_CUDA, "tensor map (weights) failed: %d", err);
+    a.M = (int32_t)M;
+    a.N = (int32_t)N;
+    a.kb_per_split = (total_kb + splits - 1) / splits;
+    splits = (total_kb + a.kb_per_split - 1) / a.kb_per_split;
+    a.out = out;
+    a.ldo_i = ldo;
+    a.ldo_j = 1;
+    a.out_mode = out_f32 ? (splits > 1 ? TC_OUT_F32_ATOMIC : TC_OUT_F32) : TC_OUT_BF16;
+    err = launch_tc_gemm(ta, tb, a, bn, splits, true, st);
+  } else {
+    const int bn = pick_bn(M);
+    if ((err = get_tmap(P, &ta, W, K, N, ldw, 128)))
+      return fail(TNL_ERR_CUDA, "tensor map (weights) failed: %d", err);
+    if ((err = get_tmap(P, &tb, X, K, M, ldx, bn)))
+      return fail(TNL_ERR_CUDA, "tensor map (activations) failed: %d", err);
+    a.M = (int32_t)N;
+    a.N = (int32_t)M;
+    a.kb_per_split = (total_kb + splits - 1) / splits;
+    splits = (total_kb + a.kb_per_split - 1) / a.kb_per_split;
+    a.out = out;
+    a.ldo_i = 1;
+    a.ldo_j = ldo;
+    a.out_mode = out_f32 ? (splits > 1 ? TC_OUT_F32_ATOMIC : TC_OUT_F32) : TC_OUT_BF16;
+    err = launch_tc_gemm(ta, tb, a, bn, splits, true, st);
+  }
+  if (err) return fail(TNL_ERR_CUDA, "tc_gemm launch failed: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
+}
+
+// split count so that m_tiles * n_tiles * splits ~ one wave of 148 SMs
+static int choose_splits(int64_t tiles, int64_t K) {
+  const int64_t total_kb = (K + 63) / 64;
+  int64_t s = std::max<int64_t>(1, 148 / std::max<int64_t>(tiles, 1));
+  return (int)std::min<int64_t>(s, total_kb);
+}
+
+static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y, int64_t ldy,
+                             void* ws, size_t ws_bytes, cudaStream_t st) {
+  size_t o_f32, o_b0, o_b1;
+  size_t need = ws_layout(P, M, &o_f32, &o_b0, &o_b1);
+  if (ws_bytes < need) return fail(TNL_ERR_ARG, "workspace %zu < required %zu bytes", ws_bytes, need);
+  char* w = static_cast<char*>(ws);
+  float* tf = reinterpret_cast<float*>(w + o_f32);
+  __nv_bfloat16* t0 = reinterpret_cast<__nv_bfloat16*>(w + o_b0);
+  __nv_bfloat16* t1 = reinterpret_cast<__nv_bfloat16*>(w + o_b1);
+  const int64_t rows_local = P->row_end - P->row_begin;
+  const bool swap = M <= kSwapMaxM;
+  tnl_status s;
+  if (P->family == TNL_FAMILY_DENSE) {
+    return tc_step(P, x, ldx, P->wdense, P->cols, M, rows_local, P->cols, y, ldy, false, swap, 1, st);
+  }
+  // first step: T = X . Win^T  (Win = B_in or U1^T), K = cols
+  const __nv_bfloat16* win = P->plan_large == TNL_PLAN_CHAIN ? P->u1t : P->bin;
+  const int64_t k1 = P->plan_large == TNL_PLAN_CHAIN ? P->r1p : P->r_pad;
+  if (swap) {
+    const int64_t tiles = (k1 + 127) / 128;
+    const int splits = choose_splits(tiles, P->cols);
+    if (splits > 1) {
+      if (cudaMemsetAsync(tf, 0, sizeof(float) * M * k1, st) != cudaSuccess)
+        return fail(TNL_ERR_CUDA, "memset failed");
+      s = tc_step(P, x, ldx, win, P->cols, M, k1, P->cols, tf, k1, true, true, splits, st);
+      if (s) return s;
+      f32_to_bf16_2d<<<grid_for(M * k1), 256, 0, st>>>(tf, k1, t0, k1, M, k1);
+      count_launch();
+    } else {
+      s = tc_step(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, true, 1, st);
+      if (s) return s;
+    }
+  } else {
+    s = tc_step(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, false, 1, st);
+    if (s) return s;
+  }
+  const __nv_bfloat16* tcur = t0;
+  int64_t kc = k1;
+  if (P->plan_large == TNL_PLAN_CHAIN) {  // T2 = T1 . G^T   (R0p x R1p)
+    s = tc_step(P, t0, k1, P->gmat, P->r1p, M, P->r0p, P->r1p, t1, P->r0p, false, swap, 1, st);
+    if (s) return s;
+    tcur = t1;
+    kc = P->r0p;
+  }
+  const __nv_bfloat16* wout = P->plan_large == TNL_PLAN_CHAIN ? P->u0 : P->aout;
+  return tc_step(P, tcur, kc, wout, kc, M, rows_local, kc, y, ldy, false, swap, 1, st);
+}
+
+static tnl_status forward_generic(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y,
+                                  int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t st) {
+  size_t o_f32, o_b0, o_b1;
+  size_t need = ws_layout(P, M, &o_f32, &o_b0, &o_b1);
+  if (ws_bytes < need) return fail(TNL_ERR_ARG, "workspace %zu < required %zu bytes", ws_bytes, need);
+  char* w = static_cast<char*>(ws);
+  const int dt = P->compute_dtype == TNL_BF16 ? DT_BF16 : DT_F32;
+  const int64_t rows_local = P->row_end - P->row_begin;
+  ChainIO io;
+  io.in = Operand{x, dt, ldx, 1};
+  const bool sharded = rows_local != P->rows;
+  float* ytmp = reinterpret_cast<float*>(w + o_f32);
+  io.out = sharded ? Operand{ytmp, DT_F32, P->rows, 1} : Operand{y, dt, ldy, 1};
+  io.ws[0] = reinterpret_cast<float*>(w + o_b0);
+  io.ws[1] = reinterpret_cast<float*>(w + o_b1);
+  std::vector<GStep> steps;
+  build_steps(P, SEG_FULL, M, io, steps);
+  if (run_steps(steps, st)) return fail(TNL_ERR_CUDA, "generic step launch failed: %s",
+                                        cudaGetErrorString(cudaGetLastError()));
+  if (sharded) {
+    copy_2d_any<<<grid_for(M * rows_local), 256, 0, st>>>(ytmp + P->row_begin, DT_F32, P->rows, 1,
+                                                          y, dt, ldy, 1, M, rows_local);
+    count_launch();
+  }
+  return TNL_OK;
+}
+
+}  // namespace tnl
+
+using namespace tnl;
+
+extern "C" {
+
+int tnl_abi_version(void) { return TNL_ABI_VERSION; }
+const char* tnl_last_error(void) { return g_err.c_str(); }
+int64_t tnl_launch_count(int32_t reset) { return launch_count(reset != 0); }
+
+tnl_status tnl_plan_create(const tnl_layer_desc* desc, int32_t compute_dtype, int64_t max_m,
+                           int32_t flags, tnl_plan** out) {
+  return create_impl(desc, compute_dtype, max_m, flags, 0, 0, out);
+}
+
+tnl_status tnl_plan_create_rows(const tnl_layer_desc* desc, int32_t compute_dtype, int64_t max_m,
+                                int32_t flags, int64_t row_begin, int64_t row_end,
+                                tnl_plan** out) {
+  return create_impl(desc, compute_dtype, max_m, flags, row_begin, row_end, out);
+}
+
+tnl_status tnl_plan_destroy(tnl_plan* plan) {
+  if (!plan) return TNL_OK;
+  cudaFree(plan->arena);
+  cudaFree(plan->stage_x);
+  cudaFree(plan->stage_y);
+  cudaFree(plan->stage_ws);
+  delete plan;
+  return TNL_OK;
+}
+
+tnl_status tnl_plan_query(const tnl_plan* P, tnl_plan_info* info) {
+  if (!P || !info) return fail(TNL_ERR_ARG, "null argument");
+  memset(info, 0, sizeof *info);
+  info->rows = P->rows;
+  info->cols = P->cols;
+  info->r_cut = P->r_cut;
+  info->param_count = P->param_count;
+  info->chain_flops_per_token = P->chain_flops;
+  info->cut_flops_per_token = P->cut_flops;
+  info->dense_flops_per_token = 2 * P->rows * P->cols;
+  const int64_t es = P->compute_dtype == TNL_BF16 ? 2 : 4;
+  const int64_t rows_local = P->row_end - P->row_begin;
+  int64_t wb = P->param_count * es;
+  if (P->plan_large == TNL_PLAN_CUT && P->family != TNL_FAMILY_DENSE)
+    wb = es * P->r_cut * (P->cols + rows_local);
+  info->weight_bytes = wb;
+  info->decode_weight_bytes = wb;
+  info->compute_dtype = P->compute_dtype;
+  info->plan_large = P->plan_large;
+  info->plan_small = P->plan_small;
+  info->decode_max_m = P->decode_max_m;
+  info->row_begin = P->row_begin;
+  info->row_end = P->row_end;
+  return TNL_OK;
+}
+
+tnl_status tnl_workspace_size(const tnl_plan* P, int64_t m, size_t* bytes) {
+  if (!P || !bytes) return fail(TNL_ERR_ARG, "null argument");
+  if (m < 0) return fail(TNL_ERR_SHAPE, "negative token count");
+  size_t a, b, c;
+  *bytes = ws_layout(P, std::max<int64_t>(m, 1), &a, &b, &c);
+  return TNL_OK;
+}
+
+tnl_status tnl_forward(const tnl_plan* plan, const void* x, int64_t m, int64_t ldx, void* y,
+                       int64_t ldy, void* workspace, size_t workspace_bytes, void* stream) {
+  tnl_plan* P = const_cast<tnl_plan*>(plan);
+  if (!P) return fail(TNL_ERR_ARG, "null plan");
+  if (m < 0) return fail(TNL_ERR_SHAPE, "negative token count");
+  if (m == 0) return TNL_OK;
+  if (!x || !y) return fail(TNL_ERR_ARG, "null x or y");
+  if (ldx < P->cols) return fail(TNL_ERR_SHAPE, "ldx %lld < cols %lld", (long long)ldx, (long long)P->cols);
+  if (ldy < P->row_end - P->row_begin) return fail(TNL_ERR_SHAPE, "ldy too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (P->plan_large == TNL_PLAN_GENERIC)
+    return forward_generic(P, x, m, ldx, y, ldy, workspace, workspace_bytes, st);
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (ldx % 8))
+    return fail(TNL_ERR_SHAPE, "tensor-core plan needs 16-byte aligned x with ldx %% 8 == 0");
+  return forward_tc(P, x, m, ldx, y, ldy, workspace, workspace_bytes, st);
+}
+
+tnl_status tnl_forward_host(tnl_plan* P, const void* x_host, int64_t m, void* y_host, void* stream) {
+  if (!P || !x_host || !y_host) return fail(TNL_ERR_ARG, "null argument");
+  if (m <= 0 || m > P->max_m)
+    return fail(TNL_ERR_SHAPE, "m=%lld outside host staging capacity %lld", (long long)m,
+                (long long)P->max_m);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t es = P->compute_dtype == TNL_BF16 ? 2 : 4;
+  const int64_t rows_local = P->row_end - P->row_begin;
+  size_t need = 0;
+  tnl_status s = tnl_workspace_size(P, P->max_m, &need);
+  if (s) return s;
+  if (P->stage_ws_bytes < need) {
+    cudaFree(P->stage_ws);
+    P->stage_ws = nullptr;
+    CUDA_TRY(cudaMalloc(&P->stage_ws, need));
+    P->stage_ws_bytes = need;
+  }
+  CUDA_TRY(cudaMemcpyAsync(P->stage_x, x_host, es * m * P->cols, cudaMemcpyHostToDevice, st));
+  s = tnl_forward(P, P->stage_x, m, P->cols, P->stage_y, rows_local, P->stage_ws, P->stage_ws_bytes,
+                  stream);
+  if (s) return s;
+  CUDA_TRY(cudaMemcpyAsync(y_host, P->stage_y, es * m * rows_local, cudaMemcpyDeviceToHost, st));
+  return TNL_OK;
+}
+
+tnl_status tnl_reconstruct(const tnl_plan* plan, void* w, int64_t ldw, int32_t out_dtype, void* stream) {
+  tnl_plan* P = const_cast<tnl_plan*>(plan);
+  if (!P || !w) return fail(TNL_ERR_ARG, "null argument");
+  if (out_dtype != TNL_F32 && out_dtype != TNL_BF16) return fail(TNL_ERR_ARG, "bad out dtype");
+  const int64_t rows_local = P->row_end - P->row_begin;
+  if (ldw < P->cols) return fail(TNL_ERR_SHAPE, "ldw too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // W^T chunk = chain(identity chunk); written transposed into w.
+  const int64_t chunk = std::min<int64_t>(P->cols, 512);
+  float *eye = nullptr, *ws0 = nullptr, *ws1 = nullptr, *tmp = nullptr;
+  const int64_t mst = std::max<int64_t>(P->max_state, 1);
+  CUDA_TRY(cudaMalloc(&eye, sizeof(float) * chunk * P->cols));
+  CUDA_TRY(cudaMalloc(&ws0, sizeof(float) * chunk * mst));
+  CUDA_TRY(cudaMalloc(&ws1, sizeof(float) * chunk * mst));
+  CUDA_TRY(cudaMalloc(&tmp, sizeof(float) * chunk * P->rows));
+  tnl_status ret = TNL_OK;
+  const int odt = out_dtype == TNL_BF16 ? DT_BF16 : DT_F32;
+  for (int64_t c0 = 0; c0 < P->cols && ret == TNL_OK; c0 += chunk) {
+    const int64_t m = std::min(chunk, P->cols - c0);
+    identity_f32<<<grid_for(m * P->cols), 256, 0, st>>>(eye, m, P->cols, c0);
+    ChainIO io;
+    io.in = Operand{eye, DT_F32, P->cols, 1};
+    io.out = Operand{tmp, DT_F32, P->rows, 1};
+    io.ws[0] = ws0;
+    io.ws[1] = ws1;
+    std::vector<GStep> steps;
+    build_steps(P, SEG_FULL, m, io, steps);
+    if (run_steps(steps, st)) ret = fail(TNL_ERR_CUDA, "reconstruct launch failed");
+    // tmp[j][i] -> w[i - row_begin][c0 + j]
+    copy_2d_any<<<grid_for(m * rows_local), 256, 0, st>>>(tmp + P->row_begin, DT_F32, P->rows, 1,
+                                                          static_cast<char*>(w) +
+                                                              c0 * (odt == DT_BF16 ? 2 : 4),
+                                                          odt, 1, ldw, m, rows_local);
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(eye);
+  cudaFree(ws0);
+  cudaFree(ws1);
+  cudaFree(tmp);
+  if (ret == TNL_OK && e != cudaSuccess) ret = fail(TNL_ERR_CUDA, "reconstruct: %s", cudaGetErrorString(e));
+  return ret;
+}
+
+}  // extern "C"

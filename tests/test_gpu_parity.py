@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle (B200 only).
+
+Tolerances (BASELINE north_star): fp32 path rel-err <= 1e-5 against the
+float64 oracle; bf16 path rel-err <= 2e-2 against the float64 oracle evaluated
+on the same bf16-rounded cores and activations.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2602_01613_b200 as tnl
+from oracle import tn_oracle as O
+from tnl_testutil import golden_layer_kwargs
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 2e-2
+DEV = "cuda"
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(a))
+
+
+def to_layer(L: O.OracleLayer, round_bf16=False):
+    f = O.round_bf16 if round_bf16 else (lambda a: a)
+    kw = dict(family=L.family, mode_shape=L.mode_shape, row_mode_count=L.row_mode_count)
+    if L.family == "tucker":
+        kw["core"] = f(L.core)
+        kw["factors"] = [f(u) for u in L.factors]
+    elif L.family in ("tt", "tr"):
+        kw["cores"] = [f(c) for c in L.cores]
+    else:
+        kw["matrix"] = f(L.matrix)
+    return tnl.CompressedLayer(**kw), O.OracleLayer(**kw)
+
+
+def run(layer, x64, dtype, flags=tnl.PLAN_AUTO):
+    x = torch.tensor(x64, dtype=dtype, device=DEV)
+    y = layer.plan(dtype, flags=flags).forward(x)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy()
+
+
+def check_bf16(L64: O.OracleLayer, m: int, seed: int, flags=tnl.PLAN_AUTO, tol=BF16_TOL):
+    layer, Lr = to_layer(L64, round_bf16=True)
+    rows, cols = Lr.matrix_shape
+    x = O.round_bf16(O.synthetic_x(m, cols, seed))
+    y = run(layer, x, torch.bfloat16, flags)
+    ref = O.forward_torch_orient(Lr, x)
+    e = rel(ref, y)
+    assert e <= tol, (L64.family, L64.mode_shape, m, flags, e)
+    return e
+
+
+# --- golden fixtures (reference outputs) ------------------------------------
+
+
+def test_golden_fp32_generic(golden):
+    index, arrays = golden
+    for rec in index["forward"] + index["decomp"]:
+        layer = tnl.CompressedLayer(**golden_layer_kwargs(rec, arrays))
+        x, y = arrays[rec["x"]], arrays[rec["y"]]
+        out = run(layer, x.T, torch.float32, tnl.PLAN_GENERIC)
+        assert rel(y.T, out) <= FP32_TOL, (rec["family"], rec["mode_shape"], rel(y.T, out))
+
+
+@pytest.mark.parametrize("flags", [tnl.PLAN_AUTO, tnl.PLAN_CUT, tnl.PLAN_CHAIN, tnl.PLAN_GENERIC])
+def test_golden_bf16_plans(golden, flags):
+    index, arrays = golden
+    for rec in index["forward"] + index["decomp"]:
+        kw = golden_layer_kwargs(rec, arrays)
+        L = O.OracleLayer(**kw)
+        layer, Lr = to_layer(L, round_bf16=True)
+        x = O.round_bf16(arrays[rec["x"]].T)
+        out = run(layer, x, torch.bfloat16, flags)
+        ref = O.forward_torch_orient(Lr, x)
+        assert rel(ref, out) <= BF16_TOL, (rec["family"], rec["mode_shape"], flags, rel(ref, out))
+
+
+def test_golden_reconstruct(golden):
+    index, arrays = golden
+    for rec in index["forward"] + index["decomp"]:
+        if "w" not in rec:
+            continue
+        layer = tnl.CompressedLayer(**golden_layer_kwargs(rec, arrays))
+        w = tnl.reconstruct(layer).cpu().numpy()
+        assert w.shape == tuple(rec["mode_shape"])
+        assert rel(arrays[rec["w"]], w) <= 1e-6
+        m = tnl.layer_to_matrix(layer).cpu().numpy()
+        assert m.shape == tuple(layer.matrix_shape)
+        assert tnl.param_count(layer) == rec["param_count"]
+
+
+# --- BASELINE config shapes -------------------------------------------------------
+
+
+def test_cfg1_tt_fp32():
+    """cfg1: TT 4096->4096, (64,64|64,64) r32, M=16, fp32 (<= 1e-5)."""
+    L = O.synthetic_layer("tt", (64, 64, 64, 64), 2, (32, 32, 32), seed=10_000 + 100)
+    L32 = O.OracleLayer("tt", L.mode_shape, 2, cores=[c.astype(np.float32).astype(np.float64) for c in L.cores])
+    layer = tnl.CompressedLayer("tt", L.mode_shape, 2, cores=[c.astype(np.float32) for c in L.cores])
+    x = O.synthetic_x(16, 4096, seed=10_000 + 9_999).astype(np.float32).astype(np.float64)
+    ref = O.forward_torch_orient(L32, x)
+    for flags in (tnl.PLAN_AUTO, tnl.PLAN_GENERIC):
+        y = run(layer, x, torch.float32, flags)
+        assert rel(ref, y) <= FP32_TOL
+    # bf16 variant of cfg1
+    check_bf16(L, 16, seed=11)
+
+
+@pytest.mark.parametrize("R", [64, 128, 256])
+@pytest.mark.parametrize("m", [1, 7, 16, 64, 200])
+def test_cfg2_tucker2(R, m):
+    L = O.synthetic_layer("tucker", (5120, 5120), 1, (R, R), seed=20_000 + R)
+    for flags in (tnl.PLAN_AUTO, tnl.PLAN_CHAIN):
+        check_bf16(L, m, seed=20_000 + 9_999 + m, flags=flags)
+
+
+@pytest.mark.parametrize("ab", [(8, 8), (16, 16)])
+@pytest.mark.parametrize("m", [1, 16, 64])
+def test_cfg2_tr2(ab, m):
+    L = O.synthetic_layer("tr", (5120, 5120), 1, ab, seed=21_000 + ab[0])
+    check_bf16(L, m, seed=21_999 + m)
+
+
+@pytest.mark.parametrize("r", [8, 16])
+@pytest.mark.parametrize("m", [1, 16, 64, 129])
+def test_cfg2_tr4(r, m):
+    L = O.synthetic_layer("tr", (64, 80, 64, 80), 2, (r, r, r, r), seed=22_000 + r)
+    check_bf16(L, m, seed=22_999 + m)
+
+
+@pytest.mark.parametrize("which", ["gate", "down"])
+def test_cfg3_mlp_tt(which):
+    ms = (160, 160, 64, 80) if which == "gate" else (64, 80, 160, 160)
+    L = O.synthetic_layer("tt", ms, 2, (64, 64, 64), seed=30_000 + len(which))
+    check_bf16(L, 256, seed=30_999)
+
+
+def test_cfg3_full_size_properties():
+    """M=8192 prefill: token independence is bit-exact; sampled rows match the oracle."""
+    L = O.synthetic_layer("tt", (160, 160, 64, 80), 2, (64, 64, 64), seed=31_000)
+    layer, Lr = to_layer(L, round_bf16=True)
+    x = torch.randn(8192, 5120, device=DEV).to(torch.bfloat16)
+    p = layer.plan(torch.bfloat16)
+    y = p.forward(x)
+    idx = torch.tensor([0, 1, 127, 128, 4095, 8191], device=DEV)
+    y_sub = p.forward(x[idx[:3]].contiguous().repeat(40, 1))[:3]  # M=120 keeps the large-M orientation
+    assert torch.equal(y[idx[:3]], y_sub)
+    xs = x[idx].float().cpu().numpy().astype(np.float64)
+    ref = O.forward_torch_orient(Lr, xs)
+    assert rel(ref, y[idx].float().cpu().numpy()) <= BF16_TOL
+    # linearity: f(2x) == 2 f(x) exactly in bf16 (power-of-two scaling is exact)
+    y2 = p.forward((2 * x.float()).to(torch.bfloat16))
+    assert torch.equal(y2, (2 * y.float()).to(torch.bfloat16))
+
+
+# --- sharding, host path, edge cases -----------------------------------------------
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_row_sharded_plans_concat_to_full(G):
+    L = O.synthetic_layer("tucker", (1024, 512), 1, (64, 64), seed=40_000)
+    layer, _ = to_layer(L, round_bf16=True)
+    x = torch.randn(300, 512, device=DEV).to(torch.bfloat16)
+    full = layer.plan(torch.bfloat16).forward(x)
+    rows = 1024
+    parts = [layer.plan(torch.bfloat16, row_range=(g * rows // G, (g + 1) * rows // G)).forward(x) for g in range(G)]
+    assert torch.equal(torch.cat(parts, dim=1), full)
+
+
+def test_forward_host_matches_device():
+    L = O.synthetic_layer("tr", (64, 80, 64, 80), 2, (8, 8, 8, 8), seed=41_000)
+    layer, _ = to_layer(L, round_bf16=True)
+    p = layer.plan(torch.bfloat16, max_m=64)
+    x = torch.randn(64, 5120).to(torch.bfloat16).pin_memory()
+    yh = torch.empty(64, 5120, dtype=torch.bfloat16).pin_memory()
+    p.forward_host(x, yh)
+    torch.cuda.synchronize()
+    yd = p.forward(x.to(DEV))
+    assert torch.equal(yh, yd.cpu())
+
+
+def test_edge_cases():
+    L = O.synthetic_layer("tt", (16, 16, 16, 16), 2, (8, 8, 8), seed=42_000)
+    layer, Lr = to_layer(L, round_bf16=True)
+    p = layer.plan(torch.bfloat16)
+    # M = 0
+    y = p.forward(torch.empty(0, 256, dtype=torch.bfloat16, device=DEV))
+    assert y.shape == (0, 256)
+    # strided x (ldx > cols)
+    big = torch.randn(33, 512, device=DEV).to(torch.bfloat16)
+    xs = big[:, :256]
+    y1 = p.forward(xs)
+    y2 = p.forward(xs.contiguous())
+    assert torch.equal(y1, y2)
+    # shape / device errors mirror the reference exception types
+    with pytest.raises(tnl.ShapeError):
+        p.forward(torch.randn(4, 255, device=DEV).to(torch.bfloat16))
+    with pytest.raises(tnl.DeviceError):
+        layer.forward(torch.randn(4, 256).to(torch.bfloat16))
+    # reference orientation
+    xr = torch.randn(256, 5, device=DEV).to(torch.bfloat16)
+    yr = tnl.apply_compressed(layer, xr)
+    ref = O.apply_chain(Lr, xr.float().cpu().numpy().astype(np.float64))
+    assert rel(ref, yr.float().cpu().numpy()) <= BF16_TOL
+
+
+def test_dense_family():
+    L = O.synthetic_layer("dense", (16, 32, 8, 16), 2, (), seed=43_000)
+    for m in (3, 100):
+        check_bf16(L, m, seed=43_001 + m)
+
+
+def test_launch_counter_counts_kernels():
+    L = O.synthetic_layer("tucker", (512, 512), 1, (64, 64), seed=44_000)
+    layer, _ = to_layer(L, round_bf16=True)
+    p = layer.plan(torch.bfloat16)
+    x = torch.randn(256, 512, device=DEV).to(torch.bfloat16)
+    p.forward(x)
+    tnl.launch_count(reset=True)
+    p.forward(x)
+    assert tnl.launch_count() >= 2
