@@ -260,16 +260,18 @@ class NativePlan:
             raise ShapeError(f"x inner dimension {tuple(x.shape)} does not match {cols} columns")
         if x.dtype != self.dtype:
             raise ValueError(f"x dtype {x.dtype} != plan dtype {self.dtype}")
-        if x.stride(1) != 1:
-            x = x.contiguous()
         m = x.shape[0]
+        if x.stride(1) != 1 or (m > 1 and x.stride(0) < cols):
+            x = x.contiguous()
+        ldx = x.stride(0) if m > 1 else cols
         if out is None:
             out = torch.empty((m, self.rows_local), dtype=self.dtype, device=x.device)
         ws = self.workspace(m)
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
-        st = self.lib.tnl_forward(self.handle, ctypes.c_void_p(x.data_ptr()), m, x.stride(0),
-                                  ctypes.c_void_p(out.data_ptr()), out.stride(0),
+        ldy = out.stride(0) if m > 1 else self.rows_local
+        st = self.lib.tnl_forward(self.handle, ctypes.c_void_p(x.data_ptr()), m, ldx,
+                                  ctypes.c_void_p(out.data_ptr()), ldy,
                                   ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(stream))
         N.check(st)
         return out
