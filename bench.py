@@ -1,0 +1,392 @@
+"""Benchmark: TN-linear tokens/s + TFLOP/s (% roofline) vs dense cuBLAS, Qwen3-32B shapes.
+
+Workload (BASELINE.json configs[1], "cfg2"): decode, M tokens (default 64)
+through a chain of L = 7 x copies distinct 5120->5120 TN projections —
+Tucker-2 R64/R128/R256, TR2 (8,8)/(16,16), TR4 (64,80|64,80) r8/r16 —
+random-init cores (Philox seeds), synthetic activations.
+A "step" is one pass of the M tokens through all L layers. The bank's weights
+exceed the 126 MB L2, so every step streams them from HBM (L2-cold by
+construction, no flush needed). value = M * L / t_step  [tokens/s per layer].
+
+    python bench.py [--gpus N --steps K --warmup W --m 64 --copies 10]
+    python bench.py --impl reference ...   # the reference's CPU algorithm (oracle port)
+
+N > 1 (torchrun): every rank runs its own replica (independent decode streams,
+no collective on the data path; "scaling": "weak"); value is the sum over
+ranks, timed as the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TN-linear tokens/s + TFLOP/s (% roofline) vs dense cuBLAS, Qwen3-32B shapes"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# reference CPU algorithm (oracle port of layer_to_matrix(L) @ x, float64)
+# ---------------------------------------------------------------------------
+
+
+def cpu_reference_sample(m: int, steps: int, variants=None):
+    """Time the reference algorithm on host cores; one cfg2 layer per step, cycling variants.
+
+    The reference's only forward is ``layer_to_matrix(L) @ x`` (tn_decompositions.py:364-365,
+    sensitivity.py:156) in float64; oracle/tn_oracle.py restates it (TR trace alpha-by-alpha).
+    """
+    import numpy as np
+
+    from oracle import tn_oracle as O
+    from paper_2602_01613_b200 import synthetic as S
+
+    variants = variants or S.CFG2_VARIANTS
+    layers = []
+    for v, (name, fam, ms, rm, ranks) in enumerate(variants):
+        L = S.make_layer(fam, ms, rm, ranks, seed=20_000 + 100 * v)
+        kw = dict(family=fam, mode_shape=ms, row_mode_count=rm)
+        if fam == "tucker":
+            kw.update(core=L.core.astype(np.float64), factors=[u.astype(np.float64) for u in L.factors])
+        else:
+            kw.update(cores=[c.astype(np.float64) for c in L.cores])
+        layers.append((name, O.OracleLayer(**kw)))
+    x = S.make_x(m, 5120, seed=29_999).astype(np.float64).T.copy()  # (cols, M) reference orientation
+    times = []
+    names = []
+    for i in range(steps):
+        name, L = layers[i % len(layers)]
+        t0 = time.perf_counter()
+        y = O.apply_reference(L, x)
+        times.append(time.perf_counter() - t0)
+        names.append(name)
+        assert y.shape == (5120, m)
+    return times, names
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    nthreads = cpu_cores()
+    steps = max(args.steps, 1)
+    # warm-up: one small pass (bounded)
+    cpu_reference_sample(args.m, min(args.warmup, 1))
+    times, names = cpu_reference_sample(args.m, steps)
+    total = sum(times)
+    value = args.m * steps / total
+    sample = (f"{steps} steps, one cfg2 5120x5120 layer per step cycling "
+              f"{len(set(names))} variants, M={args.m}, float64 reconstruct+matmul")
+    line = {
+        "metric": METRIC,
+        "impl": "reference",
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": args.gpus,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": nthreads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    return {
+        "workload": f"cfg2 decode: M={args.m} tokens through a chain of {7 * args.copies} distinct "
+                    "5120->5120 TN layers (Tucker-2 R64/R128/R256, TR2 (8,8)/(16,16), TR4 r8/r16; "
+                    f"{args.copies} copies each)",
+        "m": args.m,
+        "layers": 7 * args.copies,
+        "shape": "5120x5120 (Qwen3-32B attention projection)",
+        "l2_policy": "bank weights > 126 MB L2: streamed from HBM every step",
+        "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single",
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def time_graph(replay, steps, warmup, torch, dist=None):
+    for _ in range(warmup):
+        replay()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        replay()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    return ms / steps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="tnl", choices=["tnl", "reference"])
+    ap.add_argument("--m", type=int, default=64)
+    ap.add_argument("--copies", type=int, default=10)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense cuBLAS comparison")
+    ap.add_argument("--flags", type=int, default=0, help="TNL_PLAN_* preference for every layer")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2602_01613_b200 as tnl
+    from paper_2602_01613_b200 import synthetic as S
+    from paper_2602_01613_b200.stack import TNStack
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    hbm, tc, peak_kind = peaks()
+
+    bank = S.cfg2_bank(args.copies)
+    layers = [l for _, l in bank]
+    stack = TNStack(layers, torch.bfloat16, flags=args.flags)
+    M, L = args.m, len(layers)
+    x0 = torch.tensor(S.make_x(M, 5120, seed=29_999 + rank), dtype=torch.bfloat16, device="cuda")
+
+    # device-resident throughput (value): graph of one pass, inputs already in HBM
+    stack.capture(M, host_io=False)
+    stack.x_dev.copy_(x0)
+    launches_per_step = stack.launches_per_pass
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_end = time.time() + 1.0
+    while time.time() < t_end:  # soak so the clock samples see a loaded GPU
+        stack.replay()
+        torch.cuda.synchronize()
+    ms_step = time_graph(stack.replay, args.steps, args.warmup, torch, dist)
+    clocks = sampler.stop()
+    y_dev = stack.y_dev.clone()
+
+    # end-to-end through the public API: pinned host x -> H2D -> L layers -> D2H y, one graph
+    e2e_stack = TNStack(layers, torch.bfloat16, flags=args.flags)
+    e2e_stack.capture(M, host_io=True)
+    e2e_stack.x_host.copy_(x0.cpu())
+    ms_e2e = time_graph(e2e_stack.replay, args.steps, args.warmup, torch, dist)
+    torch.cuda.synchronize()
+    d = (e2e_stack.y_host.float() - y_dev.cpu().float()).norm() / y_dev.cpu().float().norm()
+    assert float(d) < 5e-2, f"e2e output differs from the device-resident pass ({float(d)})"
+
+    # algorithmic accounting: bytes = 2*(P + M*(rows+cols)), flops = M * chain flops
+    alg_bytes = sum(2 * (tnl.param_count(l) + M * (5120 + 5120)) for l in layers)
+    alg_flops = sum(M * l.chain_flops_per_token() for l in layers)
+    plan_bytes = sum(p.info["weight_bytes"] for p in stack.plans)
+    t_s = ms_step / 1e3
+    value = world * M * L / t_s
+    achieved_gbs = alg_bytes / t_s / 1e9
+    t_roof = max(alg_bytes / (hbm * 1e9), alg_flops / (tc * 1e12))
+
+    # per-variant breakdown (chains of the same variant)
+    breakdown = {}
+    for v, (name, *_rest) in enumerate(S.CFG2_VARIANTS):
+        sub = TNStack([l for n, l in bank if n == name], torch.bfloat16, flags=args.flags)
+        sub.capture(M, host_io=False)
+        ms_sub = time_graph(sub.replay, max(args.steps // 4, 10), 3, torch, None)
+        breakdown[name] = {
+            "us_per_layer": 1e3 * ms_sub / len(sub.plans),
+            "plan": sub.plans[0].info["plan_large_name"],
+            "launches_per_layer": sub.launches_per_pass / len(sub.plans),
+        }
+        del sub
+
+    dense = None
+    if not args.no_dense:
+        ws = [torch.randn(5120, 5120, device="cuda").to(torch.bfloat16) for _ in range(L)]
+        xd = x0.clone()
+        bufs = [torch.empty(M, 5120, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+
+        def dense_pass():
+            cur = xd
+            for i, w in enumerate(ws):
+                torch.matmul(cur, w.t(), out=bufs[i % 2])
+                cur = bufs[i % 2]
+
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            dense_pass()
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            dense_pass()
+        ms_dense = time_graph(g.replay, args.steps, args.warmup, torch, dist)
+        dense = {"value": world * M * L / (ms_dense / 1e3), "unit": "tokens/s", "ms_per_step": ms_dense,
+                 "what": "torch.matmul (cuBLAS) bf16 of the uncompressed 5120x5120 weights, same chain, CUDA graph"}
+        del ws
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        times, names = cpu_reference_sample(M, 7)
+        cpu = {"value": M * len(times) / sum(times), "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+               "sample": f"one layer of each of the 7 cfg2 variants at M={M}, reference algorithm "
+                         "layer_to_matrix(L) @ x in float64 (oracle port), numpy/OpenBLAS threads",
+               "per_variant_s": {n: t for n, t in zip(names, times)}}
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic",
+        "config": workload_config(args),
+        "tflops": alg_flops * world / t_s / 1e12,
+        "roofline": {
+            "kernel": "TN-linear layer forward (all launches of one layer, averaged over the bank)",
+            "bound": "hbm",
+            "achieved": achieved_gbs,
+            "peak": hbm,
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": achieved_gbs / hbm,
+            "traffic": None,
+            "algorithmic_bytes_per_step": alg_bytes,
+            "plan_weight_bytes_per_step": plan_bytes,
+            "t_roofline_ms": 1e3 * t_roof,
+            "frac_of_roofline_time": 1e3 * t_roof / ms_step,
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * M * L / (ms_e2e / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": e2e_stack.h2d_bytes, "d2h_bytes_per_step": e2e_stack.d2h_bytes,
+                "ms_per_step": ms_e2e, "api": "TNStack CUDA graph: pinned H2D + 70 tnl_forward + D2H"},
+        "gpu_launches": launches_per_step * args.steps,
+        "launches_per_step": launches_per_step,
+        "clocks": clocks,
+        "dense_cublas": dense,
+        "speedup_vs_dense": (value / dense["value"]) if dense else None,
+        "breakdown": breakdown,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

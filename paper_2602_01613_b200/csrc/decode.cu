@@ -1,0 +1,382 @@
+// decode.cu — small-M kernels of the merged-cut plan (see decode.cuh).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "decode.cuh"
+#include "ptx.cuh"
+
+namespace tnl {
+
+namespace {
+
+constexpr int BM = 128, BK = 64;
+constexpr uint32_t A_STAGE = BM * BK * 2;
+
+template <int BN>
+constexpr uint32_t tmem_cols() {
+  return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+}
+
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// SW128 K-major: byte offset of 16-byte chunk c (8 bf16) of row r inside a stage tile
+__device__ __forceinline__ uint32_t sw128_off(int r, int c) {
+  return (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
+}
+
+template <int BN, int STAGES, bool ACT_F32>
+__global__ void __launch_bounds__(192, 1)
+    dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+               const DecArgs a) {
+  constexpr uint32_t B_STAGE = BN * BK * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint32_t* last_flag = tmem_slot + 1;
+
+  const int tile_m = blockIdx.x;
+  const int total_kb = (a.K + BK - 1) / BK;
+  const int kb0 = blockIdx.z * a.kb_per_split;
+  const int kb1 = min(total_kb, kb0 + a.kb_per_split);
+  const int nkb = kb1 - kb0;
+  const uint32_t warp = warp_id();
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmW);
+    if (!ACT_F32) tma_prefetch_desc(&tmX);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], ACT_F32 ? 2 : 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<tmem_cols<BN>()>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const int npre = min(nkb, STAGES);
+      const uint32_t tx = A_STAGE + (ACT_F32 ? 0u : B_STAGE);
+      for (int i = 0; i < npre; ++i) {  // weights do not depend on the previous kernel
+        mbar_arrive_expect_tx(&full[i], tx);
+        tma_load_2d_hint(sA + i * A_STAGE, &tmW, &full[i], (kb0 + i) * BK, tile_m * BM,
+                         policy_evict_first());
+      }
+      pdl_wait();
+      if (!ACT_F32)
+        for (int i = 0; i < npre; ++i)
+          tma_load_2d(sB + i * B_STAGE, &tmX, &full[i], (kb0 + i) * BK, 0);
+      for (int i = npre; i < nkb; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], tx);
+        tma_load_2d_hint(sA + s * A_STAGE, &tmW, &full[s], (kb0 + i) * BK, tile_m * BM,
+                         policy_evict_first());
+        if (!ACT_F32) tma_load_2d(sB + s * B_STAGE, &tmX, &full[s], (kb0 + i) * BK, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&full[s], (i / STAGES) & 1);
+        tc_fence_after();
+        const uint64_t adesc = smem_desc_sw128(smem_u32(sA + s * A_STAGE));
+        const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + s * B_STAGE));
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) mma_bf16_ss(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
+        mma_commit(&empty[s]);
+      }
+      mma_commit(done);
+    }
+    __syncwarp();
+  } else {
+    const int et = threadIdx.x - 64;  // 0..127
+    pdl_wait();
+    if constexpr (ACT_F32) {
+      // fp32 activations [tokens][K] -> bf16 SW128 operand tiles (one per k-block; nkb <= STAGES)
+      for (int i = 0; i < nkb; ++i) {
+        uint8_t* dst = sB + i * B_STAGE;
+        const int kbase = (kb0 + i) * BK;
+        for (int e = et; e < BN * 8; e += 128) {
+          const int r = e >> 3, c = e & 7;
+          const int k = kbase + c * 8;
+          uint4 p = make_uint4(0, 0, 0, 0);
+          if (r < a.tokens && k < a.K) {
+            const float4* src = reinterpret_cast<const float4*>(a.act_f32 + (int64_t)r * a.act_ld + k);
+            const float4 v0 = __ldcg(src), v1 = __ldcg(src + 1);
+            p.x = pack_bf16x2(v0.x, v0.y);
+            p.y = pack_bf16x2(v0.z, v0.w);
+            p.z = pack_bf16x2(v1.x, v1.y);
+            p.w = pack_bf16x2(v1.z, v1.w);
+          }
+          *reinterpret_cast<uint4*>(dst + sw128_off(r, c)) = p;
+        }
+        fence_proxy_async_smem();
+        named_bar(1, 128);
+        if (et == 0) mbar_arrive(&full[i]);
+      }
+      // every activation read of this CTA is done: the last CTA re-zeroes the accumulator
+      if (a.counter) {
+        if (et == 0) {
+          __threadfence();
+          const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+          const unsigned old = atomicAdd(a.counter, 1u);
+          *last_flag = (old == total - 1) ? 1u : 0u;
+        }
+        named_bar(1, 128);
+        if (*last_flag) {
+          __threadfence();
+          float4* z = reinterpret_cast<float4*>(const_cast<float*>(a.act_f32));
+          for (int64_t e = et; e < a.zero_elems / 4; e += 128) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (et == 0) atomicExch(a.counter, 0u);
+        }
+      }
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const uint32_t q = warp & 3;
+    const int row = tile_m * BM + q * 32 + lane_id();
+    const bool row_ok = row < a.M_rows;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      float v[16];
+      tmem_ld16(tmem + ((q * 32) << 16) + c, v);
+      if (!row_ok || c >= a.tokens) continue;
+      const int n = min(16, a.tokens - c);
+      if (a.out_f32_atomic) {
+        float* o = static_cast<float*>(a.out) + (int64_t)row * a.ldo_i + (int64_t)c * a.ldo_j;
+        for (int e = 0; e < n; ++e) atomicAdd(o + (int64_t)e * a.ldo_j, v[e]);
+      } else {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + (int64_t)row * a.ldo_i + (int64_t)c * a.ldo_j;
+        for (int e = 0; e < n; ++e) o[(int64_t)e * a.ldo_j] = __float2bfloat16_rn(v[e]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<tmem_cols<BN>()>(tmem);
+}
+
+template <int BN, int STAGES, bool ACT_F32>
+int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const DecArgs& a, int splits,
+               cudaStream_t st) {
+  constexpr size_t smem = 1024 + (size_t)STAGES * (A_STAGE + BN * BK * 2) + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dec_kernel<BN, STAGES, ACT_F32>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.M_rows + BM - 1) / BM, 1, splits);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dec_kernel<BN, STAGES, ACT_F32>, w, x, a);
+  count_launch();
+  return (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-core GEMV variants (tokens <= 8)
+// ---------------------------------------------------------------------------
+constexpr int GV_CHUNK = 512;  // K elements per CTA (16 per lane)
+constexpr int GV_MAXT = 8;
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// T_acc[m][row] += sum_{k in chunk} W[row][k] x[m][k]; CTA = (chunk, 8 rows), warp = row
+__global__ void __launch_bounds__(256) gemv_a_kernel(const __nv_bfloat16* __restrict__ w, int64_t ldw,
+                                                     int rows, int K, const __nv_bfloat16* __restrict__ x,
+                                                     int64_t ldx, int tokens, float* t_acc, int64_t ldt) {
+  __shared__ __align__(16) __nv_bfloat16 xs[GV_MAXT][GV_CHUNK];
+  const int k0 = blockIdx.x * GV_CHUNK;
+  const int row = blockIdx.y * 8 + warp_id();
+  const int lane = lane_id();
+  // weights first (independent of the previous kernel)
+  uint4 wv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  if (row < rows) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = k0 + (h * 32 + lane) * 8;
+      if (k < K) wv[h] = __ldg(reinterpret_cast<const uint4*>(w + (int64_t)row * ldw + k));
+    }
+  }
+  pdl_launch_dependents();
+  pdl_wait();
+  for (int e = threadIdx.x; e < tokens * (GV_CHUNK / 8); e += 256) {
+    const int m = e / (GV_CHUNK / 8), c = e % (GV_CHUNK / 8);
+    const int k = k0 + c * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (k < K) v = *reinterpret_cast<const uint4*>(x + (int64_t)m * ldx + k);
+    *reinterpret_cast<uint4*>(&xs[m][c * 8]) = v;
+  }
+  __syncthreads();
+  if (row >= rows) return;
+  float wf[2][8];
+  bf16x8_to_f32(wv[0], wf[0]);
+  bf16x8_to_f32(wv[1], wf[1]);
+  for (int m = 0; m < tokens; ++m) {
+    float acc = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float xf[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(&xs[m][(h * 32 + lane) * 8]), xf);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = fmaf(wf[h][i], xf[i], acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) atomicAdd(t_acc + (int64_t)m * ldt + row, acc);
+  }
+}
+
+// y[m][row] = sum_k W[row][k] T_acc[m][k]; K <= 1024. Lanes per row = min(32, K/8).
+__global__ void __launch_bounds__(256) gemv_b_kernel(const __nv_bfloat16* __restrict__ w, int64_t ldw,
+                                                     int rows, int K, float* t_acc, int64_t ldt,
+                                                     int tokens, __nv_bfloat16* y, int64_t ldy,
+                                                     unsigned int* counter) {
+  extern __shared__ float ts[];  // [tokens][K]
+  __shared__ unsigned last;
+  const int lpr = min(32, K / 8);         // lanes per row
+  const int rpw = 32 / lpr;               // rows per warp pass
+  const int lane = lane_id();
+  const int sub = lane / lpr, sl = lane % lpr;
+  const int rows_per_cta = 8 * rpw * 4;   // 4 passes per warp
+  const int row0 = blockIdx.x * rows_per_cta;
+  // weights first: up to 4 passes x (K / (8*lpr)) chunks per lane, K <= 1024 -> <= 4 chunks
+  const int nch = K / (8 * lpr);
+  uint4 wv[4][4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int row = row0 + (p * 8 + (int)warp_id()) * rpw + sub;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      wv[p][c] = make_uint4(0, 0, 0, 0);
+      if (c < nch && row < rows)
+        wv[p][c] = __ldg(reinterpret_cast<const uint4*>(w + (int64_t)row * ldw + (c * lpr + sl) * 8));
+    }
+  }
+  pdl_launch_dependents();
+  pdl_wait();
+  for (int e = threadIdx.x; e < tokens * K / 4; e += 256) {
+    const int m = e / (K / 4), c = e % (K / 4);
+    reinterpret_cast<float4*>(ts)[e] = __ldcg(reinterpret_cast<const float4*>(t_acc + (int64_t)m * ldt) + c);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(counter, 1u);
+    last = (old == gridDim.x - 1) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int row = row0 + (p * 8 + (int)warp_id()) * rpw + sub;
+    float wf[4][8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) bf16x8_to_f32(wv[p][c], wf[c]);
+    for (int m = 0; m < tokens; ++m) {
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c >= nch) break;
+        const float* t = ts + m * K + (c * lpr + sl) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc = fmaf(wf[c][i], t[i], acc);
+      }
+      for (int o = lpr / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (sl == 0 && row < rows) y[(int64_t)m * ldy + row] = __float2bfloat16_rn(acc);
+    }
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    float4* z = reinterpret_cast<float4*>(t_acc);
+    for (int e = threadIdx.x; e < tokens * ldt / 4; e += 256) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (threadIdx.x == 0) atomicExch(counter, 0u);
+  }
+}
+
+template <typename K, typename... Args>
+int launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  count_launch();
+  return (int)e;
+}
+
+}  // namespace
+
+int launch_dec_a(const CUtensorMap& w, const CUtensorMap& x, const DecArgs& a, int splits, cudaStream_t st) {
+  if (a.tokens <= 16) return launch_dec<16, 4, false>(w, x, a, splits, st);
+  if (a.tokens <= 32) return launch_dec<32, 4, false>(w, x, a, splits, st);
+  return launch_dec<64, 4, false>(w, x, a, splits, st);
+}
+
+int launch_dec_b(const CUtensorMap& w, const DecArgs& a, cudaStream_t st) {
+  // K = r_pad <= 256 -> <= 4 k-blocks, all resident (no ring reuse in the fp32-operand path)
+  if (a.K > 4 * BK) return (int)cudaErrorInvalidValue;
+  if (a.tokens <= 16) return launch_dec<16, 4, true>(w, w, a, 1, st);
+  if (a.tokens <= 32) return launch_dec<32, 4, true>(w, w, a, 1, st);
+  return launch_dec<64, 4, true>(w, w, a, 1, st);
+}
+
+int launch_gemv_a(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const __nv_bfloat16* x, int64_t ldx,
+                  int tokens, float* t_acc, int64_t ldt, cudaStream_t st) {
+  if (tokens > GV_MAXT || K % 8) return (int)cudaErrorInvalidValue;
+  dim3 grid((K + GV_CHUNK - 1) / GV_CHUNK, (rows + 7) / 8);
+  return launch_pdl(gemv_a_kernel, grid, dim3(256), 0, st, w, ldw, rows, K, x, ldx, tokens, t_acc, ldt);
+}
+
+int launch_gemv_b(const __nv_bfloat16* w, int64_t ldw, int rows, int K, float* t_acc, int64_t ldt, int tokens,
+                  __nv_bfloat16* y, int64_t ldy, unsigned int* counter, cudaStream_t st) {
+  if (tokens > GV_MAXT || K % 64 || K > 1024) return (int)cudaErrorInvalidValue;
+  const int lpr = K / 8 < 32 ? K / 8 : 32;
+  const int rows_per_cta = 8 * (32 / lpr) * 4;
+  dim3 grid((rows + rows_per_cta - 1) / rows_per_cta);
+  const size_t smem = sizeof(float) * tokens * K;
+  return launch_pdl(gemv_b_kernel, grid, dim3(256), smem, st, w, ldw, rows, K, t_acc, ldt, tokens, y, ldy,
+                    counter);
+}
+
+}  // namespace tnl

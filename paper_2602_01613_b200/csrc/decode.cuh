@@ -1,0 +1,58 @@
+// decode.cuh — small-M (decode) kernels for the merged-cut plan.
+//
+// A layer at decode is y = A_out (B_in x) with M <= 64 tokens. Both steps are
+// weight-streaming: the weights sit on the MMA M side ("swap-AB"), the tokens
+// on N. Two launches per layer, chained with programmatic dependent launch:
+//
+//   phase A  T_acc[m][k] += sum_j B_in[k][j] x[m][j]      split-K over j, fp32
+//            reductions (red.global.add) into a plan-owned accumulator that
+//            is all-zero at rest;
+//   phase B  y[m][i] = sum_k A_out[i][k] bf16(T_acc[m][k]) — T_acc is read
+//            straight from fp32 global, converted to bf16 into the swizzled
+//            smem operand layout by the (otherwise idle) epilogue warps; the
+//            last CTA to finish reading re-zeroes T_acc.
+//
+// Weight tiles are TMA-loaded BEFORE griddepcontrol.wait, so the weight
+// stream of layer l overlaps the tail of the previous kernel.
+//
+// For M <= 8 the same protocol runs on CUDA cores (GEMV-like: 16-byte
+// vector loads of the weight rows, warp-shuffle reductions).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tnl {
+
+struct DecArgs {
+  int32_t M_rows;    // weight rows (MMA M side): r_pad (phase A) or rows (phase B)
+  int32_t tokens;    // M (N side)
+  int32_t K;         // contraction length
+  int32_t kb_per_split;
+  // activation operand (phase B): fp32 [tokens][K] with row stride act_ld
+  const float* act_f32;
+  int64_t act_ld;
+  // output
+  void* out;
+  int64_t ldo_i, ldo_j;  // element (weight-row i, token j)
+  int32_t out_f32_atomic; // 1: red.add fp32 (phase A); 0: bf16 store (phase B)
+  // last-CTA zeroing of act_f32 (phase B)
+  unsigned int* counter;
+  int64_t zero_elems;
+};
+
+// phase A: weights (TMA map `w`, rows=M_rows, K) x activations (TMA map `x`, bf16 tokens x K)
+int launch_dec_a(const CUtensorMap& w, const CUtensorMap& x, const DecArgs& a, int splits,
+                 cudaStream_t st);
+// phase B: weights (TMA map `w`) x fp32 activations (a.act_f32), zeroes a.act_f32 at the end
+int launch_dec_b(const CUtensorMap& w, const DecArgs& a, cudaStream_t st);
+
+// CUDA-core GEMV variants (tokens <= 8)
+int launch_gemv_a(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const __nv_bfloat16* x,
+                  int64_t ldx, int tokens, float* t_acc, int64_t ldt, cudaStream_t st);
+int launch_gemv_b(const __nv_bfloat16* w, int64_t ldw, int rows, int K, float* t_acc, int64_t ldt,
+                  int tokens, __nv_bfloat16* y, int64_t ldy, unsigned int* counter,
+                  cudaStream_t st);
+
+}  // namespace tnl

@@ -32,6 +32,7 @@
 
 #include "../../include/tnl.h"
 #include "common.cuh"
+#include "decode.cuh"
 #include "generic.cuh"
 #include "tc_gemm.cuh"
 
@@ -153,6 +154,8 @@ struct tnl_plan {
   __nv_bfloat16* u0 = nullptr;    //                 (rows_local x R0p)
   int64_t r0p = 0, r1p = 0;
   __nv_bfloat16* wdense = nullptr;  // dense (rows_local x cols)
+  float* tacc = nullptr;            // decode accumulator (kDecMaxM x r_pad), zero at rest
+  unsigned int* counter = nullptr;  // decode last-CTA counter, zero at rest
   float* gen_w_out = nullptr;       // generic dense rows slice (fp32) for sharded generic plans
   int32_t plan_large = TNL_PLAN_GENERIC, plan_small = TNL_PLAN_GENERIC;
   int32_t decode_max_m = 0;
@@ -795,7 +798,9 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   }
   P->plan_large = large;
   P->plan_small = large;
-  P->decode_max_m = 0;
+  P->decode_max_m = (tc_ok && P->family != TNL_FAMILY_DENSE && round_up(P->r_cut, 16) <= 256 &&
+                     !(flags & TNL_PLAN_NO_DECODE)) ? 64 : 0;
+  if (P->decode_max_m) P->plan_small = TNL_PLAN_CUT;
 
   // ---- device arena: generic cores + panels ----
   size_t bytes = 0;
@@ -806,7 +811,13 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   }
   size_t off_bin = 0, off_aout = 0, off_u1 = 0, off_g = 0, off_u0 = 0, off_w = 0;
   const bool dense = P->family == TNL_FAMILY_DENSE;
-  if (large == TNL_PLAN_CUT && !dense) {
+  const bool want_cut = tc_ok && !dense;
+  size_t off_tacc = 0, off_cnt = 0;
+  if (want_cut) {
+    off_tacc = bytes;
+    bytes += round_up(64 * P->r_pad * 4, 256);
+    off_cnt = bytes;
+    bytes += 256;
     off_bin = bytes;
     bytes += round_up(P->r_pad * P->cols * 2, 256);
     off_aout = bytes;
@@ -840,7 +851,10 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     copy_2d_any<<<grid_for(rows_local * P->cols), 256, 0, st>>>(
         P->gcore[0] + P->row_begin * P->cols, DT_F32, P->cols, 1, P->wdense, DT_BF16, P->cols, 1,
         rows_local, P->cols);
-  } else if (large == TNL_PLAN_CUT) {
+  }
+  if (want_cut) {
+    P->tacc = reinterpret_cast<float*>(base + off_tacc);
+    P->counter = reinterpret_cast<unsigned int*>(base + off_cnt);
     P->bin = reinterpret_cast<__nv_bfloat16*>(base + off_bin);
     P->aout = reinterpret_cast<__nv_bfloat16*>(base + off_aout);
     float *fb = nullptr, *fa = nullptr;
@@ -859,7 +873,8 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     cudaFree(fb);
     cudaFree(fa);
     if (s2 != TNL_OK) return s2;
-  } else if (large == TNL_PLAN_CHAIN) {
+  }
+  if (large == TNL_PLAN_CHAIN) {
     // Tucker-2: U1^T (R1p x cols), G (R0p x R1p), U0 rows (rows_local x R0p)
     P->u1t = reinterpret_cast<__nv_bfloat16*>(base + off_u1);
     P->gmat = reinterpret_cast<__nv_bfloat16*>(base + off_g);
@@ -976,6 +991,70 @@ static int choose_splits(int64_t tiles, int64_t K) {
   return (int)std::min<int64_t>(s, total_kb);
 }
 
+static constexpr int64_t kDecMaxM = 64;  // decode path (plan-owned accumulator capacity)
+
+static bool gemv_ok_k(int64_t K) {
+  if (K % 8) return false;
+  const int64_t l = K / 8;
+  if (l <= 32) return (l & (l - 1)) == 0;
+  return K % 256 == 0 && K <= 1024;
+}
+
+// Small-M path of the merged-cut plan: phase A (B_in, split-K, fp32 reductions into the
+// plan-owned accumulator) + phase B (A_out, reads the fp32 accumulator, re-zeroes it).
+static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y,
+                                 int64_t ldy, cudaStream_t st) {
+  const int64_t rows_local = P->row_end - P->row_begin;
+  int err = 0;
+  if (M <= 8 && gemv_ok_k(P->r_pad)) {
+    err = launch_gemv_a(P->bin, P->cols, (int)P->r_pad, (int)P->cols,
+                        static_cast<const __nv_bfloat16*>(x), ldx, (int)M, P->tacc, P->r_pad, st);
+    if (err) return fail(TNL_ERR_CUDA, "gemv_a launch: %s", cudaGetErrorString((cudaError_t)err));
+    err = launch_gemv_b(P->aout, P->r_pad, (int)rows_local, (int)P->r_pad, P->tacc, P->r_pad, (int)M,
+                        static_cast<__nv_bfloat16*>(y), ldy, P->counter, st);
+    if (err) return fail(TNL_ERR_CUDA, "gemv_b launch: %s", cudaGetErrorString((cudaError_t)err));
+    return TNL_OK;
+  }
+  CUtensorMap tw, tx, tw2;
+  const int bn = pick_bn(M);
+  if ((err = get_tmap(P, &tw, P->bin, P->cols, P->r_pad, P->cols, 128)) ||
+      (err = get_tmap(P, &tx, x, P->cols, M, ldx, bn)) ||
+      (err = get_tmap(P, &tw2, P->aout, P->r_pad, rows_local, P->r_pad, 128)))
+    return fail(TNL_ERR_CUDA, "tensor map (decode) failed: %d", err);
+  DecArgs a;
+  memset(&a, 0, sizeof a);
+  a.M_rows = (int32_t)P->r_pad;
+  a.tokens = (int32_t)M;
+  a.K = (int32_t)P->cols;
+  const int total_kb = (int)((P->cols + 63) / 64);
+  int splits = choose_splits((P->r_pad + 127) / 128, P->cols);
+  a.kb_per_split = (total_kb + splits - 1) / splits;
+  splits = (total_kb + a.kb_per_split - 1) / a.kb_per_split;
+  a.out = P->tacc;
+  a.ldo_i = 1;
+  a.ldo_j = P->r_pad;
+  a.out_f32_atomic = 1;
+  if ((err = launch_dec_a(tw, tx, a, splits, st)))
+    return fail(TNL_ERR_CUDA, "decode phase A launch: %s", cudaGetErrorString((cudaError_t)err));
+  DecArgs b;
+  memset(&b, 0, sizeof b);
+  b.M_rows = (int32_t)rows_local;
+  b.tokens = (int32_t)M;
+  b.K = (int32_t)P->r_pad;
+  b.kb_per_split = (int32_t)((P->r_pad + 63) / 64);
+  b.act_f32 = P->tacc;
+  b.act_ld = P->r_pad;
+  b.out = y;
+  b.ldo_i = 1;
+  b.ldo_j = ldy;
+  b.out_f32_atomic = 0;
+  b.counter = P->counter;
+  b.zero_elems = M * P->r_pad;
+  if ((err = launch_dec_b(tw2, b, st)))
+    return fail(TNL_ERR_CUDA, "decode phase B launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
+}
+
 static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y, int64_t ldy,
                              void* ws, size_t ws_bytes, cudaStream_t st) {
   size_t o_f32, o_b0, o_b1;
@@ -987,6 +1066,8 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
   __nv_bfloat16* t1 = reinterpret_cast<__nv_bfloat16*>(w + o_b1);
   const int64_t rows_local = P->row_end - P->row_begin;
   const bool swap = M <= kSwapMaxM;
+  if (M <= kDecMaxM && P->tacc && P->r_pad <= 256 && !(P->flags & TNL_PLAN_NO_DECODE))
+    return forward_decode(P, x, M, ldx, y, ldy, st);
   tnl_status s;
   if (P->family == TNL_FAMILY_DENSE) {
     return tc_step(P, x, ldx, P->wdense, P->cols, M, rows_local, P->cols, y, ldy, false, swap, 1, st);

@@ -252,7 +252,7 @@ class NativePlan:
             self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws
 
-    def forward(self, x, out=None, stream=None):
+    def forward(self, x, out=None, stream=None, ws=None):
         if not isinstance(x, torch.Tensor) or not x.is_cuda:
             raise DeviceError("forward needs a CUDA tensor (no CPU fallback)")
         cols = self.info["cols"]
@@ -266,7 +266,8 @@ class NativePlan:
         ldx = x.stride(0) if m > 1 else cols
         if out is None:
             out = torch.empty((m, self.rows_local), dtype=self.dtype, device=x.device)
-        ws = self.workspace(m)
+        if ws is None or ws.numel() < self.workspace_bytes(m):
+            ws = self.workspace(m)
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
         ldy = out.stride(0) if m > 1 else self.rows_local

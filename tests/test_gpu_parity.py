@@ -227,3 +227,38 @@ def test_launch_counter_counts_kernels():
     tnl.launch_count(reset=True)
     p.forward(x)
     assert tnl.launch_count() >= 2
+
+
+@pytest.mark.parametrize("m", [1, 5, 8, 9, 33, 64])
+def test_decode_repeat_zero_at_rest(m):
+    """The decode accumulator is re-zeroed by the last CTA: repeated calls agree with the oracle."""
+    L = O.synthetic_layer("tucker", (5120, 5120), 1, (128, 128), seed=45_000)
+    layer, Lr = to_layer(L, round_bf16=True)
+    p = layer.plan(torch.bfloat16)
+    assert p.info["decode_max_m"] == 64
+    x = O.round_bf16(O.synthetic_x(m, 5120, seed=45_001))
+    xt = torch.tensor(x, dtype=torch.bfloat16, device=DEV)
+    ref = O.forward_torch_orient(Lr, x)
+    for _ in range(3):
+        y = p.forward(xt)
+        torch.cuda.synchronize()
+        assert rel(ref, y.float().cpu().numpy()) <= BF16_TOL
+
+
+def test_stack_graph_replay_matches_eager():
+    from paper_2602_01613_b200.stack import TNStack
+
+    Ls = [O.synthetic_layer(f, ms, rm, rk, seed=46_000 + i) for i, (f, ms, rm, rk) in enumerate(
+        [("tucker", (1024, 1024), 1, (64, 64)), ("tr", (32, 32, 32, 32), 2, (4, 4, 4, 4)),
+         ("tt", (32, 32, 32, 32), 2, (16, 16, 16))])]
+    layers = [to_layer(L, round_bf16=True)[0] for L in Ls]
+    st = TNStack(layers, torch.bfloat16)
+    x = torch.randn(16, 1024, device=DEV).to(torch.bfloat16)
+    ye = st.forward(x).clone()
+    st.capture(16, host_io=True)
+    st.x_host.copy_(x.cpu())
+    for _ in range(3):
+        st.replay()
+    torch.cuda.synchronize()
+    d = (st.y_host.float() - ye.cpu().float()).norm() / ye.cpu().float().norm()
+    assert float(d) < 1e-2
