@@ -370,7 +370,9 @@ int launch_gemv_a(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const __
 
 int launch_gemv_b(const __nv_bfloat16* w, int64_t ldw, int rows, int K, float* t_acc, int64_t ldt, int tokens,
                   __nv_bfloat16* y, int64_t ldy, unsigned int* counter, cudaStream_t st) {
-  if (tokens > GV_MAXT || K % 64 || K > 1024) return (int)cudaErrorInvalidValue;
+  const int l8 = K / 8;
+  const bool ok = (K % 8 == 0) && ((l8 <= 32 && (l8 & (l8 - 1)) == 0) || (K % 256 == 0 && K <= 1024));
+  if (tokens > GV_MAXT || !ok) return (int)cudaErrorInvalidValue;
   const int lpr = K / 8 < 32 ? K / 8 : 32;
   const int rows_per_cta = 8 * (32 / lpr) * 4;
   dim3 grid((rows + rows_per_cta - 1) / rows_per_cta);

@@ -184,7 +184,9 @@ def test_forward_host_matches_device():
     p.forward_host(x, yh)
     torch.cuda.synchronize()
     yd = p.forward(x.to(DEV))
-    assert torch.equal(yh, yd.cpu())
+    # decode split-K reductions are fp32 atomics: equal up to summation order
+    d = (yh.float() - yd.cpu().float()).norm() / yd.cpu().float().norm()
+    assert float(d) < 5e-3
 
 
 def test_edge_cases():
