@@ -152,6 +152,11 @@ TNL_API tnl_status tnl_reconstruct(const tnl_plan* plan, void* w, int64_t ldw, i
  * (evidence counter for benchmarks). */
 TNL_API int64_t tnl_launch_count(int32_t reset);
 
+/* Debug: record per-CTA %globaltimer stamps of the decode kernels into a device
+ * buffer of >= 2*1024*16 uint64 (phase A at [0, 16K), phase B at [16K, 32K));
+ * NULL disables. Not for production use (adds global stores). */
+TNL_API tnl_status tnl_plan_set_trace(tnl_plan* plan, void* device_buffer);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,7 @@ EXPORTED = (
     "tnl_forward_host",
     "tnl_reconstruct",
     "tnl_launch_count",
+    "tnl_plan_set_trace",
 )
 
 
@@ -104,6 +105,8 @@ def load():
         lib.tnl_forward.argtypes = [P, P, i64, i64, P, i64, P, ctypes.c_size_t, P]
         lib.tnl_forward_host.argtypes = [P, P, i64, P, P]
         lib.tnl_reconstruct.argtypes = [P, P, i64, ctypes.c_int32, P]
+        lib.tnl_plan_set_trace.argtypes = [P, P]
+        lib.tnl_plan_set_trace.restype = ctypes.c_int
         lib.tnl_launch_count.argtypes = [ctypes.c_int32]
         lib.tnl_launch_count.restype = i64
         for name in ("tnl_plan_create", "tnl_plan_create_rows", "tnl_plan_destroy", "tnl_plan_query",

@@ -22,6 +22,9 @@ constexpr uint32_t tmem_cols() {
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 // SW128 K-major: byte offset of 16-byte chunk c (8 bf16) of row r inside a stage tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
@@ -29,19 +32,32 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
 }
 
 template <int BN, int STAGES, bool ACT_F32>
+struct DecSmem {
+  static constexpr uint32_t B_STAGE = BN * BK * 2;          // bf16 activation operand
+  static constexpr uint32_t F_STAGE = ACT_F32 ? BK * BN * 4 : 0;  // fp32 staging [64 k][BN tokens]
+  static constexpr uint32_t Y_BYTES = ACT_F32 ? BN * BM * 2 : 0;  // y tile [BN tokens][128 rows]
+  static constexpr size_t bytes = 1024 + (size_t)STAGES * (A_STAGE + B_STAGE + F_STAGE) + Y_BYTES + 512;
+};
+
+template <int BN, int STAGES, bool ACT_F32>
 __global__ void __launch_bounds__(192, 1)
     dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-               const DecArgs a) {
-  constexpr uint32_t B_STAGE = BN * BK * 2;
+               const __grid_constant__ CUtensorMap tmY, const DecArgs a) {
+  using SM = DecSmem<BN, STAGES, ACT_F32>;
+  constexpr uint32_t B_STAGE = SM::B_STAGE, F_STAGE = SM::F_STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  float* sF = reinterpret_cast<float*>(sB + STAGES * B_STAGE);
+  __nv_bfloat16* sY = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(sF) + STAGES * F_STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sY) + SM::Y_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* stg = empty + STAGES;
+  uint64_t* done = stg + STAGES;
+  uint64_t* flagbar = done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(flagbar + 1);
   uint32_t* last_flag = tmem_slot + 1;
 
   const int tile_m = blockIdx.x;
@@ -50,15 +66,22 @@ __global__ void __launch_bounds__(192, 1)
   const int kb1 = min(total_kb, kb0 + a.kb_per_split);
   const int nkb = kb1 - kb0;
   const uint32_t warp = warp_id();
+  unsigned long long* tr = a.trace ? a.trace + 16 * (blockIdx.x + gridDim.x * blockIdx.z) : nullptr;
+#define TRACE(ev) \
+  if (tr) tr[ev] = globaltimer();
+  if (threadIdx.x == 0) TRACE(0);
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmW);
-    if (!ACT_F32) tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmX);
+    if (ACT_F32) tma_prefetch_desc(&tmY);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], ACT_F32 ? 2 : 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&stg[s], 1);
     }
     mbar_init(done, 1);
+    mbar_init(flagbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<tmem_cols<BN>()>(tmem_slot);
@@ -67,6 +90,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
+  if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0) {
     if (elect_one()) {
@@ -77,17 +101,33 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d_hint(sA + i * A_STAGE, &tmW, &full[i], (kb0 + i) * BK, tile_m * BM,
                          policy_evict_first());
       }
+      TRACE(2);
       pdl_wait();
-      if (!ACT_F32)
-        for (int i = 0; i < npre; ++i)
+      TRACE(3);
+      for (int i = 0; i < npre; ++i) {
+        if (ACT_F32) {  // fp32 accumulator rows kappa in [k-block], all tokens
+          mbar_arrive_expect_tx(&stg[i], F_STAGE);
+          tma_load_2d(reinterpret_cast<uint8_t*>(sF) + i * F_STAGE, &tmX, &stg[i], 0, (kb0 + i) * BK);
+        } else {
           tma_load_2d(sB + i * B_STAGE, &tmX, &full[i], (kb0 + i) * BK, 0);
-      for (int i = npre; i < nkb; ++i) {
+        }
+      }
+      if (ACT_F32 && a.counter) {
+        // every accumulator read of this CTA has landed -> count it here, off the
+        // epilogue's critical path; the epilogue reads last_flag at the very end
+        for (int i = 0; i < npre; ++i) mbar_wait(&stg[i], 0);
+        __threadfence();
+        const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+        *last_flag = (atomicAdd(a.counter, 1u) == total - 1) ? 1u : 0u;
+        mbar_arrive(flagbar);
+      }
+      for (int i = npre; i < nkb; ++i) {  // (phase A only: ACT_F32 keeps nkb <= STAGES)
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(&full[s], tx);
         tma_load_2d_hint(sA + s * A_STAGE, &tmW, &full[s], (kb0 + i) * BK, tile_m * BM,
                          policy_evict_first());
-        if (!ACT_F32) tma_load_2d(sB + s * B_STAGE, &tmX, &full[s], (kb0 + i) * BK, 0);
+        tma_load_2d(sB + s * B_STAGE, &tmX, &full[s], (kb0 + i) * BK, 0);
       }
     }
   } else if (warp == 1) {
@@ -97,6 +137,7 @@ __global__ void __launch_bounds__(192, 1)
         const int s = i % STAGES;
         mbar_wait(&full[s], (i / STAGES) & 1);
         tc_fence_after();
+        if (i == 0) TRACE(4);
         const uint64_t adesc = smem_desc_sw128(smem_u32(sA + s * A_STAGE));
         const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + s * B_STAGE));
 #pragma unroll
@@ -104,80 +145,97 @@ __global__ void __launch_bounds__(192, 1)
         mma_commit(&empty[s]);
       }
       mma_commit(done);
+      TRACE(5);
     }
     __syncwarp();
   } else {
     const int et = threadIdx.x - 64;  // 0..127
     pdl_wait();
+    if (et == 0) TRACE(6);
     if constexpr (ACT_F32) {
-      // fp32 activations [tokens][K] -> bf16 SW128 operand tiles (one per k-block; nkb <= STAGES)
+      // staged fp32 [64 kappa][BN tokens] -> bf16 SW128 operand [BN tokens][64 kappa]
       for (int i = 0; i < nkb; ++i) {
+        mbar_wait(&stg[i], 0);
+        const float* src = sF + i * (F_STAGE / 4);
         uint8_t* dst = sB + i * B_STAGE;
-        const int kbase = (kb0 + i) * BK;
         for (int e = et; e < BN * 8; e += 128) {
-          const int r = e >> 3, c = e & 7;
-          const int k = kbase + c * 8;
-          uint4 p = make_uint4(0, 0, 0, 0);
-          if (r < a.tokens && k < a.K) {
-            const float4* src = reinterpret_cast<const float4*>(a.act_f32 + (int64_t)r * a.act_ld + k);
-            const float4 v0 = __ldcg(src), v1 = __ldcg(src + 1);
-            p.x = pack_bf16x2(v0.x, v0.y);
-            p.y = pack_bf16x2(v0.z, v0.w);
-            p.z = pack_bf16x2(v1.x, v1.y);
-            p.w = pack_bf16x2(v1.z, v1.w);
-          }
+          const int r = e % BN, c = e / BN;  // token r, kappa chunk c
+          float f[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) f[q] = src[(c * 8 + q) * BN + r];
+          uint4 p;
+          p.x = pack_bf16x2(f[0], f[1]);
+          p.y = pack_bf16x2(f[2], f[3]);
+          p.z = pack_bf16x2(f[4], f[5]);
+          p.w = pack_bf16x2(f[6], f[7]);
           *reinterpret_cast<uint4*>(dst + sw128_off(r, c)) = p;
         }
         fence_proxy_async_smem();
         named_bar(1, 128);
         if (et == 0) mbar_arrive(&full[i]);
       }
-      // every activation read of this CTA is done: the last CTA re-zeroes the accumulator
-      if (a.counter) {
-        if (et == 0) {
-          __threadfence();
-          const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-          const unsigned old = atomicAdd(a.counter, 1u);
-          *last_flag = (old == total - 1) ? 1u : 0u;
-        }
-        named_bar(1, 128);
-        if (*last_flag) {
-          __threadfence();
-          float4* z = reinterpret_cast<float4*>(const_cast<float*>(a.act_f32));
-          for (int64_t e = et; e < a.zero_elems / 4; e += 128) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (et == 0) atomicExch(a.counter, 0u);
-        }
-      }
+      if (et == 0) TRACE(7);
     }
     mbar_wait(done, 0);
     tc_fence_after();
+    if (et == 0) TRACE(8);
     const uint32_t q = warp & 3;
-    const int row = tile_m * BM + q * 32 + lane_id();
+    const int lrow = q * 32 + lane_id();
+    const int row = tile_m * BM + lrow;
     const bool row_ok = row < a.M_rows;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 16) {
       float v[16];
       tmem_ld16(tmem + ((q * 32) << 16) + c, v);
-      if (!row_ok || c >= a.tokens) continue;
-      const int n = min(16, a.tokens - c);
-      if (a.out_f32_atomic) {
-        float* o = static_cast<float*>(a.out) + (int64_t)row * a.ldo_i + (int64_t)c * a.ldo_j;
-        for (int e = 0; e < n; ++e) atomicAdd(o + (int64_t)e * a.ldo_j, v[e]);
+      if constexpr (ACT_F32) {
+        // y tile staged [token][row] for one TMA store
+#pragma unroll
+        for (int e = 0; e < 16; ++e) sY[(c + e) * BM + lrow] = __float2bfloat16_rn(v[e]);
       } else {
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + (int64_t)row * a.ldo_i + (int64_t)c * a.ldo_j;
-        for (int e = 0; e < n; ++e) o[(int64_t)e * a.ldo_j] = __float2bfloat16_rn(v[e]);
+        if (!row_ok || c >= a.tokens) continue;
+        const int n = min(16, a.tokens - c);
+        // kappa-major accumulator: this thread's 16 token values are contiguous
+        float* o = static_cast<float*>(a.out) + (int64_t)row * a.ldo_i + c;
+        if (n == 16) {
+#pragma unroll
+          for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e < n) atomicAdd(o + e, v[e]);
+        }
       }
     }
+    if constexpr (ACT_F32) {
+      fence_proxy_async_smem();
+      named_bar(1, 128);
+      if (et == 0) {
+        tma_store_2d(&tmY, sY, tile_m * BM, 0);
+        tma_store_commit();
+      }
+      if (a.counter) {
+        mbar_wait(flagbar, 0);  // producer lane wrote last_flag before arriving
+        if (*last_flag) {
+          float4* z = reinterpret_cast<float4*>(const_cast<float*>(a.act_f32));
+          for (int64_t e = et; e < a.zero_elems / 4; e += 128) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (et == 0) atomicExch(a.counter, 0u);
+        }
+      }
+      if (et == 0) tma_store_wait_all();
+    }
   }
+  if (threadIdx.x == 64) TRACE(9);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<tmem_cols<BN>()>(tmem);
+  if (threadIdx.x == 32) TRACE(10);
+#undef TRACE
 }
 
 template <int BN, int STAGES, bool ACT_F32>
-int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const DecArgs& a, int splits,
-               cudaStream_t st) {
-  constexpr size_t smem = 1024 + (size_t)STAGES * (A_STAGE + BN * BK * 2) + 256;
+int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& y, const DecArgs& a,
+               int splits, cudaStream_t st) {
+  constexpr size_t smem = DecSmem<BN, STAGES, ACT_F32>::bytes;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(dec_kernel<BN, STAGES, ACT_F32>,
@@ -195,7 +253,7 @@ int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const DecArgs& a, int
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dec_kernel<BN, STAGES, ACT_F32>, w, x, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dec_kernel<BN, STAGES, ACT_F32>, w, x, y, a);
   count_launch();
   return (int)e;
 }
@@ -258,7 +316,7 @@ __global__ void __launch_bounds__(256) gemv_a_kernel(const __nv_bfloat16* __rest
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) atomicAdd(t_acc + (int64_t)m * ldt + row, acc);
+    if (lane == 0) atomicAdd(t_acc + (int64_t)row * ldt + m, acc);
   }
 }
 
@@ -290,9 +348,9 @@ __global__ void __launch_bounds__(256) gemv_b_kernel(const __nv_bfloat16* __rest
   }
   pdl_launch_dependents();
   pdl_wait();
-  for (int e = threadIdx.x; e < tokens * K / 4; e += 256) {
-    const int m = e / (K / 4), c = e % (K / 4);
-    reinterpret_cast<float4*>(ts)[e] = __ldcg(reinterpret_cast<const float4*>(t_acc + (int64_t)m * ldt) + c);
+  for (int e = threadIdx.x; e < tokens * K; e += 256) {  // kappa-major [k][ldt] -> [m][k]
+    const int k = e / tokens, m = e % tokens;
+    ts[m * K + k] = __ldcg(t_acc + (int64_t)k * ldt + m);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -323,7 +381,7 @@ __global__ void __launch_bounds__(256) gemv_b_kernel(const __nv_bfloat16* __rest
   if (last) {
     __threadfence();
     float4* z = reinterpret_cast<float4*>(t_acc);
-    for (int e = threadIdx.x; e < tokens * ldt / 4; e += 256) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = threadIdx.x; e < K * ldt / 4; e += 256) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (threadIdx.x == 0) atomicExch(counter, 0u);
   }
 }
@@ -348,17 +406,18 @@ int launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Ar
 }  // namespace
 
 int launch_dec_a(const CUtensorMap& w, const CUtensorMap& x, const DecArgs& a, int splits, cudaStream_t st) {
-  if (a.tokens <= 16) return launch_dec<16, 4, false>(w, x, a, splits, st);
-  if (a.tokens <= 32) return launch_dec<32, 4, false>(w, x, a, splits, st);
-  return launch_dec<64, 4, false>(w, x, a, splits, st);
+  if (a.tokens <= 16) return launch_dec<16, 4, false>(w, x, w, a, splits, st);
+  if (a.tokens <= 32) return launch_dec<32, 4, false>(w, x, w, a, splits, st);
+  return launch_dec<64, 4, false>(w, x, w, a, splits, st);
 }
 
-int launch_dec_b(const CUtensorMap& w, const DecArgs& a, cudaStream_t st) {
+int launch_dec_b(const CUtensorMap& w, const CUtensorMap& t, const CUtensorMap& y, const DecArgs& a,
+                 cudaStream_t st) {
   // K = r_pad <= 256 -> <= 4 k-blocks, all resident (no ring reuse in the fp32-operand path)
   if (a.K > 4 * BK) return (int)cudaErrorInvalidValue;
-  if (a.tokens <= 16) return launch_dec<16, 4, true>(w, w, a, 1, st);
-  if (a.tokens <= 32) return launch_dec<32, 4, true>(w, w, a, 1, st);
-  return launch_dec<64, 4, true>(w, w, a, 1, st);
+  if (a.tokens <= 16) return launch_dec<16, 4, true>(w, t, y, a, 1, st);
+  if (a.tokens <= 32) return launch_dec<32, 4, true>(w, t, y, a, 1, st);
+  return launch_dec<64, 4, true>(w, t, y, a, 1, st);
 }
 
 int launch_gemv_a(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const __nv_bfloat16* x, int64_t ldx,

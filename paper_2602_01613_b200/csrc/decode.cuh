@@ -4,13 +4,13 @@
 // weight-streaming: the weights sit on the MMA M side ("swap-AB"), the tokens
 // on N. Two launches per layer, chained with programmatic dependent launch:
 //
-//   phase A  T_acc[m][k] += sum_j B_in[k][j] x[m][j]      split-K over j, fp32
-//            reductions (red.global.add) into a plan-owned accumulator that
-//            is all-zero at rest;
-//   phase B  y[m][i] = sum_k A_out[i][k] bf16(T_acc[m][k]) — T_acc is read
-//            straight from fp32 global, converted to bf16 into the swizzled
-//            smem operand layout by the (otherwise idle) epilogue warps; the
-//            last CTA to finish reading re-zeroes T_acc.
+//   phase A  T_acc[k][m] += sum_j B_in[k][j] x[m][j]      split-K over j, fp32
+//            vector reductions (red.global.add.v4) into a plan-owned,
+//            kappa-major accumulator that is all-zero at rest;
+//   phase B  y[m][i] = sum_k A_out[i][k] bf16(T_acc[k][m]) — T_acc is TMA-
+//            staged as fp32 and converted to the bf16 SW128 operand by the
+//            (otherwise idle) epilogue warps; y leaves through one TMA store;
+//            the last CTA to finish reading re-zeroes T_acc.
 //
 // Weight tiles are TMA-loaded BEFORE griddepcontrol.wait, so the weight
 // stream of layer l overlaps the tail of the previous kernel.
@@ -40,13 +40,18 @@ struct DecArgs {
   // last-CTA zeroing of act_f32 (phase B)
   unsigned int* counter;
   int64_t zero_elems;
+  // optional timeline (tnl_plan_set_trace): [cta][16] %globaltimer stamps
+  unsigned long long* trace;
 };
 
 // phase A: weights (TMA map `w`, rows=M_rows, K) x activations (TMA map `x`, bf16 tokens x K)
 int launch_dec_a(const CUtensorMap& w, const CUtensorMap& x, const DecArgs& a, int splits,
                  cudaStream_t st);
-// phase B: weights (TMA map `w`) x fp32 activations (a.act_f32), zeroes a.act_f32 at the end
-int launch_dec_b(const CUtensorMap& w, const DecArgs& a, cudaStream_t st);
+// phase B: weights (TMA map `w`) x fp32 accumulator (TMA map `t`: kappa-major [K][64] fp32,
+// box {BN tokens, 64 kappa}); y via TMA store (map `y`: [tokens][rows] bf16, box {128, BN});
+// the last CTA re-zeroes a.act_f32 (a.zero_elems floats)
+int launch_dec_b(const CUtensorMap& w, const CUtensorMap& t, const CUtensorMap& y, const DecArgs& a,
+                 cudaStream_t st);
 
 // CUDA-core GEMV variants (tokens <= 8)
 int launch_gemv_a(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const __nv_bfloat16* x,

@@ -133,7 +133,9 @@ __global__ void __launch_bounds__(192, 1)
             reinterpret_cast<uint4*>(o)[0] = p0;
             reinterpret_cast<uint4*>(o)[1] = p1;
           } else {
-            for (int e = 0; e < ncol; ++e) o[(int64_t)e * args.ldo_j] = __float2bfloat16_rn(v[e]);
+            #pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (e < ncol) o[(int64_t)e * args.ldo_j] = __float2bfloat16_rn(v[e]);
           }
         } else {
           float* o = static_cast<float*>(args.out) + (int64_t)row * args.ldo_i +
@@ -143,10 +145,14 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
               for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
             } else {
-              for (int e = 0; e < ncol; ++e) atomicAdd(o + (int64_t)e * args.ldo_j, v[e]);
+              #pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (e < ncol) atomicAdd(o + (int64_t)e * args.ldo_j, v[e]);
             }
           } else {
-            for (int e = 0; e < ncol; ++e) o[(int64_t)e * args.ldo_j] = v[e];
+            #pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (e < ncol) o[(int64_t)e * args.ldo_j] = v[e];
           }
         }
       }
@@ -215,6 +221,23 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t k, int64_t rows, 
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+int make_tmap_2d(CUtensorMap* map, const void* base, bool f32, int64_t inner, int64_t outer,
+                 int64_t ld, int box_inner, int box_outer, bool swizzle128) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return (int)cudaErrorNotSupported;
+  const int64_t es = f32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * es) % 16) return (int)cudaErrorInvalidValue;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }

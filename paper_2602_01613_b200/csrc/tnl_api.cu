@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -125,8 +126,11 @@ struct TmapKey {
   const void* p;
   int64_t k, rows, ld;
   int box;
+  int kind;  // 0: bf16 SW128 (box 64 x box); else: 1 + f32*2 + sw*4 with box_in in `extra`
+  int extra;
   bool operator==(const TmapKey& o) const {
-    return p == o.p && k == o.k && rows == o.rows && ld == o.ld && box == o.box;
+    return p == o.p && k == o.k && rows == o.rows && ld == o.ld && box == o.box && kind == o.kind &&
+           extra == o.extra;
   }
 };
 
@@ -154,6 +158,7 @@ struct tnl_plan {
   __nv_bfloat16* u0 = nullptr;    //                 (rows_local x R0p)
   int64_t r0p = 0, r1p = 0;
   __nv_bfloat16* wdense = nullptr;  // dense (rows_local x cols)
+  unsigned long long* trace = nullptr;  // optional decode timeline buffer (debug)
   float* tacc = nullptr;            // decode accumulator (kDecMaxM x r_pad), zero at rest
   unsigned int* counter = nullptr;  // decode last-CTA counter, zero at rest
   float* gen_w_out = nullptr;       // generic dense rows slice (fp32) for sharded generic plans
@@ -176,7 +181,7 @@ namespace tnl {
 // Returns 0 and fills *m (by value: cache entries may move on insertion).
 static int get_tmap(tnl_plan* P, CUtensorMap* m, const void* p, int64_t k, int64_t rows,
                     int64_t ld, int box) {
-  TmapKey key{p, k, rows, ld, box};
+  TmapKey key{p, k, rows, ld, box, 0, 0};
   std::lock_guard<std::mutex> g(P->tm_mu);
   for (auto& e : P->tm_cache)
     if (e.first == key) {
@@ -184,6 +189,23 @@ static int get_tmap(tnl_plan* P, CUtensorMap* m, const void* p, int64_t k, int64
       return 0;
     }
   int err = make_tmap_bf16(m, p, k, rows, ld, box);
+  if (err) return err;
+  if (P->tm_cache.size() >= 64) P->tm_cache.erase(P->tm_cache.begin());
+  P->tm_cache.emplace_back(key, *m);
+  return 0;
+}
+
+// Cached general map (make_tmap_2d parameters).
+static int get_tmap2(tnl_plan* P, CUtensorMap* m, const void* p, bool f32, int64_t inner,
+                     int64_t outer, int64_t ld, int box_in, int box_out, bool sw) {
+  TmapKey key{p, inner, outer, ld, box_out, 1 + (f32 ? 2 : 0) + (sw ? 4 : 0), box_in};
+  std::lock_guard<std::mutex> g(P->tm_mu);
+  for (auto& e : P->tm_cache)
+    if (e.first == key) {
+      *m = e.second;
+      return 0;
+    }
+  int err = make_tmap_2d(m, p, f32, inner, outer, ld, box_in, box_out, sw);
   if (err) return err;
   if (P->tm_cache.size() >= 64) P->tm_cache.erase(P->tm_cache.begin());
   P->tm_cache.emplace_back(key, *m);
@@ -1008,32 +1030,41 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
   int err = 0;
   if (M <= 8 && gemv_ok_k(P->r_pad)) {
     err = launch_gemv_a(P->bin, P->cols, (int)P->r_pad, (int)P->cols,
-                        static_cast<const __nv_bfloat16*>(x), ldx, (int)M, P->tacc, P->r_pad, st);
+                        static_cast<const __nv_bfloat16*>(x), ldx, (int)M, P->tacc, kDecMaxM, st);
     if (err) return fail(TNL_ERR_CUDA, "gemv_a launch: %s", cudaGetErrorString((cudaError_t)err));
-    err = launch_gemv_b(P->aout, P->r_pad, (int)rows_local, (int)P->r_pad, P->tacc, P->r_pad, (int)M,
+    err = launch_gemv_b(P->aout, P->r_pad, (int)rows_local, (int)P->r_pad, P->tacc, kDecMaxM, (int)M,
                         static_cast<__nv_bfloat16*>(y), ldy, P->counter, st);
     if (err) return fail(TNL_ERR_CUDA, "gemv_b launch: %s", cudaGetErrorString((cudaError_t)err));
     return TNL_OK;
   }
-  CUtensorMap tw, tx, tw2;
+  CUtensorMap tw, tx, tw2, tt, ty;
   const int bn = pick_bn(M);
+  const int64_t ldk = kDecMaxM;  // kappa-major accumulator row pitch (tokens)
   if ((err = get_tmap(P, &tw, P->bin, P->cols, P->r_pad, P->cols, 128)) ||
       (err = get_tmap(P, &tx, x, P->cols, M, ldx, bn)) ||
       (err = get_tmap(P, &tw2, P->aout, P->r_pad, rows_local, P->r_pad, 128)))
     return fail(TNL_ERR_CUDA, "tensor map (decode) failed: %d", err);
+  if ((err = get_tmap2(P, &tt, P->tacc, true, ldk, P->r_pad, ldk, bn, 64, false)) ||
+      (err = get_tmap2(P, &ty, y, false, rows_local, M, ldy, 128, bn, false)))
+    return fail(TNL_ERR_CUDA, "tensor map (decode accumulator / y) failed: %d", err);
   DecArgs a;
   memset(&a, 0, sizeof a);
   a.M_rows = (int32_t)P->r_pad;
   a.tokens = (int32_t)M;
   a.K = (int32_t)P->cols;
   const int total_kb = (int)((P->cols + 63) / 64);
-  int splits = choose_splits((P->r_pad + 127) / 128, P->cols);
-  a.kb_per_split = (total_kb + splits - 1) / splits;
-  splits = (total_kb + a.kb_per_split - 1) / a.kb_per_split;
+  // K blocks per split: fewer partials -> less reduction traffic to drain before phase B
+  static const int kb_env = [] {
+    const char* e = getenv("TNL_DEC_KB");
+    return e ? atoi(e) : 0;
+  }();
+  a.kb_per_split = kb_env > 0 ? kb_env : 4;
+  int splits = (total_kb + a.kb_per_split - 1) / a.kb_per_split;
   a.out = P->tacc;
-  a.ldo_i = 1;
-  a.ldo_j = P->r_pad;
+  a.ldo_i = ldk;
+  a.ldo_j = 1;
   a.out_f32_atomic = 1;
+  a.trace = P->trace;
   if ((err = launch_dec_a(tw, tx, a, splits, st)))
     return fail(TNL_ERR_CUDA, "decode phase A launch: %s", cudaGetErrorString((cudaError_t)err));
   DecArgs b;
@@ -1043,14 +1074,15 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
   b.K = (int32_t)P->r_pad;
   b.kb_per_split = (int32_t)((P->r_pad + 63) / 64);
   b.act_f32 = P->tacc;
-  b.act_ld = P->r_pad;
+  b.act_ld = ldk;
   b.out = y;
   b.ldo_i = 1;
   b.ldo_j = ldy;
   b.out_f32_atomic = 0;
   b.counter = P->counter;
-  b.zero_elems = M * P->r_pad;
-  if ((err = launch_dec_b(tw2, b, st)))
+  b.zero_elems = P->r_pad * ldk;
+  b.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
+  if ((err = launch_dec_b(tw2, tt, ty, b, st)))
     return fail(TNL_ERR_CUDA, "decode phase B launch: %s", cudaGetErrorString((cudaError_t)err));
   return TNL_OK;
 }
@@ -1066,7 +1098,8 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
   __nv_bfloat16* t1 = reinterpret_cast<__nv_bfloat16*>(w + o_b1);
   const int64_t rows_local = P->row_end - P->row_begin;
   const bool swap = M <= kSwapMaxM;
-  if (M <= kDecMaxM && P->tacc && P->r_pad <= 256 && !(P->flags & TNL_PLAN_NO_DECODE))
+  if (M <= kDecMaxM && P->tacc && P->r_pad <= 256 && !(P->flags & TNL_PLAN_NO_DECODE) &&
+      !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0)
     return forward_decode(P, x, M, ldx, y, ldy, st);
   tnl_status s;
   if (P->family == TNL_FAMILY_DENSE) {
@@ -1141,6 +1174,12 @@ extern "C" {
 int tnl_abi_version(void) { return TNL_ABI_VERSION; }
 const char* tnl_last_error(void) { return g_err.c_str(); }
 int64_t tnl_launch_count(int32_t reset) { return launch_count(reset != 0); }
+
+tnl_status tnl_plan_set_trace(tnl_plan* plan, void* device_buffer) {
+  if (!plan) return fail(TNL_ERR_ARG, "null plan");
+  plan->trace = static_cast<unsigned long long*>(device_buffer);
+  return TNL_OK;
+}
 
 tnl_status tnl_plan_create(const tnl_layer_desc* desc, int32_t compute_dtype, int64_t max_m,
                            int32_t flags, tnl_plan** out) {
