@@ -1,0 +1,114 @@
+"""Multi-GPU partitioning of the TN-linear forward (one process per GPU).
+
+Three ways to spread the work:
+
+* replicas      — independent decode streams: every rank holds the whole
+                  (small) TN layer and serves its own tokens. No collective.
+* token-sharded — prefill: rank g takes tokens [g*M/G, (g+1)*M/G). No collective.
+* output-sharded — prefill with one exchange step: rank g owns the output rows
+                  of its slice of the leading output mode i0 (the row range is
+                  contiguous because row modes come first,
+                  tn_decompositions.py:59-63) and computes only those; the
+                  input side up to the cut is recomputed on every rank (r_cut
+                  per token). One ``all_gather_into_tensor`` (NCCL over NVLink)
+                  assembles y; the gathered layout is [G][M][rows/G].
+
+The local compute is the C-ABI forward of a row-restricted plan
+(``tnl_plan_create_rows``). For CPU tests the compute callable can be
+injected (the gloo tests pass the oracle); the product path has no CPU
+compute.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from .errors import ShapeError
+from .layer import CompressedLayer
+
+
+def output_shard_ranges(mode_shape, row_mode_count: int, world: int) -> list[tuple[int, int]]:
+    """Row range per rank: slices of the leading output mode i0 when it divides,
+    else equal contiguous row blocks (rows must then divide by world)."""
+    ms = tuple(mode_shape)
+    rows = math.prod(ms[:row_mode_count])
+    n0 = ms[0]
+    if n0 % world == 0:
+        per = rows // world  # = (n0 / world) * prod(ms[1:rm])
+    elif rows % world == 0:
+        per = rows // world
+    else:
+        raise ShapeError(f"{rows} output rows (leading mode {n0}) cannot be split over {world} ranks")
+    return [(g * per, (g + 1) * per) for g in range(world)]
+
+
+def token_shard_range(m: int, rank: int, world: int) -> tuple[int, int]:
+    per = (m + world - 1) // world
+    lo = min(m, rank * per)
+    return lo, min(m, lo + per)
+
+
+class OutputShardedLayer:
+    """Output-mode-sharded forward with one all-gather (prefill / large M)."""
+
+    def __init__(self, layer: CompressedLayer, group=None, dtype=torch.bfloat16, device=None,
+                 local_forward: Callable | None = None):
+        self.layer = layer
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.ranges = output_shard_ranges(layer.mode_shape, layer.row_mode_count, self.world)
+        self.row_range = self.ranges[self.rank]
+        self.rows, self.cols = layer.matrix_shape
+        self.dtype = dtype
+        if local_forward is None:
+            plan = layer.plan(dtype, device, row_range=self.row_range)
+            local_forward = plan.forward
+        self.local_forward = local_forward
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        m = x.shape[0]
+        per = self.row_range[1] - self.row_range[0]
+        y_local = self.local_forward(x)  # (M, rows/G)
+        flat = torch.empty((self.world * m, per), dtype=y_local.dtype, device=y_local.device)
+        dist.all_gather_into_tensor(flat, y_local.contiguous(), group=self.group)
+        gathered = flat.view(self.world, m, per)
+        y = out if out is not None else torch.empty((m, self.rows), dtype=y_local.dtype, device=y_local.device)
+        # [G][M][rows/G] -> (M, rows): rank g's slice lands in columns [g*per, (g+1)*per)
+        y.view(m, self.world, per).copy_(gathered.permute(1, 0, 2))
+        return y
+
+    __call__ = forward
+
+
+class TokenShardedLayer:
+    """Token-sharded forward: rank g computes its own token block; no collective
+    (``gather=True`` all-gathers the blocks, for checking)."""
+
+    def __init__(self, layer: CompressedLayer, group=None, dtype=torch.bfloat16, device=None,
+                 local_forward: Callable | None = None):
+        self.layer = layer
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if local_forward is None:
+            local_forward = layer.plan(dtype, device).forward
+        self.local_forward = local_forward
+
+    def forward(self, x_full: torch.Tensor, gather: bool = False) -> torch.Tensor:
+        m = x_full.shape[0]
+        if m % self.world and gather:
+            raise ShapeError("gather=True needs M divisible by the world size")
+        lo, hi = token_shard_range(m, self.rank, self.world)
+        y = self.local_forward(x_full[lo:hi])
+        if not gather:
+            return y
+        parts = torch.empty((self.world * y.shape[0],) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)
+        dist.all_gather_into_tensor(parts, y.contiguous(), group=self.group)
+        return parts
+
+    __call__ = forward
