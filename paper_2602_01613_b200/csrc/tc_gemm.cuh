@@ -39,4 +39,11 @@ int make_tmap_2d(CUtensorMap* map, const void* base, bool f32, int64_t inner, in
 int launch_tc_gemm(const CUtensorMap& a, const CUtensorMap& b, const TcGemmArgs& args, int bn,
                    int splits, bool pdl, cudaStream_t stream);
 
+// Persistent variant (prefill): grid = min(tiles, max_ctas); bn in {64,128,256}.
+// out_mode TC_OUT_BF16 stores through TMA map `c` (out: M x N bf16, box {64, 128},
+// 128B swizzle); TC_OUT_F32_ATOMIC reduces into args.out (row-major fp32, ldo_i).
+int launch_tc_gemm_persistent(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                              const TcGemmArgs& args, int bn, int splits, int max_ctas, bool pdl,
+                              cudaStream_t st);
+
 }  // namespace tnl

@@ -1087,6 +1087,42 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
   return TNL_OK;
 }
 
+// Large-M GEMM step on the persistent kernel: out (M x N) = X (M x K) . W (N x K)^T.
+// out_f32: fp32 split-K reductions into `out` (zeroed here); else bf16 via TMA store.
+static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void* W, int64_t ldw,
+                            int64_t M, int64_t N, int64_t K, void* out, int64_t ldo, bool out_f32,
+                            int splits, cudaStream_t st) {
+  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  CUtensorMap ta, tb, tc;
+  int err;
+  if ((err = get_tmap(P, &ta, X, K, M, ldx, 128)) || (err = get_tmap(P, &tb, W, K, N, ldw, bn)))
+    return fail(TNL_ERR_CUDA, "tensor map (persistent step) failed: %d", err);
+  TcGemmArgs a;
+  memset(&a, 0, sizeof a);
+  a.M = (int32_t)M;
+  a.N = (int32_t)N;
+  a.K = (int32_t)K;
+  const int total_kb = (int)((K + 63) / 64);
+  a.kb_per_split = (total_kb + splits - 1) / splits;
+  splits = (total_kb + a.kb_per_split - 1) / a.kb_per_split;
+  a.out = out;
+  a.ldo_i = ldo;
+  a.ldo_j = 1;
+  if (out_f32) {
+    a.out_mode = TC_OUT_F32_ATOMIC;
+    if (cudaMemsetAsync(out, 0, sizeof(float) * M * ldo, st) != cudaSuccess)
+      return fail(TNL_ERR_CUDA, "memset failed");
+    tc = ta;  // unused
+  } else {
+    a.out_mode = TC_OUT_BF16;
+    if ((err = get_tmap2(P, &tc, out, false, N, M, ldo, 64, 128, true)))
+      return fail(TNL_ERR_CUDA, "tensor map (output) failed: %d", err);
+  }
+  err = launch_tc_gemm_persistent(ta, tb, tc, a, bn, splits, 148, true, st);
+  if (err) return fail(TNL_ERR_CUDA, "persistent gemm launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
+}
+
 static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y, int64_t ldy,
                              void* ws, size_t ws_bytes, cudaStream_t st) {
   size_t o_f32, o_b0, o_b1;
@@ -1103,11 +1139,41 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     return forward_decode(P, x, M, ldx, y, ldy, st);
   tnl_status s;
   if (P->family == TNL_FAMILY_DENSE) {
+    if (!swap && !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0)
+      return tc_step_p(P, x, ldx, P->wdense, P->cols, M, rows_local, P->cols, y, ldy, false, 1, st);
     return tc_step(P, x, ldx, P->wdense, P->cols, M, rows_local, P->cols, y, ldy, false, swap, 1, st);
   }
   // first step: T = X . Win^T  (Win = B_in or U1^T), K = cols
   const __nv_bfloat16* win = P->plan_large == TNL_PLAN_CHAIN ? P->u1t : P->bin;
   const int64_t k1 = P->plan_large == TNL_PLAN_CHAIN ? P->r1p : P->r_pad;
+  const __nv_bfloat16* wout = P->plan_large == TNL_PLAN_CHAIN ? P->u0 : P->aout;
+  const bool y_tma_ok = !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0;
+  if (!swap && y_tma_ok) {
+    // prefill: persistent steps. Step 1 has few output tiles (N = r_pad): split K so
+    // the grid covers the SMs, reducing in fp32, then round T to bf16 once.
+    const int64_t tiles1 = ((M + 127) / 128) * ((k1 + 255) / 256);
+    const int64_t kb1 = (P->cols + 63) / 64;
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb1 / 8));
+    if (splits > 1) {
+      s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, tf, k1, true, splits, st);
+      if (s) return s;
+      f32_to_bf16_2d<<<grid_for(M * k1), 256, 0, st>>>(tf, k1, t0, k1, M, k1);
+      count_launch();
+    } else {
+      s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, 1, st);
+      if (s) return s;
+    }
+    const __nv_bfloat16* tcur = t0;
+    int64_t kc = k1;
+    if (P->plan_large == TNL_PLAN_CHAIN) {  // T2 = T1 . G^T
+      s = tc_step_p(P, t0, k1, P->gmat, P->r1p, M, P->r0p, P->r1p, t1, P->r0p, false, 1, st);
+      if (s) return s;
+      tcur = t1;
+      kc = P->r0p;
+    }
+    return tc_step_p(P, tcur, kc, wout, kc, M, rows_local, kc, y, ldy, false, 1, st);
+  }
+  // first step: T = X . Win^T  (Win = B_in or U1^T), K = cols
   if (swap) {
     const int64_t tiles = (k1 + 127) / 128;
     const int splits = choose_splits(tiles, P->cols);
@@ -1134,7 +1200,6 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     tcur = t1;
     kc = P->r0p;
   }
-  const __nv_bfloat16* wout = P->plan_large == TNL_PLAN_CHAIN ? P->u0 : P->aout;
   return tc_step(P, tcur, kc, wout, kc, M, rows_local, kc, y, ldy, false, swap, 1, st);
 }
 
