@@ -226,7 +226,7 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t k, int64_t rows, 
 }
 
 int make_tmap_2d(CUtensorMap* map, const void* base, bool f32, int64_t inner, int64_t outer,
-                 int64_t ld, int box_inner, int box_outer, bool swizzle128) {
+                 int64_t ld, int box_inner, int box_outer, int swizzle_bytes) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return (int)cudaErrorNotSupported;
   const int64_t es = f32 ? 4 : 2;
@@ -237,7 +237,10 @@ int make_tmap_2d(CUtensorMap* map, const void* base, bool f32, int64_t inner, in
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                  : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                  : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                        : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }

@@ -31,9 +31,9 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t k, int64_t rows, 
                    int box_rows);
 
 // General 2-D map: `outer` rows of `inner` elements (bf16 or fp32), row pitch `ld`
-// elements, box (box_inner x box_outer), 128B swizzle or none.
+// elements, box (box_inner x box_outer), swizzle 0 / 32 / 64 / 128 bytes.
 int make_tmap_2d(CUtensorMap* map, const void* base, bool f32, int64_t inner, int64_t outer,
-                 int64_t ld, int box_inner, int box_outer, bool swizzle128);
+                 int64_t ld, int box_inner, int box_outer, int swizzle_bytes);
 
 // bn in {16,32,64,128,256}; splits >= 1 (grid.z). Returns cudaError_t as int.
 int launch_tc_gemm(const CUtensorMap& a, const CUtensorMap& b, const TcGemmArgs& args, int bn,

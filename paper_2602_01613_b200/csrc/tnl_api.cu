@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "../../include/tnl.h"
+#include "chain.cuh"
 #include "common.cuh"
 #include "decode.cuh"
 #include "generic.cuh"
@@ -159,6 +160,12 @@ struct tnl_plan {
   int64_t r0p = 0, r1p = 0;
   __nv_bfloat16* wdense = nullptr;  // dense (rows_local x cols)
   unsigned long long* trace = nullptr;  // optional decode timeline buffer (debug)
+  // tcgen05 core-by-core input chain (two-mode TT/TR input side)
+  bool chain_ok = false;
+  bool tucker_chain = false;  // Tucker-2 three-step chain plan
+  __nv_bfloat16* chain_d = nullptr;  // Dp [(alpha, c_pad)][n_b]
+  __nv_bfloat16* chain_c = nullptr;  // Cp [(j_a, b_pad)][c_pad]
+  int32_t ch_na = 0, ch_nb = 0, ch_r0 = 0, ch_c = 0, ch_cpad = 0, ch_b = 0, ch_bpad = 0;
   float* tacc = nullptr;            // decode accumulator (kDecMaxM x r_pad), zero at rest
   unsigned int* counter = nullptr;  // decode last-CTA counter, zero at rest
   float* gen_w_out = nullptr;       // generic dense rows slice (fp32) for sharded generic plans
@@ -197,8 +204,8 @@ static int get_tmap(tnl_plan* P, CUtensorMap* m, const void* p, int64_t k, int64
 
 // Cached general map (make_tmap_2d parameters).
 static int get_tmap2(tnl_plan* P, CUtensorMap* m, const void* p, bool f32, int64_t inner,
-                     int64_t outer, int64_t ld, int box_in, int box_out, bool sw) {
-  TmapKey key{p, inner, outer, ld, box_out, 1 + (f32 ? 2 : 0) + (sw ? 4 : 0), box_in};
+                     int64_t outer, int64_t ld, int box_in, int box_out, int sw) {
+  TmapKey key{p, inner, outer, ld, box_out, 1 + (f32 ? 1 : 0) + 2 * sw, box_in};
   std::lock_guard<std::mutex> g(P->tm_mu);
   for (auto& e : P->tm_cache)
     if (e.first == key) {
@@ -818,6 +825,23 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     else
       large = TNL_PLAN_CUT;
   }
+  // core-by-core tcgen05 chain for a two-mode TT/TR input side (cores C = core rm, D = core d-1)
+  if (tc_ok && (P->family == TNL_FAMILY_TT || P->family == TNL_FAMILY_TR) && d - rm == 2) {
+    const int64_t c = r[d - 1], b = r[rm], r0 = r[d], na = ms[rm], nb = ms[d - 1];
+    const int64_t cpad = c <= 16 ? 16 : (c <= 32 ? 32 : (c <= 64 ? 64 : 0));
+    const int64_t bpad = round_up(b, 16);
+    if (cpad && nb % 16 == 0 && r0 * cpad <= 256 && r0 * bpad <= 256) {
+      P->chain_ok = true;
+      P->ch_na = (int32_t)na;
+      P->ch_nb = (int32_t)nb;
+      P->ch_r0 = (int32_t)r0;
+      P->ch_c = (int32_t)c;
+      P->ch_cpad = (int32_t)cpad;
+      P->ch_b = (int32_t)b;
+      P->ch_bpad = (int32_t)bpad;
+      if (flags & TNL_PLAN_CHAIN) large = TNL_PLAN_CHAIN;
+    }
+  }
   P->plan_large = large;
   P->plan_small = large;
   P->decode_max_m = (tc_ok && P->family != TNL_FAMILY_DENSE && round_up(P->r_cut, 16) <= 256 &&
@@ -849,7 +873,15 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     off_w = bytes;
     bytes += round_up(rows_local * P->cols * 2, 256);
   }
-  if (large == TNL_PLAN_CHAIN) {
+  size_t off_chd = 0, off_chc = 0;
+  if (P->chain_ok) {
+    off_chd = bytes;
+    bytes += round_up((int64_t)P->ch_r0 * P->ch_cpad * P->ch_nb * 2, 256);
+    off_chc = bytes;
+    bytes += round_up((int64_t)P->ch_na * P->ch_bpad * P->ch_cpad * 2, 256);
+  }
+  P->tucker_chain = large == TNL_PLAN_CHAIN && tucker2;
+  if (P->tucker_chain) {
     P->r1p = round_up(r[1], 16);
     P->r0p = round_up(r[0], 16);
     off_u1 = bytes;
@@ -896,7 +928,26 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     cudaFree(fa);
     if (s2 != TNL_OK) return s2;
   }
-  if (large == TNL_PLAN_CHAIN) {
+  if (P->chain_ok) {
+    const int64_t na = P->ch_na, nb = P->ch_nb, r0 = P->ch_r0, c = P->ch_c, cp = P->ch_cpad,
+                  b = P->ch_b, bp = P->ch_bpad;
+    std::vector<__nv_bfloat16> hd(r0 * cp * nb, __float2bfloat16(0.f)), hc(na * bp * cp, __float2bfloat16(0.f));
+    const std::vector<float>& D = host[d - 1];  // permuted [alpha][j][c]
+    const std::vector<float>& C = host[rm];     // natural (b, n_a, c)
+    for (int64_t al = 0; al < r0; ++al)
+      for (int64_t j = 0; j < nb; ++j)
+        for (int64_t cc = 0; cc < c; ++cc)
+          hd[(al * cp + cc) * nb + j] = __float2bfloat16(D[(al * nb + j) * c + cc]);
+    for (int64_t ja = 0; ja < na; ++ja)
+      for (int64_t bb = 0; bb < b; ++bb)
+        for (int64_t cc = 0; cc < c; ++cc)
+          hc[(ja * bp + bb) * cp + cc] = __float2bfloat16(C[(bb * na + ja) * c + cc]);
+    P->chain_d = reinterpret_cast<__nv_bfloat16*>(base + off_chd);
+    P->chain_c = reinterpret_cast<__nv_bfloat16*>(base + off_chc);
+    CUDA_TRY(cudaMemcpy(P->chain_d, hd.data(), hd.size() * 2, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(P->chain_c, hc.data(), hc.size() * 2, cudaMemcpyHostToDevice));
+  }
+  if (large == TNL_PLAN_CHAIN && tucker2) {
     // Tucker-2: U1^T (R1p x cols), G (R0p x R1p), U0 rows (rows_local x R0p)
     P->u1t = reinterpret_cast<__nv_bfloat16*>(base + off_u1);
     P->gmat = reinterpret_cast<__nv_bfloat16*>(base + off_g);
@@ -944,7 +995,7 @@ static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b
     return bytes;
   }
   int64_t kmax = P->r_pad;
-  if (P->plan_large == TNL_PLAN_CHAIN) kmax = std::max(P->r0p, P->r1p);
+  if (P->tucker_chain) kmax = std::max(P->r0p, P->r1p);
   *o_f32 = take(sizeof(float) * M * kmax);
   *o_b0 = take(2 * M * kmax);
   *o_b1 = take(2 * M * kmax);
@@ -1013,6 +1064,38 @@ static int choose_splits(int64_t tiles, int64_t K) {
   return (int)std::min<int64_t>(s, total_kb);
 }
 
+// TT/TR input chain kernel: T[m][kappa] at out (strides s_m, s_k), bf16 or fp32 reductions.
+static tnl_status chain_in(tnl_plan* P, const void* x, int64_t ldx, int64_t M, void* out, int64_t s_m,
+                           int64_t s_k, bool f32_atomic, int splits, cudaStream_t st) {
+  CUtensorMap tx, td, tcm;
+  int err;
+  const int n1 = P->ch_r0 * P->ch_cpad;
+  if ((err = get_tmap2(P, &tx, x, false, P->cols, M, ldx, 16, 128, 32)) ||
+      (err = get_tmap2(P, &td, P->chain_d, false, P->ch_nb, n1, P->ch_nb, 16, n1, 32)) ||
+      (err = get_tmap2(P, &tcm, P->chain_c, false, P->ch_cpad, (int64_t)P->ch_na * P->ch_bpad, P->ch_cpad,
+                       P->ch_cpad, P->ch_bpad, 2 * P->ch_cpad)))
+    return fail(TNL_ERR_CUDA, "tensor map (chain) failed: %d", err);
+  ChainArgs a;
+  memset(&a, 0, sizeof a);
+  a.M = (int32_t)M;
+  a.n_a = P->ch_na;
+  a.n_b = P->ch_nb;
+  a.r0 = P->ch_r0;
+  a.c = P->ch_c;
+  a.c_pad = P->ch_cpad;
+  a.b = P->ch_b;
+  a.b_pad = P->ch_bpad;
+  a.ja_per_split = (P->ch_na + splits - 1) / splits;
+  splits = (P->ch_na + a.ja_per_split - 1) / a.ja_per_split;
+  a.out = out;
+  a.s_m = s_m;
+  a.s_k = s_k;
+  a.out_f32_atomic = f32_atomic ? 1 : 0;
+  if ((err = launch_chain_in2(tx, td, tcm, a, splits, st)))
+    return fail(TNL_ERR_CUDA, "chain kernel launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
+}
+
 static constexpr int64_t kDecMaxM = 64;  // decode path (plan-owned accumulator capacity)
 
 static bool gemv_ok_k(int64_t K) {
@@ -1028,7 +1111,8 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
                                  int64_t ldy, cudaStream_t st) {
   const int64_t rows_local = P->row_end - P->row_begin;
   int err = 0;
-  if (M <= 8 && gemv_ok_k(P->r_pad)) {
+  const bool use_chain = P->plan_large == TNL_PLAN_CHAIN && P->chain_ok;
+  if (M <= 8 && gemv_ok_k(P->r_pad) && !use_chain) {
     err = launch_gemv_a(P->bin, P->cols, (int)P->r_pad, (int)P->cols,
                         static_cast<const __nv_bfloat16*>(x), ldx, (int)M, P->tacc, kDecMaxM, st);
     if (err) return fail(TNL_ERR_CUDA, "gemv_a launch: %s", cudaGetErrorString((cudaError_t)err));
@@ -1044,8 +1128,8 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
       (err = get_tmap(P, &tx, x, P->cols, M, ldx, bn)) ||
       (err = get_tmap(P, &tw2, P->aout, P->r_pad, rows_local, P->r_pad, 128)))
     return fail(TNL_ERR_CUDA, "tensor map (decode) failed: %d", err);
-  if ((err = get_tmap2(P, &tt, P->tacc, true, ldk, P->r_pad, ldk, bn, 64, false)) ||
-      (err = get_tmap2(P, &ty, y, false, rows_local, M, ldy, 128, bn, false)))
+  if ((err = get_tmap2(P, &tt, P->tacc, true, ldk, P->r_pad, ldk, bn, 64, 0)) ||
+      (err = get_tmap2(P, &ty, y, false, rows_local, M, ldy, 128, bn, 0)))
     return fail(TNL_ERR_CUDA, "tensor map (decode accumulator / y) failed: %d", err);
   DecArgs a;
   memset(&a, 0, sizeof a);
@@ -1065,8 +1149,13 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
   a.ldo_j = 1;
   a.out_f32_atomic = 1;
   a.trace = P->trace;
-  if ((err = launch_dec_a(tw, tx, a, splits, st)))
+  if (use_chain) {
+    // core-by-core input chain, j_a split across CTAs, fp32 reductions into the accumulator
+    tnl_status cs = chain_in(P, x, ldx, M, P->tacc, 1, ldk, true, std::min(16, P->ch_na), st);
+    if (cs) return cs;
+  } else if ((err = launch_dec_a(tw, tx, a, splits, st))) {
     return fail(TNL_ERR_CUDA, "decode phase A launch: %s", cudaGetErrorString((cudaError_t)err));
+  }
   DecArgs b;
   memset(&b, 0, sizeof b);
   b.M_rows = (int32_t)rows_local;
@@ -1115,7 +1204,7 @@ static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void*
     tc = ta;  // unused
   } else {
     a.out_mode = TC_OUT_BF16;
-    if ((err = get_tmap2(P, &tc, out, false, N, M, ldo, 64, 128, true)))
+    if ((err = get_tmap2(P, &tc, out, false, N, M, ldo, 64, 128, 128)))
       return fail(TNL_ERR_CUDA, "tensor map (output) failed: %d", err);
   }
   err = launch_tc_gemm_persistent(ta, tb, tc, a, bn, splits, 148, true, st);
@@ -1144,9 +1233,28 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     return tc_step(P, x, ldx, P->wdense, P->cols, M, rows_local, P->cols, y, ldy, false, swap, 1, st);
   }
   // first step: T = X . Win^T  (Win = B_in or U1^T), K = cols
-  const __nv_bfloat16* win = P->plan_large == TNL_PLAN_CHAIN ? P->u1t : P->bin;
-  const int64_t k1 = P->plan_large == TNL_PLAN_CHAIN ? P->r1p : P->r_pad;
-  const __nv_bfloat16* wout = P->plan_large == TNL_PLAN_CHAIN ? P->u0 : P->aout;
+  if (P->plan_large == TNL_PLAN_CHAIN && P->chain_ok && !swap &&
+      !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0) {
+    // TT/TR core-by-core input chain -> T (bf16, or fp32 reductions when j_a is split), then
+    // the output panel GEMM. K of step 2 = r_cut (TMA zero-fills the padded columns).
+    const int64_t tiles_m = (M + 127) / 128;
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>(P->ch_na / 4, 148 / tiles_m));
+    if (splits > 1) {
+      if (cudaMemsetAsync(tf, 0, sizeof(float) * M * P->r_pad, st) != cudaSuccess)
+        return fail(TNL_ERR_CUDA, "memset failed");
+      s = chain_in(P, x, ldx, M, tf, P->r_pad, 1, true, splits, st);
+      if (s) return s;
+      f32_to_bf16_2d<<<grid_for(M * P->r_pad), 256, 0, st>>>(tf, P->r_pad, t0, P->r_pad, M, P->r_pad);
+      count_launch();
+    } else {
+      s = chain_in(P, x, ldx, M, t0, P->r_pad, 1, false, 1, st);
+      if (s) return s;
+    }
+    return tc_step_p(P, t0, P->r_pad, P->aout, P->r_pad, M, rows_local, P->r_cut, y, ldy, false, 1, st);
+  }
+  const __nv_bfloat16* win = P->tucker_chain ? P->u1t : P->bin;
+  const int64_t k1 = P->tucker_chain ? P->r1p : P->r_pad;
+  const __nv_bfloat16* wout = P->tucker_chain ? P->u0 : P->aout;
   const bool y_tma_ok = !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0;
   if (!swap && y_tma_ok) {
     // prefill: persistent steps. Step 1 has few output tiles (N = r_pad): split K so
@@ -1165,7 +1273,7 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     }
     const __nv_bfloat16* tcur = t0;
     int64_t kc = k1;
-    if (P->plan_large == TNL_PLAN_CHAIN) {  // T2 = T1 . G^T
+    if (P->tucker_chain) {  // T2 = T1 . G^T
       s = tc_step_p(P, t0, k1, P->gmat, P->r1p, M, P->r0p, P->r1p, t1, P->r0p, false, 1, st);
       if (s) return s;
       tcur = t1;
@@ -1194,7 +1302,7 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
   }
   const __nv_bfloat16* tcur = t0;
   int64_t kc = k1;
-  if (P->plan_large == TNL_PLAN_CHAIN) {  // T2 = T1 . G^T   (R0p x R1p)
+  if (P->tucker_chain) {  // T2 = T1 . G^T   (R0p x R1p)
     s = tc_step(P, t0, k1, P->gmat, P->r1p, M, P->r0p, P->r1p, t1, P->r0p, false, swap, 1, st);
     if (s) return s;
     tcur = t1;

@@ -110,8 +110,10 @@ def test_cfg1_tt_fp32():
     for flags in (tnl.PLAN_AUTO, tnl.PLAN_GENERIC):
         y = run(layer, x, torch.float32, flags)
         assert rel(ref, y) <= FP32_TOL
-    # bf16 variant of cfg1
+    # bf16 variant of cfg1 (merged cut and the tcgen05 core-by-core chain)
     check_bf16(L, 16, seed=11)
+    check_bf16(L, 16, seed=11, flags=tnl.PLAN_CHAIN)
+    check_bf16(L, 300, seed=12, flags=tnl.PLAN_CHAIN)
 
 
 @pytest.mark.parametrize("R", [64, 128, 256])
@@ -133,14 +135,17 @@ def test_cfg2_tr2(ab, m):
 @pytest.mark.parametrize("m", [1, 16, 64, 129])
 def test_cfg2_tr4(r, m):
     L = O.synthetic_layer("tr", (64, 80, 64, 80), 2, (r, r, r, r), seed=22_000 + r)
-    check_bf16(L, m, seed=22_999 + m)
+    for flags in (tnl.PLAN_AUTO, tnl.PLAN_CHAIN):
+        check_bf16(L, m, seed=22_999 + m, flags=flags)
 
 
 @pytest.mark.parametrize("which", ["gate", "down"])
 def test_cfg3_mlp_tt(which):
     ms = (160, 160, 64, 80) if which == "gate" else (64, 80, 160, 160)
     L = O.synthetic_layer("tt", ms, 2, (64, 64, 64), seed=30_000 + len(which))
-    check_bf16(L, 256, seed=30_999)
+    for flags in (tnl.PLAN_AUTO, tnl.PLAN_CHAIN):
+        for m in (256, 40):
+            check_bf16(L, m, seed=30_999 + m, flags=flags)
 
 
 def test_cfg3_full_size_properties():
@@ -267,3 +272,10 @@ def test_stack_graph_replay_matches_eager():
     torch.cuda.synchronize()
     d = (st.y_host.float() - ye.cpu().float()).norm() / ye.cpu().float().norm()
     assert float(d) < 1e-2
+
+
+def test_chain_plan_selected_for_two_mode_inputs():
+    L = O.synthetic_layer("tr", (64, 80, 64, 80), 2, (16, 16, 16, 16), seed=47_000)
+    layer, _ = to_layer(L, round_bf16=True)
+    assert layer.plan(torch.bfloat16, flags=tnl.PLAN_CHAIN).info["plan_large_name"] == "chain"
+    assert layer.plan(torch.bfloat16).info["plan_large_name"] == "cut"
