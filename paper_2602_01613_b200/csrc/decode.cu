@@ -39,8 +39,12 @@ struct DecSmem {
   static constexpr size_t bytes = 1024 + (size_t)STAGES * (A_STAGE + B_STAGE + F_STAGE) + Y_BYTES + 512;
 };
 
+// 2 non-epilogue warps (TMA, MMA) + 8 epilogue warps: two warps per TMEM lane
+// quarter split the token columns, halving the per-thread reduction / store count.
+constexpr int DEC_THREADS = 320, DEC_EPI = 256;
+
 template <int BN, int STAGES, bool ACT_F32>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(DEC_THREADS, 1)
     dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                const __grid_constant__ CUtensorMap tmY, const DecArgs a) {
   using SM = DecSmem<BN, STAGES, ACT_F32>;
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else {
-    const int et = threadIdx.x - 64;  // 0..127
+    const int et = threadIdx.x - 64;  // 0..255
     pdl_wait();
     if (et == 0) TRACE(6);
     if constexpr (ACT_F32) {
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&stg[i], 0);
         const float* src = sF + i * (F_STAGE / 4);
         uint8_t* dst = sB + i * B_STAGE;
-        for (int e = et; e < BN * 8; e += 128) {
+        for (int e = et; e < BN * 8; e += DEC_EPI) {
           const int r = e % BN, c = e / BN;  // token r, kappa chunk c
           float f[8];
 #pragma unroll
@@ -171,7 +175,7 @@ __global__ void __launch_bounds__(192, 1)
           *reinterpret_cast<uint4*>(dst + sw128_off(r, c)) = p;
         }
         fence_proxy_async_smem();
-        named_bar(1, 128);
+        named_bar(1, DEC_EPI);
         if (et == 0) mbar_arrive(&full[i]);
       }
       if (et == 0) TRACE(7);
@@ -183,8 +187,10 @@ __global__ void __launch_bounds__(192, 1)
     const int lrow = q * 32 + lane_id();
     const int row = tile_m * BM + lrow;
     const bool row_ok = row < a.M_rows;
+    constexpr int HALF = BN >= 32 ? BN / 2 : BN;
+    const int c_begin = ((warp - 2) >> 2) * HALF;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
+    for (int c = c_begin; c < c_begin + HALF && c < BN; c += 16) {
       float v[16];
       tmem_ld16(tmem + ((q * 32) << 16) + c, v);
       if constexpr (ACT_F32) {
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     if constexpr (ACT_F32) {
       fence_proxy_async_smem();
-      named_bar(1, 128);
+      named_bar(1, DEC_EPI);
       if (et == 0) {
         tma_store_2d(&tmY, sY, tile_m * BM, 0);
         tma_store_commit();
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(flagbar, 0);  // producer lane wrote last_flag before arriving
         if (*last_flag) {
           float4* z = reinterpret_cast<float4*>(const_cast<float*>(a.act_f32));
-          for (int64_t e = et; e < a.zero_elems / 4; e += 128) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int64_t e = et; e < a.zero_elems / 4; e += DEC_EPI) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (et == 0) atomicExch(a.counter, 0u);
         }
       }
@@ -245,7 +251,7 @@ int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& y,
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.M_rows + BM - 1) / BM, 1, splits);
-  cfg.blockDim = dim3(192, 1, 1);
+  cfg.blockDim = dim3(DEC_THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
