@@ -134,7 +134,10 @@ TNL_API tnl_status tnl_plan_query(const tnl_plan* plan, tnl_plan_info* info);
 TNL_API tnl_status tnl_workspace_size(const tnl_plan* plan, int64_t m, size_t* bytes);
 
 /* y[m, r] (row stride ldy, r in [row_begin,row_end)) = sum_c x[m, c] W[r, c].
- * x, y, workspace: device pointers; element type = the plan's compute dtype. */
+ * x, y, workspace: device pointers; element type = the plan's compute dtype.
+ * The workspace must be ZERO-FILLED once before its first use: its head holds the
+ * small-M (decode) split-K accumulator, which the kernels keep all-zero at rest.
+ * Concurrent calls (other streams) need distinct workspaces. */
 TNL_API tnl_status tnl_forward(const tnl_plan* plan, const void* x, int64_t m, int64_t ldx, void* y,
                        int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
 

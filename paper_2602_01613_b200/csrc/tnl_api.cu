@@ -166,8 +166,7 @@ struct tnl_plan {
   __nv_bfloat16* chain_d = nullptr;  // Dp [(alpha, c_pad)][n_b]
   __nv_bfloat16* chain_c = nullptr;  // Cp [(j_a, b_pad)][c_pad]
   int32_t ch_na = 0, ch_nb = 0, ch_r0 = 0, ch_c = 0, ch_cpad = 0, ch_b = 0, ch_bpad = 0;
-  float* tacc = nullptr;            // decode accumulator (kDecMaxM x r_pad), zero at rest
-  unsigned int* counter = nullptr;  // decode last-CTA counter, zero at rest
+
   float* gen_w_out = nullptr;       // generic dense rows slice (fp32) for sharded generic plans
   int32_t plan_large = TNL_PLAN_GENERIC, plan_small = TNL_PLAN_GENERIC;
   int32_t decode_max_m = 0;
@@ -858,12 +857,7 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   size_t off_bin = 0, off_aout = 0, off_u1 = 0, off_g = 0, off_u0 = 0, off_w = 0;
   const bool dense = P->family == TNL_FAMILY_DENSE;
   const bool want_cut = tc_ok && !dense;
-  size_t off_tacc = 0, off_cnt = 0;
   if (want_cut) {
-    off_tacc = bytes;
-    bytes += round_up(64 * P->r_pad * 4, 256);
-    off_cnt = bytes;
-    bytes += 256;
     off_bin = bytes;
     bytes += round_up(P->r_pad * P->cols * 2, 256);
     off_aout = bytes;
@@ -907,8 +901,6 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
         rows_local, P->cols);
   }
   if (want_cut) {
-    P->tacc = reinterpret_cast<float*>(base + off_tacc);
-    P->counter = reinterpret_cast<unsigned int*>(base + off_cnt);
     P->bin = reinterpret_cast<__nv_bfloat16*>(base + off_bin);
     P->aout = reinterpret_cast<__nv_bfloat16*>(base + off_aout);
     float *fb = nullptr, *fa = nullptr;
@@ -993,6 +985,11 @@ static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b
     // sharded generic plans compute full rows into a temp y
     *o_f32 = (rows_local != P->rows) ? take(sizeof(float) * M * P->rows) : 0;
     return bytes;
+  }
+  // decode accumulator + counter (zero at rest: the caller zero-fills the workspace once)
+  if (P->decode_max_m) {
+    take(sizeof(float) * 64 * P->r_pad);
+    take(256);
   }
   int64_t kmax = P->r_pad;
   if (P->tucker_chain) kmax = std::max(P->r0p, P->r1p);
@@ -1108,16 +1105,20 @@ static bool gemv_ok_k(int64_t K) {
 // Small-M path of the merged-cut plan: phase A (B_in, split-K, fp32 reductions into the
 // plan-owned accumulator) + phase B (A_out, reads the fp32 accumulator, re-zeroes it).
 static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y,
-                                 int64_t ldy, cudaStream_t st) {
+                                 int64_t ldy, void* ws, cudaStream_t st) {
+  // decode accumulator (64 x r_pad fp32, zero at rest) and counter live at the workspace head
+  float* tacc = static_cast<float*>(ws);
+  unsigned int* counter =
+      reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + round_up(sizeof(float) * 64 * P->r_pad, 256));
   const int64_t rows_local = P->row_end - P->row_begin;
   int err = 0;
   const bool use_chain = P->plan_large == TNL_PLAN_CHAIN && P->chain_ok;
   if (M <= 8 && gemv_ok_k(P->r_pad) && !use_chain) {
     err = launch_gemv_a(P->bin, P->cols, (int)P->r_pad, (int)P->cols,
-                        static_cast<const __nv_bfloat16*>(x), ldx, (int)M, P->tacc, kDecMaxM, st);
+                        static_cast<const __nv_bfloat16*>(x), ldx, (int)M, tacc, kDecMaxM, st);
     if (err) return fail(TNL_ERR_CUDA, "gemv_a launch: %s", cudaGetErrorString((cudaError_t)err));
-    err = launch_gemv_b(P->aout, P->r_pad, (int)rows_local, (int)P->r_pad, P->tacc, kDecMaxM, (int)M,
-                        static_cast<__nv_bfloat16*>(y), ldy, P->counter, st);
+    err = launch_gemv_b(P->aout, P->r_pad, (int)rows_local, (int)P->r_pad, tacc, kDecMaxM, (int)M,
+                        static_cast<__nv_bfloat16*>(y), ldy, counter, st);
     if (err) return fail(TNL_ERR_CUDA, "gemv_b launch: %s", cudaGetErrorString((cudaError_t)err));
     return TNL_OK;
   }
@@ -1128,7 +1129,7 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
       (err = get_tmap(P, &tx, x, P->cols, M, ldx, bn)) ||
       (err = get_tmap(P, &tw2, P->aout, P->r_pad, rows_local, P->r_pad, 128)))
     return fail(TNL_ERR_CUDA, "tensor map (decode) failed: %d", err);
-  if ((err = get_tmap2(P, &tt, P->tacc, true, ldk, P->r_pad, ldk, bn, 64, 0)) ||
+  if ((err = get_tmap2(P, &tt, tacc, true, ldk, P->r_pad, ldk, bn, 64, 0)) ||
       (err = get_tmap2(P, &ty, y, false, rows_local, M, ldy, 128, bn, 0)))
     return fail(TNL_ERR_CUDA, "tensor map (decode accumulator / y) failed: %d", err);
   DecArgs a;
@@ -1144,14 +1145,14 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
   }();
   a.kb_per_split = kb_env > 0 ? kb_env : 4;
   int splits = (total_kb + a.kb_per_split - 1) / a.kb_per_split;
-  a.out = P->tacc;
+  a.out = tacc;
   a.ldo_i = ldk;
   a.ldo_j = 1;
   a.out_f32_atomic = 1;
   a.trace = P->trace;
   if (use_chain) {
     // core-by-core input chain, j_a split across CTAs, fp32 reductions into the accumulator
-    tnl_status cs = chain_in(P, x, ldx, M, P->tacc, 1, ldk, true, std::min(16, P->ch_na), st);
+    tnl_status cs = chain_in(P, x, ldx, M, tacc, 1, ldk, true, std::min(16, P->ch_na), st);
     if (cs) return cs;
   } else if ((err = launch_dec_a(tw, tx, a, splits, st))) {
     return fail(TNL_ERR_CUDA, "decode phase A launch: %s", cudaGetErrorString((cudaError_t)err));
@@ -1162,13 +1163,13 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
   b.tokens = (int32_t)M;
   b.K = (int32_t)P->r_pad;
   b.kb_per_split = (int32_t)((P->r_pad + 63) / 64);
-  b.act_f32 = P->tacc;
+  b.act_f32 = tacc;
   b.act_ld = ldk;
   b.out = y;
   b.ldo_i = 1;
   b.ldo_j = ldy;
   b.out_f32_atomic = 0;
-  b.counter = P->counter;
+  b.counter = counter;
   b.zero_elems = P->r_pad * ldk;
   b.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
   if ((err = launch_dec_b(tw2, tt, ty, b, st)))
@@ -1223,9 +1224,8 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
   __nv_bfloat16* t1 = reinterpret_cast<__nv_bfloat16*>(w + o_b1);
   const int64_t rows_local = P->row_end - P->row_begin;
   const bool swap = M <= kSwapMaxM;
-  if (M <= kDecMaxM && P->tacc && P->r_pad <= 256 && !(P->flags & TNL_PLAN_NO_DECODE) &&
-      !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0)
-    return forward_decode(P, x, M, ldx, y, ldy, st);
+  if (M <= kDecMaxM && P->decode_max_m && !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0)
+    return forward_decode(P, x, M, ldx, y, ldy, ws, st);
   tnl_status s;
   if (P->family == TNL_FAMILY_DENSE) {
     if (!swap && !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0)
@@ -1441,6 +1441,7 @@ tnl_status tnl_forward_host(tnl_plan* P, const void* x_host, int64_t m, void* y_
     cudaFree(P->stage_ws);
     P->stage_ws = nullptr;
     CUDA_TRY(cudaMalloc(&P->stage_ws, need));
+    CUDA_TRY(cudaMemset(P->stage_ws, 0, need));  // decode accumulator is zero at rest
     P->stage_ws_bytes = need;
   }
   CUDA_TRY(cudaMemcpyAsync(P->stage_x, x_host, es * m * P->cols, cudaMemcpyHostToDevice, st));

@@ -247,9 +247,10 @@ class NativePlan:
         return int(n.value)
 
     def workspace(self, m: int):
+        """Zero-filled workspace (the decode accumulator at its head is kept zero at rest)."""
         need = self.workspace_bytes(m)
         if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+            self._ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws
 
     def forward(self, x, out=None, stream=None, ws=None):

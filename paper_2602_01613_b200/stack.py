@@ -4,8 +4,16 @@
 call per layer). ``capture(m)`` records one whole pass — optionally including
 the host->device copy of x and the device->host copy of y from pinned
 buffers — into a CUDA graph so small-M decode is not bound by host launch
-overhead. All plans share one workspace (the steps of a stack are
-stream-ordered, so reuse is safe).
+overhead.
+
+Decode through a chain is latency-bound (every layer is two dependent
+weight-streaming kernels), so ``capture(m, microbatches=k)`` splits the M
+tokens into k groups that run the same chain concurrently on k forked
+streams inside the graph: while one group waits on a kernel boundary the
+others use the SMs, and layers run roughly in lockstep so their weight
+streams share L2. Per-token results are unchanged (tokens are independent
+through a linear layer). Every stream has its own zero-filled workspace
+(the decode split-K accumulator lives at its head).
 """
 
 from __future__ import annotations
@@ -31,21 +39,23 @@ class TNStack:
                 raise ShapeError(f"stack link mismatch: {a.rows_local} outputs feed {b.info['cols']} inputs")
         self.cols = self.plans[0].info["cols"]
         self.rows = self.plans[-1].rows_local
-        self._ws = None
+        self.width = max(p.rows_local for p in self.plans)
+        self._ws = []
         self.graph = None
 
-    def workspace(self, m: int):
+    def workspace(self, m: int, slot: int = 0):
         need = max(p.workspace_bytes(m) for p in self.plans)
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
-        return self._ws
+        while len(self._ws) <= slot:
+            self._ws.append(None)
+        if self._ws[slot] is None or self._ws[slot].numel() < need:
+            self._ws[slot] = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
+        return self._ws[slot]
 
-    def forward(self, x, bufs=None):
+    def forward(self, x, bufs=None, slot: int = 0):
         m = x.shape[0]
-        ws = self.workspace(m)
-        width = max(p.rows_local for p in self.plans)
+        ws = self.workspace(m, slot)
         if bufs is None:
-            bufs = [torch.empty((m, width), dtype=self.dtype, device=self.device) for _ in range(2)]
+            bufs = [torch.empty((m, self.width), dtype=self.dtype, device=self.device) for _ in range(2)]
         cur = x
         for i, p in enumerate(self.plans):
             out = bufs[i % 2][:, : p.rows_local]
@@ -53,34 +63,57 @@ class TNStack:
             cur = out
         return cur
 
-    def capture(self, m: int, host_io: bool = True, warmup: int = 1):
+    def capture(self, m: int, host_io: bool = True, warmup: int = 1, microbatches: int = 1):
         """Record one pass for M = m tokens into a CUDA graph (static buffers)."""
         self.m = m
+        k = max(1, min(microbatches, m))
+        bounds = [(i * m // k, (i + 1) * m // k) for i in range(k)]
         self.x_dev = torch.zeros((m, self.cols), dtype=self.dtype, device=self.device)
-        width = max(p.rows_local for p in self.plans)
-        self.bufs = [torch.empty((m, width), dtype=self.dtype, device=self.device) for _ in range(2)]
-        self.workspace(m)
+        self.y_dev = torch.zeros((m, self.rows), dtype=self.dtype, device=self.device)
+        self.bufs = [[torch.empty((hi - lo, self.width), dtype=self.dtype, device=self.device) for _ in range(2)]
+                     for lo, hi in bounds]
+        for j, (lo, hi) in enumerate(bounds):
+            self.workspace(hi - lo, slot=j)
         self.host_io = host_io
         if host_io:
             self.x_host = torch.zeros((m, self.cols), dtype=self.dtype).pin_memory()
             self.y_host = torch.empty((m, self.rows), dtype=self.dtype).pin_memory()
-        s = torch.cuda.Stream(self.device)
-        s.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(s):
+        main = torch.cuda.Stream(self.device)
+        side = [torch.cuda.Stream(self.device) for _ in range(k)]
+
+        def one_pass():
+            if host_io:
+                self.x_dev.copy_(self.x_host, non_blocking=True)
+            fork = torch.cuda.Event()
+            fork.record(main)
+            joins = []
+            for j, (lo, hi) in enumerate(bounds):
+                s = side[j]
+                s.wait_event(fork)
+                with torch.cuda.stream(s):
+                    y = self.forward(self.x_dev[lo:hi], self.bufs[j], slot=j)
+                    self.y_dev[lo:hi].copy_(y)
+                    e = torch.cuda.Event()
+                    e.record(s)
+                    joins.append(e)
+            for e in joins:
+                main.wait_event(e)
+            if host_io:
+                self.y_host.copy_(self.y_dev, non_blocking=True)
+
+        main.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(main):
             for _ in range(warmup):  # plans build tensor maps / lazy state outside capture
-                self.y_dev = self.forward(self.x_dev, self.bufs)
-        torch.cuda.current_stream(self.device).wait_stream(s)
+                one_pass()
+        torch.cuda.current_stream(self.device).wait_stream(main)
         torch.cuda.synchronize(self.device)
         N.launch_count(reset=True)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            if host_io:
-                self.x_dev.copy_(self.x_host, non_blocking=True)
-            self.y_dev = self.forward(self.x_dev, self.bufs)
-            if host_io:
-                self.y_host.copy_(self.y_dev, non_blocking=True)
+        with torch.cuda.graph(g, stream=main):
+            one_pass()
         self.launches_per_pass = N.launch_count(reset=True)
         self.graph = g
+        self.microbatches = k
         self.h2d_bytes = self.x_dev.numel() * self.x_dev.element_size() if host_io else 0
         self.d2h_bytes = self.y_dev.numel() * self.y_dev.element_size() if host_io else 0
         return g
