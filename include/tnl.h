@@ -151,6 +151,17 @@ TNL_API tnl_status tnl_forward_host(tnl_plan* plan, const void* x_host, int64_t 
 TNL_API tnl_status tnl_reconstruct(const tnl_plan* plan, void* w, int64_t ldw, int32_t out_dtype,
                            void* stream);
 
+/* A chain of layers (a decoder's projection stack): y = L_{n-1}(...L_0(x)).
+ * For M <= 64 and merged-cut bf16 plans whose widths chain (rows % 128 == 0) this
+ * runs ONE fused kernel per layer boundary (phase B of layer l + phase A of layer
+ * l+1, the activation never leaves the SM); otherwise it chains tnl_forward.
+ * The workspace (tnl_stack_workspace_size) must be zero-filled before first use. */
+TNL_API tnl_status tnl_stack_workspace_size(const tnl_plan* const* plans, int32_t n, int64_t m,
+                                            size_t* bytes);
+TNL_API tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void* x,
+                                     int64_t m, int64_t ldx, void* y, int64_t ldy, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+
 /* Number of libtnl kernel launches issued by this thread since the last reset
  * (evidence counter for benchmarks). */
 TNL_API int64_t tnl_launch_count(int32_t reset);

@@ -37,6 +37,8 @@ EXPORTED = (
     "tnl_reconstruct",
     "tnl_launch_count",
     "tnl_plan_set_trace",
+    "tnl_stack_workspace_size",
+    "tnl_stack_forward",
 )
 
 
@@ -105,6 +107,12 @@ def load():
         lib.tnl_forward.argtypes = [P, P, i64, i64, P, i64, P, ctypes.c_size_t, P]
         lib.tnl_forward_host.argtypes = [P, P, i64, P, P]
         lib.tnl_reconstruct.argtypes = [P, P, i64, ctypes.c_int32, P]
+        lib.tnl_stack_workspace_size.argtypes = [ctypes.POINTER(P), ctypes.c_int32, i64,
+                                                 ctypes.POINTER(ctypes.c_size_t)]
+        lib.tnl_stack_workspace_size.restype = ctypes.c_int
+        lib.tnl_stack_forward.argtypes = [ctypes.POINTER(P), ctypes.c_int32, P, i64, i64, P, i64, P,
+                                          ctypes.c_size_t, P]
+        lib.tnl_stack_forward.restype = ctypes.c_int
         lib.tnl_plan_set_trace.argtypes = [P, P]
         lib.tnl_plan_set_trace.restype = ctypes.c_int
         lib.tnl_launch_count.argtypes = [ctypes.c_int32]

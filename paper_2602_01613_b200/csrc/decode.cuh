@@ -53,6 +53,23 @@ int launch_dec_a(const CUtensorMap& w, const CUtensorMap& x, const DecArgs& a, i
 int launch_dec_b(const CUtensorMap& w, const CUtensorMap& t, const CUtensorMap& y, const DecArgs& a,
                  cudaStream_t st);
 
+// Fused boundary kernel of a decode stack (decode_fused.cu): phase B of layer l
+// (A_out^l, accumulator T_l) + phase A of layer l+1 (B_in^{l+1}) in one launch.
+struct FusedArgs {
+  int32_t tokens;      // M <= 64
+  int32_t rows;        // rows of layer l == cols of layer l+1 (multiple of 128)
+  int32_t kB;          // r_pad of layer l (<= 256)
+  int32_t nA;          // r_pad of layer l+1 (<= 256)
+  float* t_in;         // T_l, kappa-major [kB][64], re-zeroed by the last CTA
+  unsigned int* cnt_in;
+  float* t_out;        // T_{l+1}, kappa-major [nA][64], fp32 reductions
+  int64_t zero_elems;
+};
+// wo: A_out^l map (box {64, 128}, SW128); t: T_l fp32 map (box {BN, 64}); wi: B_in^{l+1}
+// map (box {64, 128}, SW128). grid = rows / 128.
+int launch_dec_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi,
+                     const FusedArgs& a, int grid, cudaStream_t st);
+
 // CUDA-core GEMV variants (tokens <= 8)
 int launch_gemv_a(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const __nv_bfloat16* x,
                   int64_t ldx, int tokens, float* t_acc, int64_t ldt, cudaStream_t st);

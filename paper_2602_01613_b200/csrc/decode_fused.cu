@@ -1,0 +1,262 @@
+// decode_fused.cu — one kernel per layer boundary for a decode stack:
+// phase B of layer l fused with phase A of layer l+1 (merged-cut plans).
+//
+// CTA i owns output rows [128 i, 128 i + 128) of layer l. Those rows are
+// exactly the K-slice [128 i, 128 i + 128) that layer l+1's phase A contracts,
+// so y_l never leaves the SM:
+//   D_B (128 rows x M) = A_out^l[rows] . T_l            T_l from the fp32 accumulator
+//   x   = bf16(D_B)^T   -> SW128 smem operand [M tokens][128 k]
+//   D_A (kappa x M)     = B_in^{l+1}[:, rows] . x        -> fp32 reductions into T_{l+1}
+// One kernel boundary per layer instead of two, no activation round trip
+// through HBM/L2. T_l / T_{l+1} alternate between two zero-at-rest
+// accumulators; the last CTA to finish reading T_l re-zeroes it.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "decode.cuh"
+#include "ptx.cuh"
+
+namespace tnl {
+
+namespace {
+
+constexpr int FT = 320, FEPI = 256;  // threads: TMA warp, MMA warp, 8 epilogue warps
+constexpr uint32_t WBLK = 128 * 64 * 2;  // one 128-row x 64-k bf16 weight block (16 KB)
+
+__device__ __forceinline__ void nbar(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ uint32_t sw128(int r, int c) {
+  return (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
+}
+
+template <int BN>
+struct FSmem {
+  static constexpr uint32_t F_BLK = BN * 64 * 4;   // fp32 staging of 64 kappa x BN tokens
+  static constexpr uint32_t T_BLK = BN * 64 * 2;   // bf16 T operand block [BN][64]
+  static constexpr uint32_t X_BLK = BN * 64 * 2;   // bf16 x operand block [BN][64]
+  static constexpr size_t bytes = 1024 + 4 * WBLK /*A_out*/ + 4 * WBLK /*B_in*/ + 4 * F_BLK +
+                                  4 * T_BLK + 256;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(FT, 1)
+    dec_fused_kernel(const __grid_constant__ CUtensorMap tmWo, const __grid_constant__ CUtensorMap tmT,
+                     const __grid_constant__ CUtensorMap tmWi, const FusedArgs a) {
+  using SM = FSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sWo = smem;                   // kbB blocks
+  uint8_t* sWi = sWo + 4 * WBLK;         // nT x 2 blocks
+  float* sF = reinterpret_cast<float*>(sWi + 4 * WBLK);  // kbB fp32 staging blocks (then x operand)
+  uint8_t* sX = reinterpret_cast<uint8_t*>(sF);
+  uint8_t* sT = reinterpret_cast<uint8_t*>(sF) + 4 * SM::F_BLK;  // kbB bf16 T blocks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + 4 * SM::T_BLK);
+  uint64_t* wfull = bars;
+  uint64_t* stg = bars + 1;  // [4]
+  uint64_t* tfull = bars + 5;
+  uint64_t* bdone = bars + 6;
+  uint64_t* xfull = bars + 7;
+  uint64_t* adone = bars + 8;
+  uint64_t* flagbar = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint32_t* last_flag = tmem_slot + 1;
+
+  const int tile = blockIdx.x;
+  const int kbB = (a.kB + 63) / 64;
+  const int nT = (a.nA + 127) / 128;
+  const uint32_t warp = warp_id();
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmWo);
+    tma_prefetch_desc(&tmT);
+    tma_prefetch_desc(&tmWi);
+    mbar_init(wfull, 1);
+    for (int s = 0; s < 4; ++s) mbar_init(&stg[s], 1);
+    mbar_init(tfull, 1);
+    mbar_init(bdone, 1);
+    mbar_init(xfull, 1);
+    mbar_init(adone, 1);
+    mbar_init(flagbar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDB = tmem, tDA = tmem + BN;  // D_A: nT blocks of BN columns
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // both layers' weights first (independent of the previous kernel)
+      mbar_arrive_expect_tx(wfull, (kbB + 2 * nT) * WBLK);
+      const uint64_t pol = policy_evict_first();
+      for (int kb = 0; kb < kbB; ++kb)
+        tma_load_2d_hint(sWo + kb * WBLK, &tmWo, wfull, kb * 64, tile * 128, pol);
+      for (int t = 0; t < nT; ++t)
+        for (int h = 0; h < 2; ++h)
+          tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull, tile * 128 + h * 64, t * 128, pol);
+      pdl_wait();
+      for (int kb = 0; kb < kbB; ++kb) {
+        mbar_arrive_expect_tx(&stg[kb], SM::F_BLK);
+        tma_load_2d(reinterpret_cast<uint8_t*>(sF) + kb * SM::F_BLK, &tmT, &stg[kb], 0, kb * 64);
+      }
+      // count this CTA's reads of T_l (off the epilogue's critical path)
+      for (int kb = 0; kb < kbB; ++kb) mbar_wait(&stg[kb], 0);
+      __threadfence();
+      *last_flag = (atomicAdd(a.cnt_in, 1u) == gridDim.x - 1) ? 1u : 0u;
+      mbar_arrive(flagbar);
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      mbar_wait(wfull, 0);
+      mbar_wait(tfull, 0);
+      tc_fence_after();
+      for (int kb = 0; kb < kbB; ++kb) {
+        const uint64_t ad = smem_desc_sw128(smem_u32(sWo + kb * WBLK));
+        const uint64_t bd = smem_desc_sw128(smem_u32(sT + kb * SM::T_BLK));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mma_bf16_ss(tDB, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+      }
+      mma_commit(bdone);
+      mbar_wait(xfull, 0);
+      tc_fence_after();
+      for (int t = 0; t < nT; ++t)
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t ad = smem_desc_sw128(smem_u32(sWi + (t * 2 + h) * WBLK));
+          const uint64_t bd = smem_desc_sw128(smem_u32(sX + h * SM::X_BLK));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_bf16_ss(tDA + t * BN, ad + 2 * k, bd + 2 * k, idesc, (h | k) != 0);
+        }
+      mma_commit(adone);
+    }
+    __syncwarp();
+  } else {
+    const int et = threadIdx.x - 64;
+    pdl_wait();
+    // T_l: fp32 [64 kappa][BN tokens] -> bf16 SW128 [BN tokens][64 kappa] per k-block
+    for (int kb = 0; kb < kbB; ++kb) {
+      mbar_wait(&stg[kb], 0);
+      const float* src = sF + kb * (SM::F_BLK / 4);
+      uint8_t* dst = sT + kb * SM::T_BLK;
+      for (int e = et; e < BN * 8; e += FEPI) {
+        const int r = e % BN, c = e / BN;
+        float f[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] = src[(c * 8 + q) * BN + r];
+        uint4 p;
+        p.x = pack_bf16x2(f[0], f[1]);
+        p.y = pack_bf16x2(f[2], f[3]);
+        p.z = pack_bf16x2(f[4], f[5]);
+        p.w = pack_bf16x2(f[6], f[7]);
+        *reinterpret_cast<uint4*>(dst + sw128(r, c)) = p;
+      }
+    }
+    fence_proxy_async_smem();
+    nbar(1, FEPI);
+    if (et == 0) mbar_arrive(tfull);
+
+    const uint32_t q = warp & 3;
+    const int lrow = q * 32 + lane_id();
+    constexpr int HALF = BN >= 32 ? BN / 2 : BN;
+    const int c_begin = ((warp - 2) >> 2) * HALF;
+    // y_l tile -> x operand of layer l+1 (row = token, k = this CTA's row lrow)
+    mbar_wait(bdone, 0);
+    tc_fence_after();
+    {
+      uint8_t* xb = sX + (lrow >> 6) * SM::X_BLK;
+      const int ck = (lrow & 63) >> 3, cw = (lrow & 7) * 2;
+#pragma unroll 1
+      for (int c = c_begin; c < c_begin + HALF && c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(tDB + ((q * 32) << 16) + c, v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int r = c + e;
+          *reinterpret_cast<__nv_bfloat16*>(xb + (r >> 3) * 1024 + (r & 7) * 128 + ((ck ^ (r & 7)) << 4) + cw) =
+              __float2bfloat16_rn(v[e]);
+        }
+      }
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();
+    nbar(1, FEPI);
+    if (et == 0) mbar_arrive(xfull);
+    // D_A -> fp32 reductions into T_{l+1} (kappa-major [kappa][64])
+    mbar_wait(adone, 0);
+    tc_fence_after();
+    for (int t = 0; t < nT; ++t) {
+      const int kap = t * 128 + lrow;
+#pragma unroll 1
+      for (int c = c_begin; c < c_begin + HALF && c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(tDA + t * BN + ((q * 32) << 16) + c, v);
+        if (kap >= a.nA || c >= a.tokens) continue;
+        const int n = min(16, a.tokens - c);
+        float* o = a.t_out + (int64_t)kap * 64 + c;
+        if (n == 16) {
+#pragma unroll
+          for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e < n) atomicAdd(o + e, v[e]);
+        }
+      }
+    }
+    // the last CTA to read T_l re-zeroes it for its next use
+    mbar_wait(flagbar, 0);
+    if (*last_flag) {
+      float4* z = reinterpret_cast<float4*>(a.t_in);
+      for (int64_t e = et; e < a.zero_elems / 4; e += FEPI) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (et == 0) atomicExch(a.cnt_in, 0u);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
+template <int BN>
+int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi, const FusedArgs& a,
+                 int grid, cudaStream_t st) {
+  constexpr size_t smem = FSmem<BN>::bytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dec_fused_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(FT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dec_fused_kernel<BN>, wo, t, wi, a);
+  count_launch();
+  return (int)e;
+}
+
+}  // namespace
+
+int launch_dec_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi, const FusedArgs& a,
+                     int grid, cudaStream_t st) {
+  if (a.kB > 256 || a.nA > 256 || a.rows % 128) return (int)cudaErrorInvalidValue;
+  if (a.tokens <= 16) return launch_fused<16>(wo, t, wi, a, grid, st);
+  if (a.tokens <= 32) return launch_fused<32>(wo, t, wi, a, grid, st);
+  return launch_fused<64>(wo, t, wi, a, grid, st);
+}
+
+}  // namespace tnl

@@ -1338,6 +1338,36 @@ static tnl_status forward_generic(tnl_plan* P, const void* x, int64_t M, int64_t
   return TNL_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Decode stacks: one fused kernel per layer boundary (decode_fused.cu)
+// ---------------------------------------------------------------------------
+static bool stack_fusable(const tnl_plan* const* plans, int32_t n, int64_t m) {
+  if (n < 2 || m < 1 || m > kDecMaxM) return false;
+  for (int i = 0; i < n; ++i) {
+    const tnl_plan* P = plans[i];
+    if (!P || !P->decode_max_m || P->plan_large != TNL_PLAN_CUT || P->compute_dtype != TNL_BF16 ||
+        P->row_begin != 0 || P->row_end != P->rows)
+      return false;
+    if (i + 1 < n && (P->rows != plans[i + 1]->cols || P->rows % 128)) return false;
+  }
+  return true;
+}
+
+static size_t stack_ws_bytes(const tnl_plan* const* plans, int32_t n, int64_t m) {
+  if (stack_fusable(plans, n, m)) return 2 * round_up(sizeof(float) * 64 * 256, 256) + 256;
+  size_t mx = 0;
+  int64_t width = 0;
+  for (int i = 0; i < n; ++i) {
+    size_t a, b, c;
+    mx = std::max(mx, ws_layout(plans[i], std::max<int64_t>(m, 1), &a, &b, &c));
+    width = std::max(width, plans[i]->row_end - plans[i]->row_begin);
+  }
+  return mx + 2 * round_up(2 * m * width, 256);
+}
+
+}  // namespace tnl (stack helpers)
+namespace tnl {
 }  // namespace tnl
 
 using namespace tnl;
@@ -1347,6 +1377,132 @@ extern "C" {
 int tnl_abi_version(void) { return TNL_ABI_VERSION; }
 const char* tnl_last_error(void) { return g_err.c_str(); }
 int64_t tnl_launch_count(int32_t reset) { return launch_count(reset != 0); }
+
+tnl_status tnl_stack_workspace_size(const tnl_plan* const* plans, int32_t n, int64_t m, size_t* bytes) {
+  if (!plans || n < 1 || !bytes) return fail(TNL_ERR_ARG, "null argument");
+  for (int i = 0; i < n; ++i)
+    if (!plans[i]) return fail(TNL_ERR_ARG, "null plan %d", i);
+  *bytes = stack_ws_bytes(plans, n, m);
+  return TNL_OK;
+}
+
+tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void* x, int64_t m,
+                             int64_t ldx, void* y, int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+  if (!plans || n < 1 || !x || !y) return fail(TNL_ERR_ARG, "null argument");
+  for (int i = 0; i < n; ++i)
+    if (!plans[i]) return fail(TNL_ERR_ARG, "null plan %d", i);
+  for (int i = 0; i + 1 < n; ++i)
+    if (plans[i]->row_end - plans[i]->row_begin != plans[i + 1]->cols)
+      return fail(TNL_ERR_SHAPE, "stack link %d: %lld outputs feed %lld inputs", i,
+                  (long long)(plans[i]->row_end - plans[i]->row_begin), (long long)plans[i + 1]->cols);
+  if (m == 0) return TNL_OK;
+  const size_t need = stack_ws_bytes(plans, n, m);
+  if (ws_bytes < need) return fail(TNL_ERR_ARG, "stack workspace %zu < required %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  tnl_plan* const* Pv = const_cast<tnl_plan* const*>(plans);
+  if (!stack_fusable(plans, n, m) || (reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8 ||
+      (reinterpret_cast<uintptr_t>(x) & 15) || ldx % 8) {
+    // generic chain: per-layer forwards through two activation buffers in the workspace
+    size_t layer_ws = 0;
+    int64_t width = 0;
+    for (int i = 0; i < n; ++i) {
+      size_t a, b, c;
+      layer_ws = std::max(layer_ws, ws_layout(plans[i], std::max<int64_t>(m, 1), &a, &b, &c));
+      width = std::max(width, plans[i]->row_end - plans[i]->row_begin);
+    }
+    char* base = static_cast<char*>(ws);
+    void* buf[2] = {base + layer_ws, base + layer_ws + round_up(2 * m * width, 256)};
+    const void* cur = x;
+    int64_t ldc = ldx;
+    for (int i = 0; i < n; ++i) {
+      const bool last = i + 1 == n;
+      void* out = last ? y : buf[i & 1];
+      const int64_t ldo = last ? ldy : width;
+      tnl_status s = tnl_forward(plans[i], cur, m, ldc, out, ldo, ws, layer_ws, stream);
+      if (s) return s;
+      cur = out;
+      ldc = ldo;
+    }
+    return TNL_OK;
+  }
+  char* base = static_cast<char*>(ws);
+  const size_t slot = round_up(sizeof(float) * 64 * 256, 256);
+  float* tacc[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + slot)};
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(base + 2 * slot);  // [2]
+  const int bn = pick_bn(m);
+  int err = 0;
+  // layer 0, phase A
+  {
+    tnl_plan* P = Pv[0];
+    CUtensorMap tw, tx;
+    if ((err = get_tmap(P, &tw, P->bin, P->cols, P->r_pad, P->cols, 128)) ||
+        (err = get_tmap(P, &tx, x, P->cols, m, ldx, bn)))
+      return fail(TNL_ERR_CUDA, "tensor map (stack phase A) failed: %d", err);
+    DecArgs a;
+    memset(&a, 0, sizeof a);
+    a.M_rows = (int32_t)P->r_pad;
+    a.tokens = (int32_t)m;
+    a.K = (int32_t)P->cols;
+    const int total_kb = (int)((P->cols + 63) / 64);
+    a.kb_per_split = 4;
+    const int splits = (total_kb + 3) / 4;
+    a.out = tacc[0];
+    a.ldo_i = 64;
+    a.ldo_j = 1;
+    a.out_f32_atomic = 1;
+    if ((err = launch_dec_a(tw, tx, a, splits, st)))
+      return fail(TNL_ERR_CUDA, "stack phase A launch: %s", cudaGetErrorString((cudaError_t)err));
+  }
+  // boundaries l | l+1
+  for (int l = 0; l + 1 < n; ++l) {
+    tnl_plan* P = Pv[l];
+    tnl_plan* Q = Pv[l + 1];
+    CUtensorMap two, tt, twi;
+    if ((err = get_tmap(P, &two, P->aout, P->r_pad, P->rows, P->r_pad, 128)) ||
+        (err = get_tmap2(P, &tt, tacc[l & 1], true, 64, P->r_pad, 64, bn, 64, 0)) ||
+        (err = get_tmap(Q, &twi, Q->bin, Q->cols, Q->r_pad, Q->cols, 128)))
+      return fail(TNL_ERR_CUDA, "tensor map (stack boundary) failed: %d", err);
+    FusedArgs f;
+    memset(&f, 0, sizeof f);
+    f.tokens = (int32_t)m;
+    f.rows = (int32_t)P->rows;
+    f.kB = (int32_t)P->r_pad;
+    f.nA = (int32_t)Q->r_pad;
+    f.t_in = tacc[l & 1];
+    f.cnt_in = cnt + (l & 1);
+    f.t_out = tacc[(l + 1) & 1];
+    f.zero_elems = 64 * P->r_pad;
+    if ((err = launch_dec_fused(two, tt, twi, f, (int)(P->rows / 128), st)))
+      return fail(TNL_ERR_CUDA, "stack boundary launch: %s", cudaGetErrorString((cudaError_t)err));
+  }
+  // last layer, phase B
+  {
+    const int l = n - 1;
+    tnl_plan* P = Pv[l];
+    const int64_t rows_local = P->row_end - P->row_begin;
+    CUtensorMap tw2, tt, ty;
+    if ((err = get_tmap(P, &tw2, P->aout, P->r_pad, rows_local, P->r_pad, 128)) ||
+        (err = get_tmap2(P, &tt, tacc[l & 1], true, 64, P->r_pad, 64, bn, 64, 0)) ||
+        (err = get_tmap2(P, &ty, y, false, rows_local, m, ldy, 128, bn, 0)))
+      return fail(TNL_ERR_CUDA, "tensor map (stack phase B) failed: %d", err);
+    DecArgs b;
+    memset(&b, 0, sizeof b);
+    b.M_rows = (int32_t)rows_local;
+    b.tokens = (int32_t)m;
+    b.K = (int32_t)P->r_pad;
+    b.kb_per_split = (int32_t)((P->r_pad + 63) / 64);
+    b.act_f32 = tacc[l & 1];
+    b.act_ld = 64;
+    b.out = y;
+    b.ldo_i = 1;
+    b.ldo_j = ldy;
+    b.counter = cnt + (l & 1);
+    b.zero_elems = 64 * P->r_pad;
+    if ((err = launch_dec_b(tw2, tt, ty, b, st)))
+      return fail(TNL_ERR_CUDA, "stack phase B launch: %s", cudaGetErrorString((cudaError_t)err));
+  }
+  return TNL_OK;
+}
 
 tnl_status tnl_plan_set_trace(tnl_plan* plan, void* device_buffer) {
   if (!plan) return fail(TNL_ERR_ARG, "null plan");

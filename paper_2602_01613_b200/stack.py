@@ -18,6 +18,8 @@ through a linear layer). Every stream has its own zero-filled workspace
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _native as N
@@ -42,26 +44,39 @@ class TNStack:
         self.width = max(p.rows_local for p in self.plans)
         self._ws = []
         self.graph = None
+        self._lib = N.load()
+        self._handles = (ctypes.c_void_p * len(self.plans))(*[p.handle.value for p in self.plans])
+
+    def workspace_bytes(self, m: int) -> int:
+        n = ctypes.c_size_t()
+        N.check(self._lib.tnl_stack_workspace_size(self._handles, len(self.plans), int(m), ctypes.byref(n)))
+        return int(n.value)
 
     def workspace(self, m: int, slot: int = 0):
-        need = max(p.workspace_bytes(m) for p in self.plans)
+        """Zero-filled stack workspace for one concurrent token group (`slot`)."""
+        need = self.workspace_bytes(m)
         while len(self._ws) <= slot:
             self._ws.append(None)
         if self._ws[slot] is None or self._ws[slot].numel() < need:
             self._ws[slot] = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws[slot]
 
-    def forward(self, x, bufs=None, slot: int = 0):
+    def forward(self, x, out=None, slot: int = 0):
+        """y = L_{n-1}(...L_0(x)) through ``tnl_stack_forward`` (one fused kernel per layer
+        boundary for decode-sized M, else one ``tnl_forward`` per layer)."""
         m = x.shape[0]
+        if x.stride(1) != 1 or (m > 1 and x.stride(0) < self.cols):
+            x = x.contiguous()
+        if out is None:
+            out = torch.empty((m, self.rows), dtype=self.dtype, device=self.device)
         ws = self.workspace(m, slot)
-        if bufs is None:
-            bufs = [torch.empty((m, self.width), dtype=self.dtype, device=self.device) for _ in range(2)]
-        cur = x
-        for i, p in enumerate(self.plans):
-            out = bufs[i % 2][:, : p.rows_local]
-            p.forward(cur, out=out, ws=ws)
-            cur = out
-        return cur
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ldx = x.stride(0) if m > 1 else self.cols
+        ldy = out.stride(0) if m > 1 else self.rows
+        N.check(self._lib.tnl_stack_forward(self._handles, len(self.plans), ctypes.c_void_p(x.data_ptr()), m, ldx,
+                                            ctypes.c_void_p(out.data_ptr()), ldy, ctypes.c_void_p(ws.data_ptr()),
+                                            ws.numel(), ctypes.c_void_p(stream)))
+        return out
 
     def capture(self, m: int, host_io: bool = True, warmup: int = 1, microbatches: int = 1):
         """Record one pass for M = m tokens into a CUDA graph (static buffers)."""
@@ -70,8 +85,6 @@ class TNStack:
         bounds = [(i * m // k, (i + 1) * m // k) for i in range(k)]
         self.x_dev = torch.zeros((m, self.cols), dtype=self.dtype, device=self.device)
         self.y_dev = torch.zeros((m, self.rows), dtype=self.dtype, device=self.device)
-        self.bufs = [[torch.empty((hi - lo, self.width), dtype=self.dtype, device=self.device) for _ in range(2)]
-                     for lo, hi in bounds]
         for j, (lo, hi) in enumerate(bounds):
             self.workspace(hi - lo, slot=j)
         self.host_io = host_io
@@ -91,8 +104,7 @@ class TNStack:
                 s = side[j]
                 s.wait_event(fork)
                 with torch.cuda.stream(s):
-                    y = self.forward(self.x_dev[lo:hi], self.bufs[j], slot=j)
-                    self.y_dev[lo:hi].copy_(y)
+                    self.forward(self.x_dev[lo:hi], out=self.y_dev[lo:hi], slot=j)
                     e = torch.cuda.Event()
                     e.record(s)
                     joins.append(e)

@@ -279,3 +279,32 @@ def test_chain_plan_selected_for_two_mode_inputs():
     layer, _ = to_layer(L, round_bf16=True)
     assert layer.plan(torch.bfloat16, flags=tnl.PLAN_CHAIN).info["plan_large_name"] == "chain"
     assert layer.plan(torch.bfloat16).info["plan_large_name"] == "cut"
+
+
+@pytest.mark.parametrize("m", [64, 37, 16, 5])
+def test_stack_fused_matches_oracle_chain(m):
+    """tnl_stack_forward (one fused kernel per layer boundary) vs the oracle applied layer by layer
+    on the same bf16 values (the oracle re-rounds each intermediate to bf16, as the GPU does)."""
+    from paper_2602_01613_b200.stack import TNStack
+
+    specs = [("tucker", (5120, 5120), 1, (256, 256)), ("tr", (64, 80, 64, 80), 2, (8, 8, 8, 8)),
+             ("tr", (5120, 5120), 1, (16, 16)), ("tucker", (5120, 5120), 1, (64, 64)),
+             ("tr", (64, 80, 64, 80), 2, (16, 16, 16, 16))]
+    Ls = [O.synthetic_layer(f, ms, rm, rk, seed=48_000 + i) for i, (f, ms, rm, rk) in enumerate(specs)]
+    pairs = [to_layer(L, round_bf16=True) for L in Ls]
+    st = TNStack([p[0] for p in pairs], torch.bfloat16)
+    x = O.round_bf16(O.synthetic_x(m, 5120, seed=48_999))
+    y = st.forward(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
+    y2 = st.forward(torch.tensor(x, dtype=torch.bfloat16, device=DEV))  # accumulators re-zeroed
+    torch.cuda.synchronize()
+    ref = x
+    for _, Lr in pairs:
+        ref = O.round_bf16(O.forward_torch_orient(Lr, ref))
+    assert rel(ref, y.float().cpu().numpy()) <= 3 * BF16_TOL
+    assert rel(ref, y2.float().cpu().numpy()) <= 3 * BF16_TOL
+    # and against the per-layer C-ABI path
+    cur = torch.tensor(x, dtype=torch.bfloat16, device=DEV)
+    for layer, _ in pairs:
+        cur = layer.plan(torch.bfloat16).forward(cur)
+    d = (cur.float() - y.float()).norm() / cur.float().norm()
+    assert float(d) < 2e-2
