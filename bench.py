@@ -235,7 +235,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense cuBLAS comparison")
     ap.add_argument("--flags", type=int, default=0, help="TNL_PLAN_* preference for every layer")
-    ap.add_argument("--microbatches", type=int, default=4,
+    ap.add_argument("--microbatches", type=int, default=2,
                     help="concurrent token groups (streams) the M tokens are split into inside the graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -64,6 +64,7 @@ struct FusedArgs {
   unsigned int* cnt_in;
   float* t_out;        // T_{l+1}, kappa-major [nA][64], fp32 reductions
   int64_t zero_elems;
+  unsigned long long* trace;  // optional per-CTA %globaltimer stamps [cta][16]
 };
 // wo: A_out^l map (box {64, 128}, SW128); t: T_l fp32 map (box {BN, 64}); wi: B_in^{l+1}
 // map (box {64, 128}, SW128). grid = rows / 128.

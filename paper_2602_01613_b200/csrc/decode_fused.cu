@@ -66,6 +66,10 @@ __global__ void __launch_bounds__(FT, 1)
   uint32_t* last_flag = tmem_slot + 1;
 
   const int tile = blockIdx.x;
+  unsigned long long* tr = a.trace ? a.trace + 16 * blockIdx.x : nullptr;
+#define TRACE(ev) \
+  if (tr) tr[ev] = globaltimer();
+  if (threadIdx.x == 0) TRACE(0);
   const int kbB = (a.kB + 63) / 64;
   const int nT = (a.nA + 127) / 128;
   const uint32_t warp = warp_id();
@@ -90,6 +94,7 @@ __global__ void __launch_bounds__(FT, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tDB = tmem, tDA = tmem + BN;  // D_A: nT blocks of BN columns
   pdl_launch_dependents();
+  if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0) {
     if (elect_one()) {
@@ -101,13 +106,16 @@ __global__ void __launch_bounds__(FT, 1)
       for (int t = 0; t < nT; ++t)
         for (int h = 0; h < 2; ++h)
           tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull, tile * 128 + h * 64, t * 128, pol);
+      TRACE(2);
       pdl_wait();
+      TRACE(3);
       for (int kb = 0; kb < kbB; ++kb) {
         mbar_arrive_expect_tx(&stg[kb], SM::F_BLK);
         tma_load_2d(reinterpret_cast<uint8_t*>(sF) + kb * SM::F_BLK, &tmT, &stg[kb], 0, kb * 64);
       }
       // count this CTA's reads of T_l (off the epilogue's critical path)
       for (int kb = 0; kb < kbB; ++kb) mbar_wait(&stg[kb], 0);
+      TRACE(4);
       __threadfence();
       *last_flag = (atomicAdd(a.cnt_in, 1u) == gridDim.x - 1) ? 1u : 0u;
       mbar_arrive(flagbar);
@@ -161,6 +169,7 @@ __global__ void __launch_bounds__(FT, 1)
     fence_proxy_async_smem();
     nbar(1, FEPI);
     if (et == 0) mbar_arrive(tfull);
+    if (et == 0) TRACE(5);
 
     const uint32_t q = warp & 3;
     const int lrow = q * 32 + lane_id();
@@ -169,6 +178,7 @@ __global__ void __launch_bounds__(FT, 1)
     // y_l tile -> x operand of layer l+1 (row = token, k = this CTA's row lrow)
     mbar_wait(bdone, 0);
     tc_fence_after();
+    if (et == 0) TRACE(6);
     {
       uint8_t* xb = sX + (lrow >> 6) * SM::X_BLK;
       const int ck = (lrow & 63) >> 3, cw = (lrow & 7) * 2;
@@ -188,9 +198,11 @@ __global__ void __launch_bounds__(FT, 1)
     fence_proxy_async_smem();
     nbar(1, FEPI);
     if (et == 0) mbar_arrive(xfull);
+    if (et == 0) TRACE(7);
     // D_A -> fp32 reductions into T_{l+1} (kappa-major [kappa][64])
     mbar_wait(adone, 0);
     tc_fence_after();
+    if (et == 0) TRACE(8);
     for (int t = 0; t < nT; ++t) {
       const int kap = t * 128 + lrow;
 #pragma unroll 1
@@ -210,6 +222,7 @@ __global__ void __launch_bounds__(FT, 1)
         }
       }
     }
+    if (et == 0) TRACE(9);
     // the last CTA to read T_l re-zeroes it for its next use
     mbar_wait(flagbar, 0);
     if (*last_flag) {
@@ -221,6 +234,8 @@ __global__ void __launch_bounds__(FT, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<256>(tmem);
+  if (threadIdx.x == 32) TRACE(10);
+#undef TRACE
 }
 
 template <int BN>

@@ -1450,6 +1450,7 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     a.ldo_i = 64;
     a.ldo_j = 1;
     a.out_f32_atomic = 1;
+    a.trace = P->trace;
     if ((err = launch_dec_a(tw, tx, a, splits, st)))
       return fail(TNL_ERR_CUDA, "stack phase A launch: %s", cudaGetErrorString((cudaError_t)err));
   }
@@ -1472,6 +1473,7 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     f.cnt_in = cnt + (l & 1);
     f.t_out = tacc[(l + 1) & 1];
     f.zero_elems = 64 * P->r_pad;
+    f.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
     if ((err = launch_dec_fused(two, tt, twi, f, (int)(P->rows / 128), st)))
       return fail(TNL_ERR_CUDA, "stack boundary launch: %s", cudaGetErrorString((cudaError_t)err));
   }
@@ -1498,6 +1500,7 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     b.ldo_j = ldy;
     b.counter = cnt + (l & 1);
     b.zero_elems = 64 * P->r_pad;
+    b.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
     if ((err = launch_dec_b(tw2, tt, ty, b, st)))
       return fail(TNL_ERR_CUDA, "stack phase B launch: %s", cudaGetErrorString((cudaError_t)err));
   }

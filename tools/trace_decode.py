@@ -37,6 +37,7 @@ for b in bufs:
 st.replay()
 torch.cuda.synchronize()
 EV = ["start", "setup", "w_issued", "pdl_passed", "mma_first", "mma_issued", "epi_pdl", "act_ready", "done", "stored", "end"]
+EVF = ["start", "setup", "w_issued", "pdl_passed", "T_landed", "T_converted", "B_done", "x_ready", "A_done", "reds_issued", "end"]
 t0 = None
 for li, (v, b) in enumerate(zip(vs, bufs)):
     arr = b.view(2, 1024, 16).cpu().numpy()
@@ -49,10 +50,12 @@ for li, (v, b) in enumerate(zip(vs, bufs)):
         if t0 is None:
             t0 = blk[:, 0].min()
         row = []
-        for e, nm in enumerate(EV):
+        names = EVF if (ph == 1 and li + 1 < len(vs)) else EV
+        for e, nm in enumerate(names):
             col = blk[:, e]
             col = col[col > 0]
             if len(col) == 0:
                 continue
             row.append(f"{nm}={(col.min()-t0)/1e3:.2f}/{(np.median(col)-t0)/1e3:.2f}/{(col.max()-t0)/1e3:.2f}")
-        print(f"L{li} v{v} phase{'AB'[ph]} ctas={used.sum()}: " + " ".join(row))
+        kind = "fused" if (ph == 1 and li + 1 < len(vs)) else "phase" + "AB"[ph]
+        print(f"L{li} v{v} {kind} ctas={used.sum()}: " + " ".join(row))
