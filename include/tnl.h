@@ -80,7 +80,8 @@ enum {
   TNL_PLAN_CHAIN = 2,   /* core-by-core chain (Tucker-2: U_in, G, U_out; TT/TR:
                            input modes streamed, cut kept on chip)            */
   TNL_PLAN_GENERIC = 4, /* CUDA-core strided chain (exact fp32 FFMA path)     */
-  TNL_PLAN_NO_DECODE = 8 /* disable the small-M GEMV decode kernel            */
+  TNL_PLAN_NO_DECODE = 8, /* disable the small-M decode kernels                 */
+  TNL_PLAN_GEMV = 16     /* M <= 8: CUDA-core GEMV decode variant (warp per row) */
 };
 
 /* Host description of a layer (construct-from-cores, CompressedLayer fields).

@@ -7,7 +7,7 @@ in ``include/tnl.h``). There is no CPU fallback.
 """
 
 from . import modes
-from ._native import PLAN_AUTO, PLAN_CHAIN, PLAN_CUT, PLAN_GENERIC, PLAN_NO_DECODE, launch_count
+from ._native import PLAN_AUTO, PLAN_CHAIN, PLAN_CUT, PLAN_GEMV, PLAN_GENERIC, PLAN_NO_DECODE, launch_count
 from .errors import (
     DegenerateReferenceError,
     DeviceError,
@@ -49,6 +49,7 @@ __all__ = [
     "PLAN_CHAIN",
     "PLAN_GENERIC",
     "PLAN_NO_DECODE",
+    "PLAN_GEMV",
     "MinimaError",
     "ShapeError",
     "NumericsError",

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libtnl.so")
 TNL_OK, TNL_ERR_SHAPE, TNL_ERR_RANK, TNL_ERR_NUMERICS, TNL_ERR_CUDA, TNL_ERR_UNSUPPORTED, TNL_ERR_ARG = range(7)
 FAMILY_CODE = {"dense": 0, "tucker": 1, "tt": 2, "tr": 3}
 TNL_F64, TNL_F32, TNL_BF16 = 0, 1, 2
-PLAN_AUTO, PLAN_CUT, PLAN_CHAIN, PLAN_GENERIC, PLAN_NO_DECODE = 0, 1, 2, 4, 8
+PLAN_AUTO, PLAN_CUT, PLAN_CHAIN, PLAN_GENERIC, PLAN_NO_DECODE, PLAN_GEMV = 0, 1, 2, 4, 8, 16
 PLAN_NAMES = {PLAN_CUT: "cut", PLAN_CHAIN: "chain", PLAN_GENERIC: "generic", 0: "none"}
 MAX_MODES = 6
 

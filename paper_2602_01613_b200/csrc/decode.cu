@@ -265,10 +265,15 @@ int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& y,
 }
 
 // ---------------------------------------------------------------------------
-// CUDA-core GEMV variants (tokens <= 8)
+// CUDA-core GEMV variants (tokens <= 8): one warp per weight row, the whole
+// contraction in the warp (16-byte vector loads, warp-shuffle reduction), so
+// no split-K reduction and no atomics. A CTA's weight rows are contiguous and
+// arrive by one bulk TMA copy issued before griddepcontrol.wait; the
+// activations follow after the wait. T is plain fp32 [tokens][ldt].
 // ---------------------------------------------------------------------------
-constexpr int GV_CHUNK = 512;  // K elements per CTA (16 per lane)
 constexpr int GV_MAXT = 8;
+constexpr int GV_ROWS_A = 8;   // phase A: rows (warps) per CTA
+constexpr int GV_ROWS_B = 32;  // phase B: rows per CTA (4 per warp)
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -280,115 +285,131 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
   }
 }
 
-// T_acc[m][row] += sum_{k in chunk} W[row][k] x[m][k]; CTA = (chunk, 8 rows), warp = row
-__global__ void __launch_bounds__(256) gemv_a_kernel(const __nv_bfloat16* __restrict__ w, int64_t ldw,
-                                                     int rows, int K, const __nv_bfloat16* __restrict__ x,
-                                                     int64_t ldx, int tokens, float* t_acc, int64_t ldt) {
-  __shared__ __align__(16) __nv_bfloat16 xs[GV_MAXT][GV_CHUNK];
-  const int k0 = blockIdx.x * GV_CHUNK;
-  const int row = blockIdx.y * 8 + warp_id();
-  const int lane = lane_id();
-  // weights first (independent of the previous kernel)
-  uint4 wv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-  if (row < rows) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = k0 + (h * 32 + lane) * 8;
-      if (k < K) wv[h] = __ldg(reinterpret_cast<const uint4*>(w + (int64_t)row * ldw + k));
-    }
-  }
-  pdl_launch_dependents();
-  pdl_wait();
-  for (int e = threadIdx.x; e < tokens * (GV_CHUNK / 8); e += 256) {
-    const int m = e / (GV_CHUNK / 8), c = e % (GV_CHUNK / 8);
-    const int k = k0 + c * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (k < K) v = *reinterpret_cast<const uint4*>(x + (int64_t)m * ldx + k);
-    *reinterpret_cast<uint4*>(&xs[m][c * 8]) = v;
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// T[m][row] = sum_k W[row][k] x[m][k]   (W rows contiguous, ldw == K)
+__global__ void __launch_bounds__(256) gemv_a_kernel(const __nv_bfloat16* __restrict__ w, int rows, int K,
+                                                     const __nv_bfloat16* __restrict__ x, int64_t ldx,
+                                                     int tokens, float* t, int64_t ldt) {
+  extern __shared__ __align__(128) uint8_t gsm[];
+  __nv_bfloat16* ws = reinterpret_cast<__nv_bfloat16*>(gsm);                 // [8][K]
+  __nv_bfloat16* xs = ws + GV_ROWS_A * K;                                    // [tokens][K]
+  __shared__ __align__(8) uint64_t bar;
+  const int row0 = blockIdx.x * GV_ROWS_A;
+  const int nrows = min(GV_ROWS_A, rows - row0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
   }
   __syncthreads();
-  if (row >= rows) return;
-  float wf[2][8];
-  bf16x8_to_f32(wv[0], wf[0]);
-  bf16x8_to_f32(wv[1], wf[1]);
-  for (int m = 0; m < tokens; ++m) {
-    float acc = 0.f;
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)(nrows * K * 2));
+    bulk_g2s(ws, w + (int64_t)row0 * K, (uint32_t)(nrows * K * 2), &bar);
+  }
+  pdl_wait();
+  for (int e = threadIdx.x; e < tokens * (K / 8); e += 256) {
+    const int m = e / (K / 8), c = e % (K / 8);
+    reinterpret_cast<uint4*>(xs + (int64_t)m * K)[c] = __ldcg(reinterpret_cast<const uint4*>(x + (int64_t)m * ldx) + c);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int wid = warp_id(), lane = lane_id();
+  if (wid >= nrows) return;
+  float acc[GV_MAXT];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+  for (int m = 0; m < GV_MAXT; ++m) acc[m] = 0.f;
+  const uint4* wr = reinterpret_cast<const uint4*>(ws + (int64_t)wid * K);
+  for (int c = lane; c < K / 8; c += 32) {
+    float wf[8];
+    bf16x8_to_f32(wr[c], wf);
+#pragma unroll
+    for (int m = 0; m < GV_MAXT; ++m) {
+      if (m >= tokens) break;
       float xf[8];
-      bf16x8_to_f32(*reinterpret_cast<const uint4*>(&xs[m][(h * 32 + lane) * 8]), xf);
+      bf16x8_to_f32(reinterpret_cast<const uint4*>(xs + (int64_t)m * K)[c], xf);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc = fmaf(wf[h][i], xf[i], acc);
+      for (int i = 0; i < 8; ++i) acc[m] = fmaf(wf[i], xf[i], acc[m]);
     }
+  }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) atomicAdd(t_acc + (int64_t)row * ldt + m, acc);
+  for (int m = 0; m < GV_MAXT; ++m) {
+    if (m >= tokens) break;
+    float v = acc[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) t[(int64_t)m * ldt + row0 + wid] = v;
   }
 }
 
-// y[m][row] = sum_k W[row][k] T_acc[m][k]; K <= 1024. Lanes per row = min(32, K/8).
-__global__ void __launch_bounds__(256) gemv_b_kernel(const __nv_bfloat16* __restrict__ w, int64_t ldw,
-                                                     int rows, int K, float* t_acc, int64_t ldt,
-                                                     int tokens, __nv_bfloat16* y, int64_t ldy,
-                                                     unsigned int* counter) {
-  extern __shared__ float ts[];  // [tokens][K]
-  __shared__ unsigned last;
-  const int lpr = min(32, K / 8);         // lanes per row
-  const int rpw = 32 / lpr;               // rows per warp pass
-  const int lane = lane_id();
-  const int sub = lane / lpr, sl = lane % lpr;
-  const int rows_per_cta = 8 * rpw * 4;   // 4 passes per warp
-  const int row0 = blockIdx.x * rows_per_cta;
-  // weights first: up to 4 passes x (K / (8*lpr)) chunks per lane, K <= 1024 -> <= 4 chunks
-  const int nch = K / (8 * lpr);
-  uint4 wv[4][4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int row = row0 + (p * 8 + (int)warp_id()) * rpw + sub;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      wv[p][c] = make_uint4(0, 0, 0, 0);
-      if (c < nch && row < rows)
-        wv[p][c] = __ldg(reinterpret_cast<const uint4*>(w + (int64_t)row * ldw + (c * lpr + sl) * 8));
-    }
-  }
-  pdl_launch_dependents();
-  pdl_wait();
-  for (int e = threadIdx.x; e < tokens * K; e += 256) {  // kappa-major [k][ldt] -> [m][k]
-    const int k = e / tokens, m = e % tokens;
-    ts[m * K + k] = __ldcg(t_acc + (int64_t)k * ldt + m);
-  }
-  __syncthreads();
+// y[m][row] = sum_k W[row][k] bf16(T[m][k])   (W rows contiguous, ldw == K, K % 8 == 0)
+__global__ void __launch_bounds__(256) gemv_b_kernel(const __nv_bfloat16* __restrict__ w, int rows, int K,
+                                                     const float* __restrict__ t, int64_t ldt, int tokens,
+                                                     __nv_bfloat16* y, int64_t ldy) {
+  extern __shared__ __align__(128) uint8_t gsm[];
+  __nv_bfloat16* ws = reinterpret_cast<__nv_bfloat16*>(gsm);   // [32][K]
+  float* ts = reinterpret_cast<float*>(ws + GV_ROWS_B * K);     // [tokens][K]
+  __shared__ __align__(8) uint64_t bar;
+  const int row0 = blockIdx.x * GV_ROWS_B;
+  const int nrows = min(GV_ROWS_B, rows - row0);
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned old = atomicAdd(counter, 1u);
-    last = (old == gridDim.x - 1) ? 1u : 0u;
-  }
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int row = row0 + (p * 8 + (int)warp_id()) * rpw + sub;
-    float wf[4][8];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) bf16x8_to_f32(wv[p][c], wf[c]);
-    for (int m = 0; m < tokens; ++m) {
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c >= nch) break;
-        const float* t = ts + m * K + (c * lpr + sl) * 8;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc = fmaf(wf[c][i], t[i], acc);
-      }
-      for (int o = lpr / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (sl == 0 && row < rows) y[(int64_t)m * ldy + row] = __float2bfloat16_rn(acc);
-    }
+    mbar_init(&bar, 1);
+    fence_barrier_init();
   }
   __syncthreads();
-  if (last) {
-    __threadfence();
-    float4* z = reinterpret_cast<float4*>(t_acc);
-    for (int e = threadIdx.x; e < K * ldt / 4; e += 256) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (threadIdx.x == 0) atomicExch(counter, 0u);
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)(nrows * K * 2));
+    bulk_g2s(ws, w + (int64_t)row0 * K, (uint32_t)(nrows * K * 2), &bar);
+  }
+  pdl_wait();
+  for (int e = threadIdx.x; e < tokens * K / 4; e += 256) {
+    const int m = e / (K / 4), c = e % (K / 4);
+    reinterpret_cast<float4*>(ts + (int64_t)m * K)[c] = __ldcg(reinterpret_cast<const float4*>(t + (int64_t)m * ldt) + c);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int wid = warp_id(), lane = lane_id();
+  for (int rr = 0; rr < GV_ROWS_B / 8; ++rr) {
+    const int lr = wid * (GV_ROWS_B / 8) + rr;
+    if (lr >= nrows) break;
+    float acc[GV_MAXT];
+#pragma unroll
+    for (int m = 0; m < GV_MAXT; ++m) acc[m] = 0.f;
+    const uint4* wr = reinterpret_cast<const uint4*>(ws + (int64_t)lr * K);
+    for (int c = lane; c < K / 8; c += 32) {
+      float wf[8];
+      bf16x8_to_f32(wr[c], wf);
+#pragma unroll
+      for (int m = 0; m < GV_MAXT; ++m) {
+        if (m >= tokens) break;
+        const float4* tp = reinterpret_cast<const float4*>(ts + (int64_t)m * K + c * 8);
+        const float4 a0 = tp[0], a1 = tp[1];
+        // T is rounded to bf16 exactly as the tensor-core path rounds its operand
+        acc[m] = fmaf(wf[0], __bfloat162float(__float2bfloat16_rn(a0.x)), acc[m]);
+        acc[m] = fmaf(wf[1], __bfloat162float(__float2bfloat16_rn(a0.y)), acc[m]);
+        acc[m] = fmaf(wf[2], __bfloat162float(__float2bfloat16_rn(a0.z)), acc[m]);
+        acc[m] = fmaf(wf[3], __bfloat162float(__float2bfloat16_rn(a0.w)), acc[m]);
+        acc[m] = fmaf(wf[4], __bfloat162float(__float2bfloat16_rn(a1.x)), acc[m]);
+        acc[m] = fmaf(wf[5], __bfloat162float(__float2bfloat16_rn(a1.y)), acc[m]);
+        acc[m] = fmaf(wf[6], __bfloat162float(__float2bfloat16_rn(a1.z)), acc[m]);
+        acc[m] = fmaf(wf[7], __bfloat162float(__float2bfloat16_rn(a1.w)), acc[m]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < GV_MAXT; ++m) {
+      if (m >= tokens) break;
+      float v = acc[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) y[(int64_t)m * ldy + row0 + lr] = __float2bfloat16_rn(v);
+    }
   }
 }
 
@@ -427,23 +448,33 @@ int launch_dec_b(const CUtensorMap& w, const CUtensorMap& t, const CUtensorMap& 
 }
 
 int launch_gemv_a(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const __nv_bfloat16* x, int64_t ldx,
-                  int tokens, float* t_acc, int64_t ldt, cudaStream_t st) {
-  if (tokens > GV_MAXT || K % 8) return (int)cudaErrorInvalidValue;
-  dim3 grid((K + GV_CHUNK - 1) / GV_CHUNK, (rows + 7) / 8);
-  return launch_pdl(gemv_a_kernel, grid, dim3(256), 0, st, w, ldw, rows, K, x, ldx, tokens, t_acc, ldt);
+                  int tokens, float* t, int64_t ldt, cudaStream_t st) {
+  if (tokens > GV_MAXT || K % 8 || ldw != K || (ldx % 8)) return (int)cudaErrorInvalidValue;
+  const size_t smem = (size_t)(GV_ROWS_A + tokens) * K * 2;
+  if (smem > 220 * 1024) return (int)cudaErrorInvalidValue;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemv_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return (int)e;
+    attr = 220 * 1024;
+  }
+  return launch_pdl(gemv_a_kernel, dim3((rows + GV_ROWS_A - 1) / GV_ROWS_A), dim3(256), smem, st, w, rows, K, x,
+                    ldx, tokens, t, ldt);
 }
 
-int launch_gemv_b(const __nv_bfloat16* w, int64_t ldw, int rows, int K, float* t_acc, int64_t ldt, int tokens,
-                  __nv_bfloat16* y, int64_t ldy, unsigned int* counter, cudaStream_t st) {
-  const int l8 = K / 8;
-  const bool ok = (K % 8 == 0) && ((l8 <= 32 && (l8 & (l8 - 1)) == 0) || (K % 256 == 0 && K <= 1024));
-  if (tokens > GV_MAXT || !ok) return (int)cudaErrorInvalidValue;
-  const int lpr = K / 8 < 32 ? K / 8 : 32;
-  const int rows_per_cta = 8 * (32 / lpr) * 4;
-  dim3 grid((rows + rows_per_cta - 1) / rows_per_cta);
-  const size_t smem = sizeof(float) * tokens * K;
-  return launch_pdl(gemv_b_kernel, grid, dim3(256), smem, st, w, ldw, rows, K, t_acc, ldt, tokens, y, ldy,
-                    counter);
+int launch_gemv_b(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const float* t, int64_t ldt, int tokens,
+                  __nv_bfloat16* y, int64_t ldy, cudaStream_t st) {
+  if (tokens > GV_MAXT || K % 8 || ldw != K) return (int)cudaErrorInvalidValue;
+  const size_t smem = (size_t)GV_ROWS_B * K * 2 + (size_t)tokens * K * 4;
+  if (smem > 220 * 1024) return (int)cudaErrorInvalidValue;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemv_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return (int)e;
+    attr = 220 * 1024;
+  }
+  return launch_pdl(gemv_b_kernel, dim3((rows + GV_ROWS_B - 1) / GV_ROWS_B), dim3(256), smem, st, w, rows, K, t,
+                    ldt, tokens, y, ldy);
 }
 
 }  // namespace tnl

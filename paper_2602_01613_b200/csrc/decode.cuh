@@ -71,11 +71,11 @@ struct FusedArgs {
 int launch_dec_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi,
                      const FusedArgs& a, int grid, cudaStream_t st);
 
-// CUDA-core GEMV variants (tokens <= 8)
+// CUDA-core GEMV variants (tokens <= 8): warp per weight row, no atomics.
+// T is fp32 [tokens][ldt] (plain stores, no zero-at-rest requirement).
 int launch_gemv_a(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const __nv_bfloat16* x,
-                  int64_t ldx, int tokens, float* t_acc, int64_t ldt, cudaStream_t st);
-int launch_gemv_b(const __nv_bfloat16* w, int64_t ldw, int rows, int K, float* t_acc, int64_t ldt,
-                  int tokens, __nv_bfloat16* y, int64_t ldy, unsigned int* counter,
-                  cudaStream_t st);
+                  int64_t ldx, int tokens, float* t, int64_t ldt, cudaStream_t st);
+int launch_gemv_b(const __nv_bfloat16* w, int64_t ldw, int rows, int K, const float* t, int64_t ldt,
+                  int tokens, __nv_bfloat16* y, int64_t ldy, cudaStream_t st);
 
 }  // namespace tnl

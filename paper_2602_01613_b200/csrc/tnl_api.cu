@@ -1095,12 +1095,6 @@ static tnl_status chain_in(tnl_plan* P, const void* x, int64_t ldx, int64_t M, v
 
 static constexpr int64_t kDecMaxM = 64;  // decode path (plan-owned accumulator capacity)
 
-static bool gemv_ok_k(int64_t K) {
-  if (K % 8) return false;
-  const int64_t l = K / 8;
-  if (l <= 32) return (l & (l - 1)) == 0;
-  return K % 256 == 0 && K <= 1024;
-}
 
 // Small-M path of the merged-cut plan: phase A (B_in, split-K, fp32 reductions into the
 // plan-owned accumulator) + phase B (A_out, reads the fp32 accumulator, re-zeroes it).
@@ -1113,12 +1107,14 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
   const int64_t rows_local = P->row_end - P->row_begin;
   int err = 0;
   const bool use_chain = P->plan_large == TNL_PLAN_CHAIN && P->chain_ok;
-  if (M <= 8 && gemv_ok_k(P->r_pad) && !use_chain) {
-    err = launch_gemv_a(P->bin, P->cols, (int)P->r_pad, (int)P->cols,
-                        static_cast<const __nv_bfloat16*>(x), ldx, (int)M, tacc, kDecMaxM, st);
+  if (M <= 8 && !use_chain && (P->flags & TNL_PLAN_GEMV)) {
+    // CUDA-core GEMV variant; T goes to the (non-accumulating) scratch after the accumulator
+    float* t = reinterpret_cast<float*>(static_cast<char*>(ws) + round_up(sizeof(float) * 64 * P->r_pad, 256) + 256);
+    err = launch_gemv_a(P->bin, P->cols, (int)P->r_pad, (int)P->cols, static_cast<const __nv_bfloat16*>(x), ldx,
+                        (int)M, t, P->r_pad, st);
     if (err) return fail(TNL_ERR_CUDA, "gemv_a launch: %s", cudaGetErrorString((cudaError_t)err));
-    err = launch_gemv_b(P->aout, P->r_pad, (int)rows_local, (int)P->r_pad, tacc, kDecMaxM, (int)M,
-                        static_cast<__nv_bfloat16*>(y), ldy, counter, st);
+    err = launch_gemv_b(P->aout, P->r_pad, (int)rows_local, (int)P->r_pad, t, P->r_pad, (int)M,
+                        static_cast<__nv_bfloat16*>(y), ldy, st);
     if (err) return fail(TNL_ERR_CUDA, "gemv_b launch: %s", cudaGetErrorString((cudaError_t)err));
     return TNL_OK;
   }

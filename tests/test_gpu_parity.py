@@ -308,3 +308,13 @@ def test_stack_fused_matches_oracle_chain(m):
         cur = layer.plan(torch.bfloat16).forward(cur)
     d = (cur.float() - y.float()).norm() / cur.float().norm()
     assert float(d) < 2e-2
+
+
+@pytest.mark.parametrize("spec", [("tucker", (5120, 5120), 1, (128, 128)), ("tr", (64, 80, 64, 80), 2, (16, 16, 16, 16)),
+                                  ("tr", (5120, 5120), 1, (8, 8)), ("tt", (16, 16, 16, 16), 2, (8, 8, 8))])
+@pytest.mark.parametrize("m", [1, 5, 8])
+def test_decode_gemv_variant(spec, m):
+    """CUDA-core GEMV decode variant (warp per weight row, no atomics) for M <= 8."""
+    fam, ms, rm, rk = spec
+    L = O.synthetic_layer(fam, ms, rm, rk, seed=49_000 + m)
+    check_bf16(L, m, seed=49_500 + m, flags=tnl.PLAN_GEMV)
