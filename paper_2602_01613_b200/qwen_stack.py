@@ -1,0 +1,126 @@
+"""Qwen3-32B-shaped stack driver of TN projections (BASELINE cfg4).
+
+64 decoder layers x {q 5120->8192, k/v 5120->1024, o 8192->5120, gate/up 5120->25600,
+down 25600->5120}, all TN-compressed with the pinned "sensitivity-mix" layout of SURVEY §8(d):
+  q/o Tucker-2 R256; k/v Tucker-2 R128;
+  MLP: layers 0-1 and 62-63 Tucker-2 R256 (fragile edges, mirroring planner.py:140-143);
+       other layers rotate by l mod 3 among TT r64, TR4 (4,16,16,16) and
+       Tucker-4 (32,32,16,16) (down: (16,16,32,32)).
+Mode shapes come from ``default_mode_shape`` (tn_decompositions.py:59-63); Tucker-2 uses the
+two-mode (rows | cols) shape.
+
+The attention core is not part of the TN-linear path: it is a pass-through (the attention
+output is taken to be q). Pre-norm as in Qwen3 (RMSNorm without learned scale), per layer:
+  h = rms(x); q, k, v = Lq(h), Lk(h), Lv(h);  x = x + Lo(q)
+  h = rms(x); x = x + Ld(silu(Lg(h)) * Lu(h))
+The projections run through libtnl (tnl_forward); residual adds and SiLU*mul are torch
+element-wise plumbing. ``capture(m)`` records one whole pass into a CUDA graph.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import synthetic as S
+from .modes import default_mode_shape
+
+HIDDEN, QDIM, KVDIM, FFN = 5120, 8192, 1024, 25600
+
+
+def _tn(kind: str, rows: int, cols: int, seed: int):
+    if kind.startswith("tucker2-"):
+        r = int(kind.split("-")[1])
+        return S.make_layer("tucker", (rows, cols), 1, (r, r), seed)
+    ms, rm = default_mode_shape(rows, cols)
+    if kind == "tt64":
+        return S.make_layer("tt", ms, rm, (64,) * (len(ms) - 1), seed)
+    if kind == "tr4":
+        return S.make_layer("tr", ms, rm, (4, 16, 16, 16), seed)
+    if kind == "tucker4":
+        ranks = (32, 32, 16, 16) if rows > cols else (16, 16, 32, 32)
+        return S.make_layer("tucker", ms, rm, ranks, seed)
+    raise ValueError(kind)
+
+
+def layer_kinds(l: int, n_layers: int = 64) -> dict:
+    mlp = "tucker2-256" if (l < 2 or l >= n_layers - 2) else ("tt64", "tr4", "tucker4")[l % 3]
+    return {"q": "tucker2-256", "k": "tucker2-128", "v": "tucker2-128", "o": "tucker2-256",
+            "gate": mlp, "up": mlp, "down": mlp}
+
+
+SHAPES = {"q": (QDIM, HIDDEN), "k": (KVDIM, HIDDEN), "v": (KVDIM, HIDDEN), "o": (HIDDEN, QDIM),
+          "gate": (FFN, HIDDEN), "up": (FFN, HIDDEN), "down": (HIDDEN, FFN)}
+
+
+class QwenTNStack:
+    def __init__(self, n_layers: int = 64, dtype=torch.bfloat16, device=None, seed: int = 40_000):
+        self.n_layers = n_layers
+        self.dtype = dtype
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.layers = []
+        for l in range(n_layers):
+            kinds = layer_kinds(l, n_layers)
+            blk = {}
+            for j, name in enumerate(("q", "k", "v", "o", "gate", "up", "down")):
+                rows, cols = SHAPES[name]
+                layer = _tn(kinds[name], rows, cols, seed=seed + 100 * l + 10 * j)
+                blk[name] = (kinds[name], layer, layer.plan(dtype, self.device))
+            self.layers.append(blk)
+        self._ws = None
+
+    def param_count(self) -> int:
+        from .layer import param_count
+
+        return sum(param_count(lay) for blk in self.layers for _, lay, _ in blk.values())
+
+    def chain_flops_per_token(self) -> int:
+        return sum(lay.chain_flops_per_token() for blk in self.layers for _, lay, _ in blk.values())
+
+    def workspace(self, m: int):
+        need = max(p.workspace_bytes(m) for blk in self.layers for _, _, p in blk.values())
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _buffers(self, m: int):
+        mk = lambda n: torch.empty((m, n), dtype=self.dtype, device=self.device)  # noqa: E731
+        return {"h": mk(HIDDEN), "q": mk(QDIM), "k": mk(KVDIM), "v": mk(KVDIM), "o": mk(HIDDEN), "g": mk(FFN),
+                "u": mk(FFN), "d": mk(HIDDEN)}
+
+    def forward(self, x: torch.Tensor, bufs=None) -> torch.Tensor:
+        """One pass of all layers; x (M x 5120) is updated in place (residual stream)."""
+        m = x.shape[0]
+        ws = self.workspace(m)
+        b = bufs or self._buffers(m)
+        rms = lambda t: torch.nn.functional.rms_norm(t, (HIDDEN,), eps=1e-6)  # noqa: E731
+        for blk in self.layers:
+            b["h"].copy_(rms(x))
+            blk["q"][2].forward(b["h"], out=b["q"], ws=ws)
+            blk["k"][2].forward(b["h"], out=b["k"], ws=ws)
+            blk["v"][2].forward(b["h"], out=b["v"], ws=ws)
+            blk["o"][2].forward(b["q"], out=b["o"], ws=ws)  # attention core: pass-through
+            x.add_(b["o"])
+            b["h"].copy_(rms(x))
+            blk["gate"][2].forward(b["h"], out=b["g"], ws=ws)
+            blk["up"][2].forward(b["h"], out=b["u"], ws=ws)
+            torch.nn.functional.silu(b["g"], inplace=True)
+            b["g"].mul_(b["u"])
+            blk["down"][2].forward(b["g"], out=b["d"], ws=ws)
+            x.add_(b["d"])
+        return x
+
+    def capture(self, m: int):
+        self.x = torch.zeros((m, HIDDEN), dtype=self.dtype, device=self.device)
+        self.bufs = self._buffers(m)
+        self.workspace(m)
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.forward(self.x, self.bufs)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.forward(self.x, self.bufs)
+        self.graph = g
+        return g
