@@ -681,6 +681,51 @@ static tnl_status alloc_arena(tnl_plan* P, size_t bytes) {
 // by running the segment's chain on identity inputs in chunks.
 static tnl_status build_panel_f32(tnl_plan* P, int seg, float* out, cudaStream_t st) {
   const int64_t K = P->r_cut;
+  // Single-mode sides: the panel is one core, permuted (TT/TR, Tucker factor) or one
+  // GEMM (Tucker U0 . G); no identity chain needed.
+  const int d = P->d, rm = P->rm;
+  const int64_t nr = P->row_end - P->row_begin;
+  const bool ttr = P->family == TNL_FAMILY_TT || P->family == TNL_FAMILY_TR;
+  if (seg == SEG_INPUT && d - rm == 1 && (ttr || P->tucker_cut_in)) {
+    const int64_t n = P->ms[d - 1];
+    if (ttr) {  // B_in[(alpha,b)][j] = D[b][j][alpha]; gcore[d-1] is [alpha][j][b]
+      const int64_t b = P->rk[d - 1], r0 = P->rk[d];
+      for (int64_t al = 0; al < r0; ++al)
+        copy_2d_any<<<grid_for(b * n), 256, 0, st>>>(P->gcore[d - 1] + al * n * b, DT_F32, 1, b,
+                                                     out + al * b * n, DT_F32, n, 1, b, n);
+    } else {  // B_in = U_{d-1}^T
+      const int64_t R = P->rk[d - 1];
+      copy_2d_any<<<grid_for(R * n), 256, 0, st>>>(P->gcore[1 + d - 1], DT_F32, 1, R, out, DT_F32, n, 1, R, n);
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    return TNL_OK;
+  }
+  if (seg == SEG_OUTPUT && rm == 1) {
+    if (ttr) {  // A_out[i][(alpha,b)] = G0[alpha][i][b]; gcore[0] is [i][(alpha,b)] already
+      copy_2d_any<<<grid_for(nr * K), 256, 0, st>>>(P->gcore[0] + P->row_begin * K, DT_F32, K, 1, out, DT_F32, K,
+                                                    1, nr, K);
+    } else if (P->tucker_cut_in) {  // A_out = U0[rows] . G  (rows x R_in)
+      const int64_t R0 = P->rk[0], Rin = K;
+      GStep g = mk(1, 1, nr, R0, Rin);
+      g.A = P->gcore[1] + P->row_begin * R0;
+      g.sai = R0;
+      g.sap = 1;
+      g.B = P->gcore[0];
+      g.sbp = Rin;
+      g.sbj = 1;
+      g.C = out;
+      g.sci = Rin;
+      g.scj = 1;
+      if (launch_generic_step(g, st)) return fail(TNL_ERR_CUDA, "panel GEMM launch failed");
+    } else {  // cut on R_out: A_out = U0[rows]
+      copy_2d_any<<<grid_for(nr * K), 256, 0, st>>>(P->gcore[1] + P->row_begin * K, DT_F32, K, 1, out, DT_F32, K,
+                                                    1, nr, K);
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    return TNL_OK;
+  }
   const int64_t n_in = (seg == SEG_INPUT) ? P->cols : K;       // identity size
   const int64_t chunk = std::min<int64_t>(n_in, 512);
   float *eye = nullptr, *ws0 = nullptr, *ws1 = nullptr, *tmp = nullptr;
