@@ -117,6 +117,7 @@ typedef struct {
 } tnl_plan_info;
 
 typedef struct tnl_plan tnl_plan;
+typedef struct tnl_mlp tnl_mlp;
 
 TNL_API int tnl_abi_version(void);
 TNL_API const char* tnl_last_error(void);
@@ -162,6 +163,21 @@ TNL_API tnl_status tnl_stack_workspace_size(const tnl_plan* const* plans, int32_
 TNL_API tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void* x,
                                      int64_t m, int64_t ldx, void* y, int64_t ldy, void* workspace,
                                      size_t workspace_bytes, void* stream);
+
+/* Qwen3 MLP block of three TN layers: y = down(silu(gate(x)) * up(x)).
+ * For merged-cut bf16 plans (gate/up cut <= 128, down cut <= 256) and M > 64 the
+ * intermediate h (M x inter) never reaches HBM: one kernel streams chunks of the
+ * gate/up output panels and the down input panel, applies SiLU*mul on chip and
+ * folds h into down's cut accumulator. Otherwise (or flags & 1) it runs unfused.
+ * The plans must outlive the block. */
+TNL_API tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_plan* down,
+                                  int32_t flags, tnl_mlp** out);
+TNL_API tnl_status tnl_mlp_destroy(tnl_mlp* mlp);
+TNL_API int32_t tnl_mlp_is_fused(const tnl_mlp* mlp);
+TNL_API tnl_status tnl_mlp_workspace_size(const tnl_mlp* mlp, int64_t m, size_t* bytes);
+TNL_API tnl_status tnl_mlp_forward(const tnl_mlp* mlp, const void* x, int64_t m, int64_t ldx,
+                                   void* y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                                   void* stream);
 
 /* Number of libtnl kernel launches issued by this thread since the last reset
  * (evidence counter for benchmarks). */

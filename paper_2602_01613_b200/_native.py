@@ -39,6 +39,11 @@ EXPORTED = (
     "tnl_plan_set_trace",
     "tnl_stack_workspace_size",
     "tnl_stack_forward",
+    "tnl_mlp_create",
+    "tnl_mlp_destroy",
+    "tnl_mlp_is_fused",
+    "tnl_mlp_workspace_size",
+    "tnl_mlp_forward",
 )
 
 
@@ -113,6 +118,16 @@ def load():
         lib.tnl_stack_forward.argtypes = [ctypes.POINTER(P), ctypes.c_int32, P, i64, i64, P, i64, P,
                                           ctypes.c_size_t, P]
         lib.tnl_stack_forward.restype = ctypes.c_int
+        lib.tnl_mlp_create.argtypes = [P, P, P, ctypes.c_int32, ctypes.POINTER(P)]
+        lib.tnl_mlp_create.restype = ctypes.c_int
+        lib.tnl_mlp_destroy.argtypes = [P]
+        lib.tnl_mlp_destroy.restype = ctypes.c_int
+        lib.tnl_mlp_is_fused.argtypes = [P]
+        lib.tnl_mlp_is_fused.restype = ctypes.c_int32
+        lib.tnl_mlp_workspace_size.argtypes = [P, i64, ctypes.POINTER(ctypes.c_size_t)]
+        lib.tnl_mlp_workspace_size.restype = ctypes.c_int
+        lib.tnl_mlp_forward.argtypes = [P, P, i64, i64, P, i64, P, ctypes.c_size_t, P]
+        lib.tnl_mlp_forward.restype = ctypes.c_int
         lib.tnl_plan_set_trace.argtypes = [P, P]
         lib.tnl_plan_set_trace.restype = ctypes.c_int
         lib.tnl_launch_count.argtypes = [ctypes.c_int32]

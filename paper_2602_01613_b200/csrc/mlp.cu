@@ -1,0 +1,302 @@
+// mlp.cu — fused middle of a TN-compressed Qwen3 MLP block.
+//
+//   y = down( silu(gate(x)) * up(x) ),  gate/up/down merged-cut TN layers.
+// With the cut panels (gate: B_g, A_g; up: B_u, A_u; down: B_d, A_d) the block is
+//   T_g = x B_g^T, T_u = x B_u^T                 (one GEMM over the concatenated B_g|B_u)
+//   h   = silu(T_g A_g^T) * (T_u A_u^T)          (M x 25600 — the expensive intermediate)
+//   T_d = h B_d^T                                 (contracts the 25600 intermediate)
+//   y   = T_d A_d^T
+// This kernel fuses the middle two lines: per (128-token tile, slice of the intermediate)
+// it streams 64-column chunks of A_g, A_u, B_d through an smem ring; G and U land in
+// double-buffered TMEM accumulators, the epilogue warps apply SiLU*mul and write the bf16
+// h chunk straight into a 128B-swizzled smem operand, and the next MMA folds it into the
+// T_d accumulator (TMEM). h never touches HBM; only the (M x r_d) partial T_d is reduced
+// into global memory (fp32, vector reductions).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "mlp.cuh"
+#include "ptx.cuh"
+
+namespace tnl {
+
+namespace {
+
+constexpr int CH = 64;                        // intermediate columns per chunk
+constexpr uint32_t TBLK = 128 * 64 * 2;       // 128-row x 64-k bf16 block (16 KB)
+constexpr uint32_t WBLK = 64 * 64 * 2;        // 64-row x 64-k bf16 weight block (8 KB)
+
+__device__ __forceinline__ void nbar(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct MlpLayout {
+  int kg, ku, kd;  // k-blocks of r_g, r_u; r_d/64 row blocks of B_d chunk
+  uint32_t stage, ag_off, au_off, bd_off;
+  int stages;
+  int nb;   // G/U TMEM accumulator pairs (and h smem buffers) in flight
+  int lag;  // the T_d MMA of chunk i-lag is issued after the G/U MMAs of chunk i
+  size_t t_bytes, total;
+};
+
+__host__ __device__ inline MlpLayout mlp_layout(const MlpArgs& a) {
+  MlpLayout L;
+  L.kg = a.rg / 64;
+  L.ku = a.ru / 64;
+  L.kd = a.rd / 64;
+  L.ag_off = 0;
+  L.au_off = L.kg * WBLK;
+  L.bd_off = L.au_off + L.ku * WBLK;
+  L.stage = L.bd_off + (uint32_t)a.rd * 128;  // B_d chunk: rd rows x 64 k (128 B rows)
+  L.stage = (L.stage + 1023) / 1024 * 1024;
+  L.t_bytes = (size_t)(L.kg + L.ku) * TBLK;
+  L.nb = (3 * 128 + a.rd <= 512) ? 3 : 2;  // TMEM: nb x (G|U 128 cols) + T_d (rd cols)
+  size_t fixed = 1024 + L.t_bytes + (size_t)L.nb * TBLK /*h*/ + 256;
+  L.stages = 4;
+  while (L.stages > 2 && fixed + (size_t)L.stages * L.stage > 227 * 1024) --L.stages;
+  if (fixed + (size_t)L.stages * L.stage > 227 * 1024 && L.nb == 3) {
+    L.nb = 2;
+    fixed -= TBLK;
+  }
+  L.lag = L.nb - 1 < L.stages - 2 ? L.nb - 1 : L.stages - 2;
+  if (L.lag < 1) L.lag = 1;
+  L.total = fixed + (size_t)L.stages * L.stage;
+  return L;
+}
+
+// silu(g) = g * sigmoid(g) = g * (0.5 + 0.5 tanh(g/2)): one MUFU op (tanh.approx) per element
+// instead of two (ex2 + rcp) — the SFU is the epilogue's bottleneck (8192 elements per chunk).
+__device__ __forceinline__ float silu(float g) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * g));
+  return g * fmaf(0.5f, t, 0.5f);
+}
+
+// warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (two warps per TMEM lane quarter, 32 columns each)
+constexpr int MLP_THREADS = 320, MLP_EPI = 256;
+
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+    mlp_mid_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmAg,
+                   const __grid_constant__ CUtensorMap tmAu, const __grid_constant__ CUtensorMap tmBd,
+                   const MlpArgs a) {
+  const MlpLayout L = mlp_layout(a);
+  const int S = L.stages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sT = smem;                    // [kg blocks of T_g][ku blocks of T_u]
+  const int NB = L.nb;
+  uint8_t* sH = sT + L.t_bytes;          // NB x 16 KB
+  uint8_t* sR = sH + NB * TBLK;          // ring stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sR + (size_t)S * L.stage);
+  uint64_t* full = bars;           // [4]
+  uint64_t* empty = bars + 4;      // [4]
+  uint64_t* tfull = bars + 8;
+  uint64_t* gu_full = bars + 9;    // [3]
+  uint64_t* gu_empty = bars + 12;  // [3]
+  uint64_t* h_full = bars + 15;    // [3]
+  uint64_t* h_empty = bars + 18;   // [3]
+  uint64_t* td_done = bars + 21;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+
+  const int tile = blockIdx.x;
+  const int total_ch = a.inter / CH;
+  const int c0 = blockIdx.y * a.chunks_per_slice;
+  const int nch = min(total_ch, c0 + a.chunks_per_slice) - c0;
+  const uint32_t warp = warp_id();
+  const uint32_t stage_tx = (uint32_t)((L.kg + L.ku) * WBLK + a.rd * 128);
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmT);
+    tma_prefetch_desc(&tmAg);
+    tma_prefetch_desc(&tmAu);
+    tma_prefetch_desc(&tmBd);
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&gu_full[b], 1);
+      mbar_init(&gu_empty[b], 8);
+      mbar_init(&h_full[b], 8);
+      mbar_init(&h_empty[b], 1);
+    }
+    mbar_init(td_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tTD = tmem + NB * 128;  // T_d accumulator (rd columns)
+  pdl_launch_dependents();
+
+  if (nch > 0) {
+    if (warp == 0) {
+      if (elect_one()) {
+        auto load_stage = [&](int i) {
+          const int s = i % S;
+          uint8_t* st = sR + (size_t)s * L.stage;
+          const int col = (c0 + i) * CH;  // intermediate column of this chunk
+          mbar_arrive_expect_tx(&full[s], stage_tx);
+          for (int k = 0; k < L.kg; ++k) tma_load_2d(st + L.ag_off + k * WBLK, &tmAg, &full[s], k * 64, col);
+          for (int k = 0; k < L.ku; ++k) tma_load_2d(st + L.au_off + k * WBLK, &tmAu, &full[s], k * 64, col);
+          tma_load_2d(st + L.bd_off, &tmBd, &full[s], col, 0);
+        };
+        const int npre = min(nch, S);
+        for (int i = 0; i < npre; ++i) load_stage(i);  // weights: before the dependency wait
+        pdl_wait();
+        mbar_arrive_expect_tx(tfull, (uint32_t)((L.kg + L.ku) * TBLK));
+        for (int k = 0; k < L.kg + L.ku; ++k) tma_load_2d(sT + k * TBLK, &tmT, tfull, k * 64, tile * 128);
+        for (int i = npre; i < nch; ++i) {
+          mbar_wait(&empty[i % S], ((i / S) & 1) ^ 1);
+          load_stage(i);
+        }
+      }
+    } else if (warp == 1) {
+      if (elect_one()) {
+        const uint32_t idesc_gu = idesc_bf16_f32(128, CH);
+        const uint32_t idesc_d = idesc_bf16_f32(128, a.rd);
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        auto mma_d = [&](int j) {  // T_d += h_j . B_d[:, chunk j]^T, then free stage j and h_j
+          const int s = j % S;
+          mbar_wait(&h_full[j % NB], (j / NB) & 1);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_sw128(smem_u32(sH + (j % NB) * TBLK));
+          const uint64_t bd = smem_desc_sw128(smem_u32(sR + (size_t)s * L.stage + L.bd_off));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_bf16_ss(tTD, ad + 2 * k, bd + 2 * k, idesc_d, (j > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&h_empty[j % NB]);
+          mma_commit(&empty[s]);
+        };
+        unsigned long long* tr = (a.trace && blockIdx.x == 0 && blockIdx.y == 0) ? a.trace : nullptr;
+        for (int i = 0; i < nch; ++i) {
+          const int s = i % S;
+          const int b = i % NB;
+          mbar_wait(&full[s], (i / S) & 1);
+          if (tr && i < 256) tr[i * 4 + 0] = globaltimer();
+          if (i >= NB) mbar_wait(&gu_empty[b], ((i / NB) & 1) ^ 1);
+          tc_fence_after();
+          uint8_t* st = sR + (size_t)s * L.stage;
+          const uint32_t tG = tmem + b * 128, tU = tG + 64;
+          for (int k = 0; k < L.kg; ++k) {
+            const uint64_t ad = smem_desc_sw128(smem_u32(sT + k * TBLK));
+            const uint64_t bd = smem_desc_sw128(smem_u32(st + L.ag_off + k * WBLK));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mma_bf16_ss(tG, ad + 2 * q, bd + 2 * q, idesc_gu, (k | q) != 0);
+          }
+          for (int k = 0; k < L.ku; ++k) {
+            const uint64_t ad = smem_desc_sw128(smem_u32(sT + (L.kg + k) * TBLK));
+            const uint64_t bd = smem_desc_sw128(smem_u32(st + L.au_off + k * WBLK));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mma_bf16_ss(tU, ad + 2 * q, bd + 2 * q, idesc_gu, (k | q) != 0);
+          }
+          mma_commit(&gu_full[b]);
+          if (tr && i < 256) tr[i * 4 + 1] = globaltimer();
+          if (i >= L.lag) mma_d(i - L.lag);
+        }
+        for (int j = nch - L.lag < 0 ? 0 : nch - L.lag; j < nch; ++j) mma_d(j);
+        mma_commit(td_done);
+      }
+      __syncwarp();
+    } else {
+      const uint32_t q = warp & 3;
+      const int lrow = q * 32 + lane_id();
+      const uint32_t lane_base = (q * 32) << 16;
+      unsigned long long* tr = (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && warp == 2 && lane_id() == 0) ? a.trace : nullptr;
+      for (int i = 0; i < nch; ++i) {
+        const int b = i % NB;
+        mbar_wait(&gu_full[b], (i / NB) & 1);
+        tc_fence_after();
+        if (tr && i < 256) tr[i * 4 + 2] = globaltimer();
+        if (i >= NB) mbar_wait(&h_empty[b], ((i / NB) & 1) ^ 1);
+        if (tr && i < 256) tr[1024 + i * 4 + 2] = globaltimer();
+        uint8_t* rowp = sH + b * TBLK + (lrow >> 3) * 1024 + (lrow & 7) * 128;
+        const int cb = ((warp - 2) >> 2) * 32;  // this warp's 32 columns of the chunk
+        const uint32_t tG = tmem + b * 128 + lane_base + cb, tU = tG + 64;
+        uint32_t gr[32], ur[32];
+        tmem_ld32_nowait(tG, gr);
+        tmem_ld32_nowait(tU, ur);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&gu_empty[b]);  // accumulator pair b may be overwritten
+        if (tr && i < 256) tr[1024 + i * 4 + 0] = globaltimer();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 p;
+          float h[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            h[e] = silu(__uint_as_float(gr[8 * j + e])) * __uint_as_float(ur[8 * j + e]);
+          p.x = pack_bf16x2(h[0], h[1]);
+          p.y = pack_bf16x2(h[2], h[3]);
+          p.z = pack_bf16x2(h[4], h[5]);
+          p.w = pack_bf16x2(h[6], h[7]);
+          const int ch = cb / 8 + j;
+          *reinterpret_cast<uint4*>(rowp + ((ch ^ (lrow & 7)) << 4)) = p;
+        }
+        if (tr && i < 256) tr[1024 + i * 4 + 1] = globaltimer();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&h_full[b]);
+        if (tr && i < 256) tr[i * 4 + 3] = globaltimer();
+      }
+      // partial T_d (this slice of the intermediate) -> fp32 reductions
+      mbar_wait(td_done, 0);
+      tc_fence_after();
+      const int m = tile * 128 + lrow;
+      const int half = a.rd / 2;  // rd is a multiple of 64
+#pragma unroll 1
+      for (int c = ((warp - 2) >> 2) * half; c < ((warp - 2) >> 2) * half + half; c += 16) {
+        float v[16];
+        tmem_ld16(tTD + lane_base + c, v);
+        if (m >= a.M) continue;
+        float* o = a.td + (int64_t)m * a.ld_td + c;
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+size_t mlp_mid_smem(const MlpArgs& a) { return mlp_layout(a).total; }
+
+int launch_mlp_mid(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMap& au, const CUtensorMap& bd,
+                   const MlpArgs& a, int slices, cudaStream_t st) {
+  const MlpLayout L = mlp_layout(a);
+  if (a.rg % 64 || a.ru % 64 || a.rd % 64 || a.rg > 128 || a.ru > 128 || a.rd > 256 || a.inter % CH ||
+      L.total > 227 * 1024)
+    return (int)cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(mlp_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.M + 127) / 128, slices, 1);
+  cfg.blockDim = dim3(MLP_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, mlp_mid_kernel, t, ag, au, bd, a);
+  count_launch();
+  return (int)e;
+}
+
+}  // namespace tnl

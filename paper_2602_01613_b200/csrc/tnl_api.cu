@@ -36,6 +36,7 @@
 #include "common.cuh"
 #include "decode.cuh"
 #include "generic.cuh"
+#include "mlp.cuh"
 #include "tc_gemm.cuh"
 
 namespace tnl {
@@ -111,6 +112,23 @@ __global__ void copy_2d_any(const void* src, int s_dt, int64_t s_r, int64_t s_c,
   }
 }
 static int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+// unfused MLP fallback: g <- silu(g) * u (bf16, 8 elements per thread)
+__global__ void silu_mul_bf16(__nv_bfloat16* g, const __nv_bfloat16* u, int64_t n8) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
+    uint4 gv = reinterpret_cast<uint4*>(g)[e];
+    const uint4 uv = reinterpret_cast<const uint4*>(u)[e];
+    __nv_bfloat162* gh = reinterpret_cast<__nv_bfloat162*>(&gv);
+    const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&uv);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 a = __bfloat1622float2(gh[i]), b = __bfloat1622float2(uh[i]);
+      a.x = a.x / (1.f + __expf(-a.x)) * b.x;
+      a.y = a.y / (1.f + __expf(-a.y)) * b.y;
+      gh[i] = __floats2bfloat162_rn(a.x, a.y);
+    }
+    reinterpret_cast<uint4*>(g)[e] = gv;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Plan
@@ -1409,6 +1427,46 @@ static size_t stack_ws_bytes(const tnl_plan* const* plans, int32_t n, int64_t m)
 
 }  // namespace tnl (stack helpers)
 namespace tnl {
+
+// ---------------------------------------------------------------------------
+// Fused TN MLP block: y = down(silu(gate(x)) * up(x))  (mlp.cu)
+// ---------------------------------------------------------------------------
+}  // namespace tnl
+
+struct tnl_mlp {
+  tnl_plan* g = nullptr;
+  tnl_plan* u = nullptr;
+  tnl_plan* d = nullptr;
+  bool fused = false;
+  int64_t hidden = 0, inter = 0, rg = 0, ru = 0, rd = 0;
+  __nv_bfloat16* bgu = nullptr;  // [B_g (rg rows) ; B_u (ru rows)] x hidden
+};
+
+namespace tnl {
+
+static void mlp_ws_layout(const tnl_mlp* B, int64_t M, size_t off[4], size_t* total) {
+  size_t bytes = 0;
+  auto take = [&](size_t n) {
+    size_t o = bytes;
+    bytes += round_up((int64_t)n, 256);
+    return o;
+  };
+  if (B->fused && M > kSwapMaxM) {
+    off[0] = take(sizeof(float) * M * (B->rg + B->ru));  // T_gu fp32 (split-K)
+    off[1] = take(2 * M * (B->rg + B->ru));              // T_gu bf16
+    off[2] = take(sizeof(float) * M * B->rd);            // T_d fp32 (slice reductions)
+    off[3] = take(2 * M * B->rd);                        // T_d bf16
+  } else {
+    size_t a, b, c, mx = 0;
+    for (const tnl_plan* P : {B->g, B->u, B->d}) mx = std::max(mx, ws_layout(P, M, &a, &b, &c));
+    off[0] = take(mx);                  // per-layer workspace (zero-filled: decode accumulators)
+    off[1] = take(2 * M * B->inter);    // g / h
+    off[2] = take(2 * M * B->inter);    // u
+    off[3] = 0;
+  }
+  *total = bytes;
+}
+
 }  // namespace tnl
 
 using namespace tnl;
@@ -1546,6 +1604,152 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
       return fail(TNL_ERR_CUDA, "stack phase B launch: %s", cudaGetErrorString((cudaError_t)err));
   }
   return TNL_OK;
+}
+
+
+tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_plan* down, int32_t flags,
+                          tnl_mlp** out) {
+  if (!gate || !up || !down || !out) return fail(TNL_ERR_ARG, "null argument");
+  *out = nullptr;
+  for (const tnl_plan* P : {gate, up, down})
+    if (P->compute_dtype != TNL_BF16 || P->row_begin != 0 || P->row_end != P->rows)
+      return fail(TNL_ERR_UNSUPPORTED, "MLP block needs full-row bf16 plans");
+  if (gate->rows != up->rows || gate->cols != up->cols || down->cols != gate->rows || down->rows != gate->cols)
+    return fail(TNL_ERR_SHAPE, "MLP block shapes: gate %lldx%lld, up %lldx%lld, down %lldx%lld",
+                (long long)gate->rows, (long long)gate->cols, (long long)up->rows, (long long)up->cols,
+                (long long)down->rows, (long long)down->cols);
+  std::unique_ptr<tnl_mlp> B(new tnl_mlp());
+  B->g = const_cast<tnl_plan*>(gate);
+  B->u = const_cast<tnl_plan*>(up);
+  B->d = const_cast<tnl_plan*>(down);
+  B->hidden = gate->cols;
+  B->inter = gate->rows;
+  auto cut = [](const tnl_plan* P) { return P->family != TNL_FAMILY_DENSE && P->bin && P->aout; };
+  B->rg = round_up(gate->r_pad, 64);
+  B->ru = round_up(up->r_pad, 64);
+  B->rd = round_up(down->r_pad, 64);
+  B->fused = !(flags & 1) && cut(gate) && cut(up) && cut(down) && B->rg <= 128 && B->ru <= 128 && B->rd <= 256 &&
+             B->inter % 64 == 0 && B->hidden % 8 == 0;
+  if (B->fused) {
+    MlpArgs a;
+    memset(&a, 0, sizeof a);
+    a.rg = (int32_t)B->rg;
+    a.ru = (int32_t)B->ru;
+    a.rd = (int32_t)B->rd;
+    if (mlp_mid_smem(a) > 227 * 1024) B->fused = false;
+  }
+  if (B->fused) {
+    const size_t bytes = 2 * (B->rg + B->ru) * B->hidden;
+    CUDA_TRY(cudaMalloc(&B->bgu, bytes));
+    CUDA_TRY(cudaMemset(B->bgu, 0, bytes));
+    CUDA_TRY(cudaMemcpy(B->bgu, gate->bin, 2 * gate->r_pad * B->hidden, cudaMemcpyDeviceToDevice));
+    CUDA_TRY(cudaMemcpy(B->bgu + B->rg * B->hidden, up->bin, 2 * up->r_pad * B->hidden, cudaMemcpyDeviceToDevice));
+  }
+  *out = B.release();
+  return TNL_OK;
+}
+
+tnl_status tnl_mlp_destroy(tnl_mlp* B) {
+  if (!B) return TNL_OK;
+  cudaFree(B->bgu);
+  delete B;
+  return TNL_OK;
+}
+
+int32_t tnl_mlp_is_fused(const tnl_mlp* B) { return B && B->fused ? 1 : 0; }
+
+tnl_status tnl_mlp_workspace_size(const tnl_mlp* B, int64_t m, size_t* bytes) {
+  if (!B || !bytes) return fail(TNL_ERR_ARG, "null argument");
+  size_t off[4];
+  mlp_ws_layout(B, std::max<int64_t>(m, 1), off, bytes);
+  return TNL_OK;
+}
+
+tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
+                           void* ws, size_t ws_bytes, void* stream) {
+  tnl_mlp* B = const_cast<tnl_mlp*>(Bc);
+  if (!B || !x || !y) return fail(TNL_ERR_ARG, "null argument");
+  if (m == 0) return TNL_OK;
+  size_t off[4], need;
+  mlp_ws_layout(B, m, off, &need);
+  if (ws_bytes < need) return fail(TNL_ERR_ARG, "MLP workspace %zu < required %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  const bool prefill = m > kSwapMaxM;
+  if (B->fused && prefill && ((reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8 ||
+                              (reinterpret_cast<uintptr_t>(x) & 15) || ldx % 8))
+    return fail(TNL_ERR_SHAPE, "fused MLP needs 16-byte aligned x/y with row pitches % 8 == 0");
+  if (!B->fused || !prefill) {
+    // unfused: three layer forwards + a SiLU*mul kernel
+    void* lws = w + off[0];
+    size_t a_, b_, c_, lbytes = 0;
+    for (const tnl_plan* P : {B->g, B->u, B->d}) lbytes = std::max(lbytes, ws_layout(P, m, &a_, &b_, &c_));
+    __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(w + off[1]);
+    __nv_bfloat16* u = reinterpret_cast<__nv_bfloat16*>(w + off[2]);
+    tnl_status s = tnl_forward(B->g, x, m, ldx, g, B->inter, lws, lbytes, stream);
+    if (s) return s;
+    if ((s = tnl_forward(B->u, x, m, ldx, u, B->inter, lws, lbytes, stream))) return s;
+    silu_mul_bf16<<<grid_for(m * B->inter / 8), 256, 0, st>>>(g, u, m * B->inter / 8);
+    count_launch();
+    return tnl_forward(B->d, g, m, B->inter, y, ldy, lws, lbytes, stream);
+  }
+  const int64_t rgu = B->rg + B->ru;
+  float* tgu32 = reinterpret_cast<float*>(w + off[0]);
+  __nv_bfloat16* tgu = reinterpret_cast<__nv_bfloat16*>(w + off[1]);
+  float* td32 = reinterpret_cast<float*>(w + off[2]);
+  __nv_bfloat16* td = reinterpret_cast<__nv_bfloat16*>(w + off[3]);
+  tnl_status s;
+  // 1. T_gu = x . [B_g; B_u]^T
+  const int64_t tiles1 = ((m + 127) / 128) * ((rgu + 255) / 256);
+  const int64_t kb = (B->hidden + 63) / 64;
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb / 8));
+  if (splits > 1) {
+    if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu32, rgu, true, splits, st))) return s;
+    f32_to_bf16_2d<<<grid_for(m * rgu), 256, 0, st>>>(tgu32, rgu, tgu, rgu, m, rgu);
+    count_launch();
+  } else if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st))) {
+    return s;
+  }
+  // 2. T_d = (silu(T_g A_g^T) * (T_u A_u^T)) B_d^T, h on chip
+  CUtensorMap tt, tag, tau, tbd;
+  int err;
+  if ((err = get_tmap(B->g, &tt, tgu, rgu, m, rgu, 128)) ||
+      (err = get_tmap2(B->g, &tag, B->g->aout, false, B->g->r_pad, B->inter, B->g->r_pad, 64, 64, 128)) ||
+      (err = get_tmap2(B->u, &tau, B->u->aout, false, B->u->r_pad, B->inter, B->u->r_pad, 64, 64, 128)) ||
+      (err = get_tmap2(B->d, &tbd, B->d->bin, false, B->inter, B->d->r_pad, B->inter, 64, (int)B->rd, 128)))
+    return fail(TNL_ERR_CUDA, "tensor map (MLP) failed: %d", err);
+  MlpArgs a;
+  memset(&a, 0, sizeof a);
+  a.M = (int32_t)m;
+  a.inter = (int32_t)B->inter;
+  a.rg = (int32_t)B->rg;
+  a.ru = (int32_t)B->ru;
+  a.rd = (int32_t)B->rd;
+  const int64_t tiles_m = (m + 127) / 128, nchunks = B->inter / 64;
+  // Slice the intermediate so the grid's waves are nearly full: one CTA per SM (smem-bound),
+  // each CTA pays ~4 chunk-times of fixed cost (T tile load, pipeline fill, T_d flush).
+  int slices = 1;
+  {
+    int64_t best = INT64_MAX;
+    for (int64_t s = 1; s <= nchunks; ++s) {
+      const int64_t waves = (tiles_m * s + 147) / 148;
+      const int64_t cost = waves * ((nchunks + s - 1) / s + 4);
+      if (cost < best) best = cost, slices = (int)s;
+    }
+    if (const char* e = getenv("TNL_MLP_SLICES")) slices = std::max(1, atoi(e));
+  }
+  a.chunks_per_slice = (int32_t)((nchunks + slices - 1) / slices);
+  slices = (int)((nchunks + a.chunks_per_slice - 1) / a.chunks_per_slice);
+  a.td = td32;
+  a.ld_td = B->rd;
+  a.trace = B->g->trace;
+  if (cudaMemsetAsync(td32, 0, sizeof(float) * m * B->rd, st) != cudaSuccess) return fail(TNL_ERR_CUDA, "memset");
+  if ((err = launch_mlp_mid(tt, tag, tau, tbd, a, slices, st)))
+    return fail(TNL_ERR_CUDA, "MLP middle kernel launch: %s", cudaGetErrorString((cudaError_t)err));
+  f32_to_bf16_2d<<<grid_for(m * B->rd), 256, 0, st>>>(td32, B->rd, td, B->rd, m, B->rd);
+  count_launch();
+  // 3. y = T_d . A_d^T
+  return tc_step_p(B->d, td, B->rd, B->d->aout, B->d->r_pad, m, B->hidden, B->d->r_pad, y, ldy, false, 1, st);
 }
 
 tnl_status tnl_plan_set_trace(tnl_plan* plan, void* device_buffer) {

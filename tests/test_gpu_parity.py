@@ -318,3 +318,44 @@ def test_decode_gemv_variant(spec, m):
     fam, ms, rm, rk = spec
     L = O.synthetic_layer(fam, ms, rm, rk, seed=49_000 + m)
     check_bf16(L, m, seed=49_500 + m, flags=tnl.PLAN_GEMV)
+
+
+def _mlp_ref(Lg, Lu, Ld, x):
+    g = O.forward_torch_orient(Lg, x)
+    u = O.forward_torch_orient(Lu, x)
+    h = O.round_bf16(g / (1.0 + np.exp(-g)) * u)
+    return O.forward_torch_orient(Ld, h)
+
+
+@pytest.mark.parametrize("m", [300, 5, 2048])
+@pytest.mark.parametrize("fused", [True, False])
+def test_mlp_block(m, fused):
+    """y = down(silu(gate(x)) * up(x)): fused (h on chip) and unfused vs the oracle."""
+    from paper_2602_01613_b200.mlp import TNMLP
+
+    Lg = O.synthetic_layer("tt", (32, 32, 16, 32), 2, (16, 16, 16), seed=50_001)
+    Lu = O.synthetic_layer("tr", (32, 32, 16, 32), 2, (2, 8, 8, 8), seed=50_002)
+    Ld = O.synthetic_layer("tucker", (512, 1024), 1, (32, 32), seed=50_003)
+    (g, Lgr), (u, Lur), (d, Ldr) = (to_layer(L, round_bf16=True) for L in (Lg, Lu, Ld))
+    mlp = TNMLP(g, u, d, fused=fused)
+    assert mlp.fused == fused
+    x = O.round_bf16(O.synthetic_x(m, 512, seed=50_004))
+    y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
+    torch.cuda.synchronize()
+    ref = _mlp_ref(Lgr, Lur, Ldr, x)
+    assert rel(ref, y.float().cpu().numpy()) <= 2 * BF16_TOL
+
+
+def test_mlp_block_cfg3():
+    """cfg3: Qwen3-32B MLP (5120 -> 25600 -> 5120), TT r64 gate/up/down, fused."""
+    from paper_2602_01613_b200.mlp import TNMLP
+
+    Ls = [O.synthetic_layer("tt", ms, 2, (64, 64, 64), seed=51_000 + i) for i, ms in
+          enumerate([(160, 160, 64, 80), (160, 160, 64, 80), (64, 80, 160, 160)])]
+    pairs = [to_layer(L, round_bf16=True) for L in Ls]
+    mlp = TNMLP(*[p[0] for p in pairs])
+    assert mlp.fused
+    x = O.round_bf16(O.synthetic_x(256, 5120, seed=51_009))
+    y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
+    ref = _mlp_ref(*[p[1] for p in pairs], x)
+    assert rel(ref, y.float().cpu().numpy()) <= 2 * BF16_TOL
