@@ -268,9 +268,282 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// TS variant: the T tile and h live in TMEM, so the tensor core reads only the streamed
+// weight chunks from shared memory (the SS kernel above re-reads the 128-token T tile from
+// smem for every chunk and round-trips h through smem: ~3x the smem traffic per chunk).
+//   TMEM columns: [b*128, b*128+128) G|U accumulator pair b (NB of them; after the
+//   epilogue, h_b is packed bf16 in columns b*128 + {0..15, 32..47}), then T (32 columns per
+//   64-wide k-block, packed bf16 as the MMA's A operand), then T_d (rd columns).
+struct MlpTsLayout {
+  int kg, ku;
+  uint32_t stage, ag_off, au_off, bd_off;
+  int stages, nb, lag;
+  uint32_t t_col, td_col;
+  size_t t_bytes, total;
+};
+
+__host__ __device__ inline MlpTsLayout mlp_ts_layout(const MlpArgs& a) {
+  MlpTsLayout L;
+  L.kg = a.rg / 64;
+  L.ku = a.ru / 64;
+  L.ag_off = 0;
+  L.au_off = L.kg * WBLK;
+  L.bd_off = L.au_off + L.ku * WBLK;
+  L.stage = (L.bd_off + (uint32_t)a.rd * 128 + 1023) / 1024 * 1024;
+  L.t_bytes = (size_t)(L.kg + L.ku) * TBLK;
+  const int tcols = (L.kg + L.ku) * 32;
+  L.nb = (512 - tcols - a.rd) / 128;
+  if (L.nb > 3) L.nb = 3;
+  L.t_col = L.nb * 128;
+  L.td_col = L.t_col + tcols;
+  const size_t fixed = 1024 + L.t_bytes + 256;
+  L.stages = 6;
+  while (L.stages > 2 && fixed + (size_t)L.stages * L.stage > 227 * 1024) --L.stages;
+  L.lag = L.nb - 1 < L.stages - 2 ? L.nb - 1 : L.stages - 2;
+  if (L.lag < 1) L.lag = 1;
+  L.total = fixed + (size_t)L.stages * L.stage;
+  return L;
+}
+
+// circular-buffer position: slot index and the mbarrier phase parity of its current use
+struct Ring {
+  int idx = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++idx == n) {
+      idx = 0;
+      ph ^= 1;
+    }
+  }
+  __device__ __forceinline__ void next2(int n) {  // two slots ahead (n >= 2)
+    idx += 2;
+    if (idx >= n) {
+      idx -= n;
+      ph ^= 1;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(MLP_THREADS, 1)
+    mlp_mid_ts_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmAg,
+                      const __grid_constant__ CUtensorMap tmAu, const __grid_constant__ CUtensorMap tmBd,
+                      const MlpArgs a) {
+  const MlpTsLayout L = mlp_ts_layout(a);
+  const int S = L.stages, NB = L.nb;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sT = smem;             // T tile staging (TMA -> smem -> TMEM)
+  uint8_t* sR = sT + L.t_bytes;   // ring stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sR + (size_t)S * L.stage);
+  uint64_t* full = bars;           // [8]
+  uint64_t* empty = bars + 8;      // [8]
+  uint64_t* tfull = bars + 16;
+  uint64_t* t_tmem = bars + 17;
+  uint64_t* gu_full = bars + 18;   // [3]
+  uint64_t* gu_empty = bars + 21;  // [3]
+  uint64_t* h_full = bars + 24;    // [3]
+  uint64_t* td_done = bars + 27;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+
+  const int tile = blockIdx.x;
+  const int total_ch = a.inter / CH;
+  const int c0 = blockIdx.y * a.chunks_per_slice;
+  const int nch = min(total_ch, c0 + a.chunks_per_slice) - c0;
+  const uint32_t warp = warp_id();
+  const uint32_t stage_tx = (uint32_t)((L.kg + L.ku) * WBLK + a.rd * 128);
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmT);
+    tma_prefetch_desc(&tmAg);
+    tma_prefetch_desc(&tmAu);
+    tma_prefetch_desc(&tmBd);
+    for (int s = 0; s < 8; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(t_tmem, 8);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&gu_full[b], 1);
+      mbar_init(&gu_empty[b], 1);
+      mbar_init(&h_full[b], 4);
+    }
+    mbar_init(td_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tT = tmem + L.t_col, tTD = tmem + L.td_col;
+  pdl_launch_dependents();
+
+  if (nch > 0) {
+    if (warp == 0) {
+      if (elect_one()) {
+        Ring r;
+        auto load_stage = [&](int i) {
+          const int s = r.idx;
+          uint8_t* st = sR + (size_t)s * L.stage;
+          const int col = (c0 + i) * CH;
+          mbar_arrive_expect_tx(&full[s], stage_tx);
+          for (int k = 0; k < L.kg; ++k) tma_load_2d(st + L.ag_off + k * WBLK, &tmAg, &full[s], k * 64, col);
+          for (int k = 0; k < L.ku; ++k) tma_load_2d(st + L.au_off + k * WBLK, &tmAu, &full[s], k * 64, col);
+          tma_load_2d(st + L.bd_off, &tmBd, &full[s], col, 0);
+          r.next(S);
+        };
+        const int npre = min(nch, S);
+        for (int i = 0; i < npre; ++i) load_stage(i);  // weights: before the dependency wait
+        pdl_wait();
+        mbar_arrive_expect_tx(tfull, (uint32_t)((L.kg + L.ku) * TBLK));
+        for (int k = 0; k < L.kg + L.ku; ++k) tma_load_2d(sT + k * TBLK, &tmT, tfull, k * 64, tile * 128);
+        for (int i = npre; i < nch; ++i) {
+          mbar_wait(&empty[r.idx], r.ph ^ 1);
+          load_stage(i);
+        }
+      }
+    } else if (warp == 1) {
+      if (elect_one()) {
+        const uint32_t idesc_gu = idesc_bf16_f32(128, CH);
+        const uint32_t idesc_d = idesc_bf16_f32(128, a.rd);
+        mbar_wait(t_tmem, 0);
+        tc_fence_after();
+        Ring rf, rb, js, jb;  // G/U side: stage, pair; T_d side: stage, pair
+        auto mma_d = [&](int j) {  // T_d += h_j . B_d[:, chunk j]^T; frees stage j and pair j
+          mbar_wait(&h_full[jb.idx], jb.ph);
+          tc_fence_after();
+          const uint32_t th = tmem + jb.idx * 128;
+          const uint64_t bd = smem_desc_sw128(smem_u32(sR + (size_t)js.idx * L.stage + L.bd_off));
+          if (!(a.dbg & 4))
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_bf16_ts(tTD, th + (k >> 1) * 32 + (k & 1) * 8, bd + 2 * k, idesc_d, (j > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&gu_empty[jb.idx]);
+          mma_commit(&empty[js.idx]);
+          js.next(S);
+          jb.next(NB);
+        };
+        unsigned long long* tr = (a.trace && blockIdx.x == 0 && blockIdx.y == 0) ? a.trace : nullptr;
+        for (int i = 0; i < nch; ++i) {
+          const int s = rf.idx, b = rb.idx;
+          mbar_wait(&full[s], rf.ph);
+          if (tr && i < 256) tr[i * 4 + 0] = globaltimer();
+          if (i >= NB) mbar_wait(&gu_empty[b], rb.ph ^ 1);
+          rf.next(S);
+          rb.next(NB);
+          tc_fence_after();
+          uint8_t* st = sR + (size_t)s * L.stage;
+          const uint32_t tG = tmem + b * 128, tU = tG + 64;
+          if (!(a.dbg & 2))
+          for (int k = 0; k < L.kg; ++k) {
+            const uint64_t bd = smem_desc_sw128(smem_u32(st + L.ag_off + k * WBLK));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mma_bf16_ts(tG, tT + k * 32 + q * 8, bd + 2 * q, idesc_gu, (k | q) != 0);
+          }
+          if (!(a.dbg & 2))
+          for (int k = 0; k < L.ku; ++k) {
+            const uint64_t bd = smem_desc_sw128(smem_u32(st + L.au_off + k * WBLK));
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              mma_bf16_ts(tU, tT + (L.kg + k) * 32 + q * 8, bd + 2 * q, idesc_gu, (k | q) != 0);
+          }
+          mma_commit(&gu_full[b]);
+          if (tr && i < 256) tr[i * 4 + 1] = globaltimer();
+          if (i >= L.lag) mma_d(i - L.lag);
+        }
+        for (int j = nch - L.lag < 0 ? 0 : nch - L.lag; j < nch; ++j) mma_d(j);
+        mma_commit(td_done);
+      }
+      __syncwarp();
+    } else {
+      const uint32_t q = warp & 3, hh = (warp - 2) >> 2;
+      const int lrow = q * 32 + lane_id();
+      const uint32_t lane_base = (q * 32) << 16;
+      // T tile: smem (SW128, k-blocks of 64) -> TMEM (packed bf16 pairs, 32 columns per k-block)
+      mbar_wait(tfull, 0);
+      for (int kb = hh; kb < L.kg + L.ku; kb += 2) {
+        const uint8_t* rowp = sT + kb * TBLK + (lrow >> 3) * 1024 + (lrow & 7) * 128;
+        uint32_t r[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((c ^ (lrow & 7)) << 4));
+          r[4 * c] = v.x;
+          r[4 * c + 1] = v.y;
+          r[4 * c + 2] = v.z;
+          r[4 * c + 3] = v.w;
+        }
+        tmem_st32(tT + lane_base + kb * 32, r);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(t_tmem);
+      unsigned long long* tr = (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (warp == 2 || warp == 6) && lane_id() == 0) ? a.trace : nullptr;
+      // the two epilogue warps of a lane quarter take alternate chunks (all 64 columns each),
+      // so one warp's SFU work overlaps the other's TMEM round trips and barrier waits
+      Ring eb;
+      eb.idx = hh;
+      for (int i = hh; i < nch; i += 2) {
+        const int b = eb.idx;
+        mbar_wait(&gu_full[b], eb.ph);
+        eb.next2(NB);
+        tc_fence_after();
+        if (tr && i < 256) tr[i * 4 + 2] = globaltimer();
+        const uint32_t tG = tmem + b * 128 + lane_base, tU = tG + 64;
+        uint32_t gr[64], ur[64];
+        tmem_ld32_nowait(tG, gr);
+        tmem_ld32_nowait(tU, ur);
+        tmem_ld32_nowait(tG + 32, gr + 32);
+        tmem_ld32_nowait(tU + 32, ur + 32);
+        tmem_wait_ld();
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t hp[16];
+          if (a.dbg & 1) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) hp[e] = gr[32 * hf + 2 * e] ^ ur[32 * hf + 2 * e + 1];
+          } else
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            hp[e] = pack_bf16x2(silu(__uint_as_float(gr[32 * hf + 2 * e])) * __uint_as_float(ur[32 * hf + 2 * e]),
+                                silu(__uint_as_float(gr[32 * hf + 2 * e + 1])) * __uint_as_float(ur[32 * hf + 2 * e + 1]));
+          tmem_st16(tG + hf * 32, hp);  // h over already-read G columns
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&h_full[b]);
+        if (tr && i < 256) tr[i * 4 + 3] = globaltimer();
+      }
+      mbar_wait(td_done, 0);
+      tc_fence_after();
+      const int m = tile * 128 + lrow;
+      const int half = a.rd / 2;
+#pragma unroll 1
+      for (int c = hh * half; c < hh * half + half; c += 16) {
+        float v[16];
+        tmem_ld16(tTD + lane_base + c, v);
+        if (m >= a.M) continue;
+        float* o = a.td + (int64_t)m * a.ld_td + c;
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
 }  // namespace
 
-size_t mlp_mid_smem(const MlpArgs& a) { return mlp_layout(a).total; }
+size_t mlp_mid_smem(const MlpArgs& a) {
+  const MlpTsLayout Lt = mlp_ts_layout(a);
+  return Lt.nb >= 2 ? Lt.total : mlp_layout(a).total;
+}
 
 int launch_mlp_mid(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMap& au, const CUtensorMap& bd,
                    const MlpArgs& a, int slices, cudaStream_t st) {
@@ -281,20 +554,26 @@ int launch_mlp_mid(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMa
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(mlp_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mlp_mid_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
+  const MlpTsLayout Lt = mlp_ts_layout(a);
+  static const int ts_env = getenv("TNL_MLP_SS") ? 0 : 1;
+  const bool ts = ts_env && Lt.nb >= 2 && Lt.total <= 227 * 1024;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.M + 127) / 128, slices, 1);
   cfg.blockDim = dim3(MLP_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = L.total;
+  cfg.dynamicSmemBytes = ts ? Lt.total : L.total;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, mlp_mid_kernel, t, ag, au, bd, a);
+  cudaError_t e = ts ? cudaLaunchKernelEx(&cfg, mlp_mid_ts_kernel, t, ag, au, bd, a)
+                     : cudaLaunchKernelEx(&cfg, mlp_mid_kernel, t, ag, au, bd, a);
   count_launch();
   return (int)e;
 }

@@ -88,6 +88,15 @@ __global__ void f32_to_bf16_2d(const float* __restrict__ src, int64_t lds, __nv_
     dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
   }
 }
+// contiguous fp32 -> bf16, 8 elements per thread (n % 8 == 0, 16-byte aligned buffers)
+__global__ void f32_to_bf16_v8(const float4* __restrict__ src, uint4* __restrict__ dst, int64_t n8) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = src[2 * e], b = src[2 * e + 1];
+    __nv_bfloat162 o[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
+                           __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
+    dst[e] = *reinterpret_cast<uint4*>(o);
+  }
+}
 __global__ void identity_f32(float* dst, int64_t rows, int64_t cols, int64_t offset) {
   // dst[r][c] = (c == r + offset)
   int64_t n = rows * cols;
@@ -112,6 +121,15 @@ __global__ void copy_2d_any(const void* src, int s_dt, int64_t s_r, int64_t s_c,
   }
 }
 static int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+// dense [rows][cols] fp32 -> bf16 (both contiguous)
+static void to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st) {
+  if (n % 8 == 0 && !(reinterpret_cast<uintptr_t>(src) & 15) && !(reinterpret_cast<uintptr_t>(dst) & 15))
+    f32_to_bf16_v8<<<grid_for(n / 8), 256, 0, st>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<uint4*>(dst),
+                                                      n / 8);
+  else
+    f32_to_bf16_2d<<<grid_for(n), 256, 0, st>>>(src, n, dst, n, 1, n);
+  count_launch();
+}
 // unfused MLP fallback: g <- silu(g) * u (bf16, 8 elements per thread)
 __global__ void silu_mul_bf16(__nv_bfloat16* g, const __nv_bfloat16* u, int64_t n8) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
@@ -1240,8 +1258,8 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
 // out_f32: fp32 split-K reductions into `out` (zeroed here); else bf16 via TMA store.
 static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void* W, int64_t ldw,
                             int64_t M, int64_t N, int64_t K, void* out, int64_t ldo, bool out_f32,
-                            int splits, cudaStream_t st) {
-  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+                            int splits, cudaStream_t st, int bn_force = 0) {
+  const int bn = bn_force ? bn_force : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
   CUtensorMap ta, tb, tc;
   int err;
   if ((err = get_tmap(P, &ta, X, K, M, ldx, 128)) || (err = get_tmap(P, &tb, W, K, N, ldw, bn)))
@@ -1303,8 +1321,7 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
         return fail(TNL_ERR_CUDA, "memset failed");
       s = chain_in(P, x, ldx, M, tf, P->r_pad, 1, true, splits, st);
       if (s) return s;
-      f32_to_bf16_2d<<<grid_for(M * P->r_pad), 256, 0, st>>>(tf, P->r_pad, t0, P->r_pad, M, P->r_pad);
-      count_launch();
+      to_bf16(tf, t0, M * P->r_pad, st);
     } else {
       s = chain_in(P, x, ldx, M, t0, P->r_pad, 1, false, 1, st);
       if (s) return s;
@@ -1324,8 +1341,7 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     if (splits > 1) {
       s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, tf, k1, true, splits, st);
       if (s) return s;
-      f32_to_bf16_2d<<<grid_for(M * k1), 256, 0, st>>>(tf, k1, t0, k1, M, k1);
-      count_launch();
+      to_bf16(tf, t0, M * k1, st);
     } else {
       s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, 1, st);
       if (s) return s;
@@ -1349,8 +1365,7 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
         return fail(TNL_ERR_CUDA, "memset failed");
       s = tc_step(P, x, ldx, win, P->cols, M, k1, P->cols, tf, k1, true, true, splits, st);
       if (s) return s;
-      f32_to_bf16_2d<<<grid_for(M * k1), 256, 0, st>>>(tf, k1, t0, k1, M, k1);
-      count_launch();
+      to_bf16(tf, t0, M * k1, st);
     } else {
       s = tc_step(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, true, 1, st);
       if (s) return s;
@@ -1703,10 +1718,12 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   const int64_t tiles1 = ((m + 127) / 128) * ((rgu + 255) / 256);
   const int64_t kb = (B->hidden + 63) / 64;
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb / 8));
-  if (splits > 1) {
+  if (((m + 127) / 128) * ((rgu + 63) / 64) >= 96) {
+    // enough 64-wide output tiles to fill the SMs: no split-K, bf16 straight from the epilogue
+    if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st, 64))) return s;
+  } else if (splits > 1) {
     if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu32, rgu, true, splits, st))) return s;
-    f32_to_bf16_2d<<<grid_for(m * rgu), 256, 0, st>>>(tgu32, rgu, tgu, rgu, m, rgu);
-    count_launch();
+    to_bf16(tgu32, tgu, m * rgu, st);
   } else if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st))) {
     return s;
   }
@@ -1743,11 +1760,11 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   a.td = td32;
   a.ld_td = B->rd;
   a.trace = B->g->trace;
+  if (const char* e = getenv("TNL_MLP_DBG")) a.dbg = atoi(e);
   if (cudaMemsetAsync(td32, 0, sizeof(float) * m * B->rd, st) != cudaSuccess) return fail(TNL_ERR_CUDA, "memset");
   if ((err = launch_mlp_mid(tt, tag, tau, tbd, a, slices, st)))
     return fail(TNL_ERR_CUDA, "MLP middle kernel launch: %s", cudaGetErrorString((cudaError_t)err));
-  f32_to_bf16_2d<<<grid_for(m * B->rd), 256, 0, st>>>(td32, B->rd, td, B->rd, m, B->rd);
-  count_launch();
+  to_bf16(td32, td, m * B->rd, st);
   // 3. y = T_d . A_d^T
   return tc_step_p(B->d, td, B->rd, B->d->aout, B->d->r_pad, m, B->hidden, B->d->r_pad, y, ldy, false, 1, st);
 }
