@@ -73,6 +73,14 @@ __device__ __forceinline__ float silu(float g) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * g));
   return g * fmaf(0.5f, t, 0.5f);
 }
+// silu(g) * u = (g/2 * u) * (1 + tanh(g/2)): FMUL, MUFU, FMUL, FFMA per element
+__device__ __forceinline__ float silu_mul(float g, float u) {
+  const float a = 0.5f * g;
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(a));
+  const float b = a * u;
+  return fmaf(b, t, b);
+}
 
 // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (two warps per TMEM lane quarter, 32 columns each)
 constexpr int MLP_THREADS = 320, MLP_EPI = 256;
@@ -538,6 +546,285 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Pair variant (cta_group::2): the two CTAs of a 2x1 cluster (one TPC) run M=256 MMAs over
+// their two 128-token tiles. A tcgen05.mma costs >= ~44 cycles however small N is (measured:
+// tools/ubench/mma*.cu), so at N=64 one pair instruction doing both SMs' work halves the
+// tensor-pipe time per token; each CTA also streams only HALF of every weight chunk (A_g/A_u:
+// 32 of the 64 chunk rows, B_d: r_d/2 rows). T (the G/U A operand) lives in TMEM; h is written
+// by the epilogue into a 128B-swizzled smem ring (the D MMA's A operand), so a G/U TMEM pair is
+// released as soon as the epilogue has loaded it rather than after the D MMA — the MMA warp's
+// waits are then normally already satisfied. The leader (rank 0) issues every MMA and owns
+// full / t_tmem / gu_empty / h_full; MMA completions are multicast to both CTAs.
+constexpr uint32_t HBLK = 32 * 128;  // 32-row x 64-k bf16 half weight block (4 KB)
+// warp 0 TMA, warp 1 G/U MMA issuer, warps 2..9 epilogue, warp 10 D MMA issuer
+constexpr int MLP_PAIR_THREADS = 352;
+
+struct MlpPairLayout {
+  int kg, ku;
+  uint32_t stage, ag_off, au_off, bd_off, stage_tx;  // stage_tx: bytes per CTA
+  int stages, nb, nh, lag;
+  uint32_t t_col, td_col;
+  size_t t_bytes, h_off, total;
+};
+
+__host__ __device__ inline MlpPairLayout mlp_pair_layout(const MlpArgs& a) {
+  MlpPairLayout L;
+  L.kg = a.rg / 64;
+  L.ku = a.ru / 64;
+  L.ag_off = 0;
+  L.au_off = L.kg * HBLK;
+  L.bd_off = L.au_off + L.ku * HBLK;
+  L.stage_tx = L.bd_off + (uint32_t)(a.rd / 2) * 128;
+  L.stage = (L.stage_tx + 1023) / 1024 * 1024;
+  L.t_bytes = (size_t)(L.kg + L.ku) * TBLK;
+  const int tcols = (L.kg + L.ku) * 32;
+  L.nb = (512 - tcols - a.rd) / 128;
+  if (L.nb > 3) L.nb = 3;
+  L.nh = 3;
+  L.t_col = L.nb * 128;
+  L.td_col = L.t_col + tcols;
+  L.h_off = L.t_bytes;
+  const size_t fixed = 1024 + L.t_bytes + (size_t)L.nh * TBLK + 512;
+  L.stages = 12;
+  while (L.stages > 3 && fixed + (size_t)L.stages * L.stage > 227 * 1024) --L.stages;
+  L.lag = 2;
+  L.total = fixed + (size_t)L.stages * L.stage;
+  return L;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP_PAIR_THREADS, 1)
+    mlp_mid_pair_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmAg,
+                        const __grid_constant__ CUtensorMap tmAu, const __grid_constant__ CUtensorMap tmBd,
+                        const MlpArgs a) {
+  const MlpPairLayout L = mlp_pair_layout(a);
+  const int S = L.stages, NB = L.nb, NH = L.nh;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sT = smem;                 // own T tile (TMA -> smem -> TMEM)
+  uint8_t* sH = smem + L.h_off;       // NH x 16 KB h ring (own 128 rows)
+  uint8_t* sR = sH + NH * TBLK;       // weight ring (own halves)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sR + (size_t)S * L.stage);
+  uint64_t* full = bars;           // [12] leader: both CTAs' weight bytes
+  uint64_t* empty = bars + 12;     // [12] per CTA (multicast commit)
+  uint64_t* tfull = bars + 24;     //      per CTA (own T tile)
+  uint64_t* t_tmem = bars + 25;    //      leader: T copied into TMEM in both CTAs (16 warps)
+  uint64_t* gu_full = bars + 26;   // [3]  per CTA (multicast commit)
+  uint64_t* gu_empty = bars + 29;  // [3]  leader: G/U pair loaded by both CTAs' epilogues (8 warps)
+  uint64_t* h_full = bars + 32;    // [3]  leader: h chunk written in both CTAs (8 warps)
+  uint64_t* h_empty = bars + 35;   // [3]  per CTA (multicast commit of the D MMA)
+  uint64_t* td_done = bars + 38;   //      per CTA (multicast commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 39);
+
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int tile = blockIdx.x;
+  const int total_ch = a.inter / CH;
+  const int c0 = blockIdx.y * a.chunks_per_slice;
+  const int nch = min(total_ch, c0 + a.chunks_per_slice) - c0;
+  const uint32_t warp = warp_id();
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmT);
+    tma_prefetch_desc(&tmAg);
+    tma_prefetch_desc(&tmAu);
+    tma_prefetch_desc(&tmBd);
+    for (int s = 0; s < 12; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);  // G/U issuer + D issuer
+    }
+    mbar_init(tfull, 1);
+    mbar_init(t_tmem, 16);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&gu_full[b], 1);
+      mbar_init(&gu_empty[b], 8);
+      mbar_init(&h_full[b], 8);
+      mbar_init(&h_empty[b], 1);
+    }
+    mbar_init(td_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // peer barriers initialised before any remote arrive / multicast commit
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tT = tmem + L.t_col, tTD = tmem + L.td_col;
+  pdl_launch_dependents();
+
+  if (nch > 0) {
+    if (warp == 0) {
+      if (elect_one()) {
+        Ring r;
+        const int wrow = (int)rank * 32, drow = (int)rank * (a.rd / 2);
+        auto load_stage = [&](int i) {
+          const int s = r.idx;
+          uint8_t* st = sR + (size_t)s * L.stage;
+          const int col = (c0 + i) * CH;
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * L.stage_tx);
+          for (int k = 0; k < L.kg; ++k) tma_load_2d_pair(st + L.ag_off + k * HBLK, &tmAg, &full[s], k * 64, col + wrow);
+          for (int k = 0; k < L.ku; ++k) tma_load_2d_pair(st + L.au_off + k * HBLK, &tmAu, &full[s], k * 64, col + wrow);
+          tma_load_2d_pair(st + L.bd_off, &tmBd, &full[s], col, drow);
+          r.next(S);
+        };
+        const int npre = min(nch, S);
+        for (int i = 0; i < npre; ++i) load_stage(i);  // weights: before the dependency wait
+        pdl_wait();
+        mbar_arrive_expect_tx(tfull, (uint32_t)((L.kg + L.ku) * TBLK));
+        for (int k = 0; k < L.kg + L.ku; ++k) tma_load_2d(sT + k * TBLK, &tmT, tfull, k * 64, tile * 128);
+        for (int i = npre; i < nch; ++i) {
+          mbar_wait(&empty[r.idx], r.ph ^ 1);
+          load_stage(i);
+        }
+      }
+    } else if (warp == 1) {
+      // G/U issuer: G_i = T_g A_g[chunk i]^T, U_i = T_u A_u[chunk i]^T into TMEM pair i % NB
+      if (leader && elect_one()) {
+        const uint32_t idesc_gu = idesc_bf16_f32(256, CH);
+        unsigned long long* tr = (a.trace && blockIdx.x == 0 && blockIdx.y == 0) ? a.trace : nullptr;
+        mbar_wait(t_tmem, 0);
+        tc_fence_after();
+        Ring rf, rb;
+        for (int i = 0; i < nch; ++i) {
+          const int s = rf.idx, b = rb.idx;
+          mbar_wait(&full[s], rf.ph);
+          if (tr && i < 256) tr[i * 4 + 0] = globaltimer();
+          if (i >= NB) mbar_wait(&gu_empty[b], rb.ph ^ 1);
+          rf.next(S);
+          rb.next(NB);
+          tc_fence_after();
+          uint8_t* st = sR + (size_t)s * L.stage;
+          const uint32_t tG = tmem + b * 128, tU = tG + 64;
+          for (int k = 0; k < L.kg; ++k) {
+            const uint64_t bd = smem_desc_sw128(smem_u32(st + L.ag_off + k * HBLK));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mma_bf16_ts_pair(tG, tT + k * 32 + q * 8, bd + 2 * q, idesc_gu, (k | q) != 0);
+          }
+          for (int k = 0; k < L.ku; ++k) {
+            const uint64_t bd = smem_desc_sw128(smem_u32(st + L.au_off + k * HBLK));
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              mma_bf16_ts_pair(tU, tT + (L.kg + k) * 32 + q * 8, bd + 2 * q, idesc_gu, (k | q) != 0);
+          }
+          mma_commit_pair(&gu_full[b], 3);
+          mma_commit_pair(&empty[s], 3);
+          if (tr && i < 256) tr[i * 4 + 1] = globaltimer();
+        }
+      }
+      __syncwarp();
+    } else if (warp == MLP_PAIR_THREADS / 32 - 1) {
+      // D issuer: T_d += h_j B_d[:, chunk j]^T (A = h from the smem ring); its own warp (SMSP)
+      // so the two MMA chains interleave on the tensor pipe instead of serialising
+      if (leader && elect_one()) {
+        const uint32_t idesc_d = idesc_bf16_f32(256, a.rd);
+        Ring rf, rh;
+        for (int j = 0; j < nch; ++j) {
+          const int s = rf.idx, hb = rh.idx;
+          mbar_wait(&full[s], rf.ph);
+          mbar_wait(&h_full[hb], rh.ph);
+          rf.next(S);
+          rh.next(NH);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_sw128(smem_u32(sH + hb * TBLK));
+          const uint64_t bd = smem_desc_sw128(smem_u32(sR + (size_t)s * L.stage + L.bd_off));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_bf16_ss_pair(tTD, ad + 2 * k, bd + 2 * k, idesc_d, (j > 0 || k > 0) ? 1u : 0u);
+          mma_commit_pair(&h_empty[hb], 3);
+          mma_commit_pair(&empty[s], 3);
+        }
+        mma_commit_pair(td_done, 3);
+      }
+      __syncwarp();
+    } else {
+      const uint32_t q = warp & 3, hh = (warp - 2) >> 2;
+      const int lrow = q * 32 + lane_id();
+      const uint32_t lane_base = (q * 32) << 16;
+      // T tile: smem (SW128, k-blocks of 64) -> TMEM (packed bf16 pairs, 32 columns per k-block)
+      mbar_wait(tfull, 0);
+      for (int kb = hh; kb < L.kg + L.ku; kb += 2) {
+        const uint8_t* rowp = sT + kb * TBLK + (lrow >> 3) * 1024 + (lrow & 7) * 128;
+        uint32_t r[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((c ^ (lrow & 7)) << 4));
+          r[4 * c] = v.x;
+          r[4 * c + 1] = v.y;
+          r[4 * c + 2] = v.z;
+          r[4 * c + 3] = v.w;
+        }
+        tmem_st32(tT + lane_base + kb * 32, r);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive_remote(mapa_shared(t_tmem, 0));
+      unsigned long long* tr =
+          (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (warp == 2 || warp == 6) && lane_id() == 0) ? a.trace : nullptr;
+      // the two epilogue warps of a lane quarter take alternate chunks (all 64 columns each)
+      Ring eb, ehb;
+      eb.idx = hh;
+      ehb.idx = hh;
+      for (int i = hh; i < nch; i += 2) {
+        const int b = eb.idx, hb = ehb.idx;
+        const uint32_t hph = ehb.ph;
+        mbar_wait(&gu_full[b], eb.ph);
+        eb.next2(NB);
+        ehb.next2(NH);
+        tc_fence_after();
+        if (tr && i < 256) tr[i * 4 + 2] = globaltimer();
+        const uint32_t tG = tmem + b * 128 + lane_base, tU = tG + 64;
+        uint32_t gr[64], ur[64];
+        tmem_ld32_nowait(tG, gr);
+        tmem_ld32_nowait(tU, ur);
+        tmem_ld32_nowait(tG + 32, gr + 32);
+        tmem_ld32_nowait(tU + 32, ur + 32);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive_remote(mapa_shared(&gu_empty[b], 0));  // pair b reusable
+        if (i >= NH) mbar_wait(&h_empty[hb], hph ^ 1);
+        uint8_t* rowp = sH + hb * TBLK + (lrow >> 3) * 1024 + (lrow & 7) * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4 p;
+          p.x = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 0]), __uint_as_float(ur[8 * c + 0])),
+                            silu_mul(__uint_as_float(gr[8 * c + 1]), __uint_as_float(ur[8 * c + 1])));
+          p.y = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 2]), __uint_as_float(ur[8 * c + 2])),
+                            silu_mul(__uint_as_float(gr[8 * c + 3]), __uint_as_float(ur[8 * c + 3])));
+          p.z = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 4]), __uint_as_float(ur[8 * c + 4])),
+                            silu_mul(__uint_as_float(gr[8 * c + 5]), __uint_as_float(ur[8 * c + 5])));
+          p.w = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 6]), __uint_as_float(ur[8 * c + 6])),
+                            silu_mul(__uint_as_float(gr[8 * c + 7]), __uint_as_float(ur[8 * c + 7])));
+          *reinterpret_cast<uint4*>(rowp + ((c ^ (lrow & 7)) << 4)) = p;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive_remote(mapa_shared(&h_full[hb], 0));
+        if (tr && i < 256) tr[i * 4 + 3] = globaltimer();
+      }
+      mbar_wait(td_done, 0);
+      tc_fence_after();
+      const int m = tile * 128 + lrow;
+      const int half = a.rd / 2;
+#pragma unroll 1
+      for (int c = hh * half; c < hh * half + half; c += 16) {
+        float v[16];
+        tmem_ld16(tTD + lane_base + c, v);
+        if (m >= a.M) continue;
+        float* o = a.td + (int64_t)m * a.ld_td + c;
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_pair<512>(tmem);
+}
+
 }  // namespace
 
 size_t mlp_mid_smem(const MlpArgs& a) {
@@ -574,6 +861,43 @@ int launch_mlp_mid(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMa
   cfg.numAttrs = 1;
   cudaError_t e = ts ? cudaLaunchKernelEx(&cfg, mlp_mid_ts_kernel, t, ag, au, bd, a)
                      : cudaLaunchKernelEx(&cfg, mlp_mid_kernel, t, ag, au, bd, a);
+  count_launch();
+  return (int)e;
+}
+
+}  // namespace tnl
+
+namespace tnl {
+
+bool mlp_pair_ok(const MlpArgs& a) {
+  if (getenv("TNL_MLP_NOPAIR")) return false;
+  const MlpPairLayout L = mlp_pair_layout(a);
+  return L.nb >= 2 && L.total <= 227 * 1024 && a.rg % 64 == 0 && a.ru % 64 == 0 && a.rd % 64 == 0 &&
+         a.rg <= 128 && a.ru <= 128 && a.rd <= 256 && a.inter % CH == 0;
+}
+
+int launch_mlp_mid_pair(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMap& au, const CUtensorMap& bd,
+                        const MlpArgs& a, int slices, cudaStream_t st) {
+  if (!mlp_pair_ok(a)) return (int)cudaErrorInvalidValue;
+  const MlpPairLayout L = mlp_pair_layout(a);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(mlp_mid_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  const int tiles = (a.M + 127) / 128;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((tiles + 1) / 2 * 2, slices, 1);
+  cfg.blockDim = dim3(MLP_PAIR_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, mlp_mid_pair_kernel, t, ag, au, bd, a);
   count_launch();
   return (int)e;
 }

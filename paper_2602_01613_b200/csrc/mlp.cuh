@@ -25,5 +25,9 @@ struct MlpArgs {
 int launch_mlp_mid(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMap& au,
                    const CUtensorMap& bd, const MlpArgs& a, int slices, cudaStream_t st);
 size_t mlp_mid_smem(const MlpArgs& a);
+// CTA-pair variant (cta_group::2, 2x1 clusters over token tiles): ag/au box {64, 32}, bd box {64, rd/2}
+bool mlp_pair_ok(const MlpArgs& a);
+int launch_mlp_mid_pair(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMap& au,
+                        const CUtensorMap& bd, const MlpArgs& a, int slices, cudaStream_t st);
 
 }  // namespace tnl

@@ -1728,13 +1728,6 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
     return s;
   }
   // 2. T_d = (silu(T_g A_g^T) * (T_u A_u^T)) B_d^T, h on chip
-  CUtensorMap tt, tag, tau, tbd;
-  int err;
-  if ((err = get_tmap(B->g, &tt, tgu, rgu, m, rgu, 128)) ||
-      (err = get_tmap2(B->g, &tag, B->g->aout, false, B->g->r_pad, B->inter, B->g->r_pad, 64, 64, 128)) ||
-      (err = get_tmap2(B->u, &tau, B->u->aout, false, B->u->r_pad, B->inter, B->u->r_pad, 64, 64, 128)) ||
-      (err = get_tmap2(B->d, &tbd, B->d->bin, false, B->inter, B->d->r_pad, B->inter, 64, (int)B->rd, 128)))
-    return fail(TNL_ERR_CUDA, "tensor map (MLP) failed: %d", err);
   MlpArgs a;
   memset(&a, 0, sizeof a);
   a.M = (int32_t)m;
@@ -1742,7 +1735,18 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   a.rg = (int32_t)B->rg;
   a.ru = (int32_t)B->ru;
   a.rd = (int32_t)B->rd;
-  const int64_t tiles_m = (m + 127) / 128, nchunks = B->inter / 64;
+  const bool pair = mlp_pair_ok(a);  // CTA pairs stream half of each weight chunk per CTA
+  const int wbox = pair ? 32 : 64, dbox = pair ? (int)B->rd / 2 : (int)B->rd;
+  CUtensorMap tt, tag, tau, tbd;
+  int err;
+  if ((err = get_tmap(B->g, &tt, tgu, rgu, m, rgu, 128)) ||
+      (err = get_tmap2(B->g, &tag, B->g->aout, false, B->g->r_pad, B->inter, B->g->r_pad, 64, wbox, 128)) ||
+      (err = get_tmap2(B->u, &tau, B->u->aout, false, B->u->r_pad, B->inter, B->u->r_pad, 64, wbox, 128)) ||
+      (err = get_tmap2(B->d, &tbd, B->d->bin, false, B->inter, B->d->r_pad, B->inter, 64, dbox, 128)))
+    return fail(TNL_ERR_CUDA, "tensor map (MLP) failed: %d", err);
+  int64_t tiles_m = (m + 127) / 128;
+  if (pair) tiles_m = (tiles_m + 1) / 2 * 2;
+  const int64_t nchunks = B->inter / 64;
   // Slice the intermediate so the grid's waves are nearly full: one CTA per SM (smem-bound),
   // each CTA pays ~4 chunk-times of fixed cost (T tile load, pipeline fill, T_d flush).
   int slices = 1;
@@ -1762,7 +1766,7 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   a.trace = B->g->trace;
   if (const char* e = getenv("TNL_MLP_DBG")) a.dbg = atoi(e);
   if (cudaMemsetAsync(td32, 0, sizeof(float) * m * B->rd, st) != cudaSuccess) return fail(TNL_ERR_CUDA, "memset");
-  if ((err = launch_mlp_mid(tt, tag, tau, tbd, a, slices, st)))
+  if ((err = pair ? launch_mlp_mid_pair(tt, tag, tau, tbd, a, slices, st) : launch_mlp_mid(tt, tag, tau, tbd, a, slices, st)))
     return fail(TNL_ERR_CUDA, "MLP middle kernel launch: %s", cudaGetErrorString((cudaError_t)err));
   to_bf16(td32, td, m * B->rd, st);
   // 3. y = T_d . A_d^T

@@ -25,3 +25,7 @@ for i in (1, 2, 3, n - 2):
           "sts_done", (e[i, 1] - t0) / 1e3, "h_full", (t[i, 3] - t0) / 1e3)
 d = np.diff(t[:n, 0]) / 1e3
 print("mean us per chunk (mma start)", d.mean(), "epi span", ((t[:n, 3] - t[:n, 2]) / 1e3).mean())
+# MMA-warp detail (pair kernel): [before full wait, after full+gu_empty waits, mma_d: before h wait, after h wait, after D issue]
+d = buf[2048:2048 + 8 * 128].view(-1, 8).cpu().numpy().astype(np.int64)
+for i in list(range(0, 6)) + list(range(38, 44)):
+    print("mma", i, [round((d[i, k] - t0) / 1e3, 3) for k in range(5)])
