@@ -43,14 +43,18 @@ class TNMLP:
         except Exception:
             pass
 
-    def workspace(self, m: int):
+    def workspace_bytes(self, m: int) -> int:
         n = ctypes.c_size_t()
         N.check(self.lib.tnl_mlp_workspace_size(self.handle, int(m), ctypes.byref(n)))
-        if self._ws is None or self._ws.numel() < n.value:
-            self._ws = torch.zeros(max(int(n.value), 256), dtype=torch.uint8, device=self.device)
+        return int(n.value)
+
+    def workspace(self, m: int):
+        n = self.workspace_bytes(m)
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = torch.zeros(max(n, 256), dtype=torch.uint8, device=self.device)
         return self._ws
 
-    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
         if not isinstance(x, torch.Tensor) or not x.is_cuda:
             raise DeviceError("forward needs a CUDA tensor (no CPU fallback)")
         if x.dim() != 2 or x.shape[1] != self.hidden:
@@ -60,7 +64,10 @@ class TNMLP:
             x = x.contiguous()
         if out is None:
             out = torch.empty((m, self.hidden), dtype=self.dtype, device=self.device)
-        ws = self.workspace(m)
+        if ws is None:
+            ws = self.workspace(m)
+        elif ws.numel() < self.workspace_bytes(m):
+            raise ShapeError(f"MLP workspace {ws.numel()} < {self.workspace_bytes(m)} bytes")
         stream = torch.cuda.current_stream(self.device).cuda_stream
         N.check(self.lib.tnl_mlp_forward(self.handle, ctypes.c_void_p(x.data_ptr()), m,
                                          x.stride(0) if m > 1 else self.hidden, ctypes.c_void_p(out.data_ptr()),

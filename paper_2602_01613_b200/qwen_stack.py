@@ -13,7 +13,9 @@ The attention core is not part of the TN-linear path: it is a pass-through (the 
 output is taken to be q). Pre-norm as in Qwen3 (RMSNorm without learned scale), per layer:
   h = rms(x); q, k, v = Lq(h), Lk(h), Lv(h);  x = x + Lo(q)
   h = rms(x); x = x + Ld(silu(Lg(h)) * Lu(h))
-The projections run through libtnl (tnl_forward); residual adds and SiLU*mul are torch
+The projections run through libtnl (tnl_forward); the MLP half runs as one ``TNMLP`` block
+(tnl_mlp_forward: gate/up/SiLU*mul/down fused with h on chip for prefill-sized M and
+merged-cut ranks <= 128, else three layers around a SiLU*mul kernel); residual adds are torch
 element-wise plumbing. ``capture(m)`` records one whole pass into a CUDA graph.
 """
 
@@ -22,6 +24,7 @@ from __future__ import annotations
 import torch
 
 from . import synthetic as S
+from .mlp import TNMLP
 from .modes import default_mode_shape
 
 HIDDEN, QDIM, KVDIM, FFN = 5120, 8192, 1024, 25600
@@ -53,7 +56,8 @@ SHAPES = {"q": (QDIM, HIDDEN), "k": (KVDIM, HIDDEN), "v": (KVDIM, HIDDEN), "o": 
 
 
 class QwenTNStack:
-    def __init__(self, n_layers: int = 64, dtype=torch.bfloat16, device=None, seed: int = 40_000):
+    def __init__(self, n_layers: int = 64, dtype=torch.bfloat16, device=None, seed: int = 40_000,
+                 fused_mlp: bool = True):
         self.n_layers = n_layers
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -65,27 +69,35 @@ class QwenTNStack:
                 rows, cols = SHAPES[name]
                 layer = _tn(kinds[name], rows, cols, seed=seed + 100 * l + 10 * j)
                 blk[name] = (kinds[name], layer, layer.plan(dtype, self.device))
+            blk["mlp"] = TNMLP(blk["gate"][1], blk["up"][1], blk["down"][1], dtype=dtype, device=self.device,
+                               fused=fused_mlp)
             self.layers.append(blk)
         self._ws = None
 
     def param_count(self) -> int:
         from .layer import param_count
 
-        return sum(param_count(lay) for blk in self.layers for _, lay, _ in blk.values())
+        return sum(param_count(lay) for _, lay, _ in self.projections())
+
+    def projections(self):
+        return [blk[n] for blk in self.layers for n in ("q", "k", "v", "o", "gate", "up", "down")]
 
     def chain_flops_per_token(self) -> int:
-        return sum(lay.chain_flops_per_token() for blk in self.layers for _, lay, _ in blk.values())
+        return sum(lay.chain_flops_per_token() for _, lay, _ in self.projections())
+
+    def fused_mlp_count(self) -> int:
+        return sum(blk["mlp"].fused for blk in self.layers)
 
     def workspace(self, m: int):
-        need = max(p.workspace_bytes(m) for blk in self.layers for _, _, p in blk.values())
+        need = max(max(p.workspace_bytes(m) for _, _, p in self.projections()),
+                   max(blk["mlp"].workspace_bytes(m) for blk in self.layers))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws
 
     def _buffers(self, m: int):
         mk = lambda n: torch.empty((m, n), dtype=self.dtype, device=self.device)  # noqa: E731
-        return {"h": mk(HIDDEN), "q": mk(QDIM), "k": mk(KVDIM), "v": mk(KVDIM), "o": mk(HIDDEN), "g": mk(FFN),
-                "u": mk(FFN), "d": mk(HIDDEN)}
+        return {"h": mk(HIDDEN), "q": mk(QDIM), "k": mk(KVDIM), "v": mk(KVDIM), "o": mk(HIDDEN), "d": mk(HIDDEN)}
 
     def forward(self, x: torch.Tensor, bufs=None) -> torch.Tensor:
         """One pass of all layers; x (M x 5120) is updated in place (residual stream)."""
@@ -101,11 +113,7 @@ class QwenTNStack:
             blk["o"][2].forward(b["q"], out=b["o"], ws=ws)  # attention core: pass-through
             x.add_(b["o"])
             b["h"].copy_(rms(x))
-            blk["gate"][2].forward(b["h"], out=b["g"], ws=ws)
-            blk["up"][2].forward(b["h"], out=b["u"], ws=ws)
-            torch.nn.functional.silu(b["g"], inplace=True)
-            b["g"].mul_(b["u"])
-            blk["down"][2].forward(b["g"], out=b["d"], ws=ws)
+            blk["mlp"].forward(b["h"], out=b["d"], ws=ws)
             x.add_(b["d"])
         return x
 

@@ -359,3 +359,20 @@ def test_mlp_block_cfg3():
     y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
     ref = _mlp_ref(*[p[1] for p in pairs], x)
     assert rel(ref, y.float().cpu().numpy()) <= 2 * BF16_TOL
+
+
+def test_qwen_stack_fused_mlp_matches_unfused():
+    """cfg4 driver: the stack with fused TNMLP blocks (TT r64 / TR4 layers) equals the unfused stack."""
+    from paper_2602_01613_b200.qwen_stack import QwenTNStack
+
+    st_f = QwenTNStack(8, fused_mlp=True)
+    st_u = QwenTNStack(8, fused_mlp=False)
+    assert st_f.fused_mlp_count() == 2 and st_u.fused_mlp_count() == 0  # layers 3 (TT r64), 4 (TR4)
+    torch.manual_seed(0)
+    x0 = (0.5 * torch.randn(256, 5120, device=DEV)).to(torch.bfloat16)
+    xf, xu = x0.clone(), x0.clone()
+    st_f.forward(xf)
+    st_u.forward(xu)
+    torch.cuda.synchronize()
+    assert torch.isfinite(xf.float()).all()
+    assert rel(xu.float().cpu().numpy(), xf.float().cpu().numpy()) <= 2 * BF16_TOL

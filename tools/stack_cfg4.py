@@ -17,16 +17,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--layers", type=int, default=64)
 ap.add_argument("--ms", default="1,64,8192")
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--unfused-mlp", action="store_true")
 a = ap.parse_args()
 HBM, TC = 6554.6e9, 1635e12
 
 t0 = time.time()
-st = QwenTNStack(a.layers)
+st = QwenTNStack(a.layers, fused_mlp=not a.unfused_mlp)
 build_s = time.time() - t0
 P = st.param_count()
 F = st.chain_flops_per_token()
 print(json.dumps({"layers": a.layers, "projections": 7 * a.layers, "params": P, "chain_flops_per_token": F,
-                  "build_s": build_s}), flush=True)
+                  "build_s": build_s, "fused_mlp_blocks": st.fused_mlp_count()}), flush=True)
 for m in [int(t) for t in a.ms.split(",")]:
     g = st.capture(m)
     st.x.normal_()
@@ -40,7 +41,7 @@ for m in [int(t) for t in a.ms.split(",")]:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.iters
-    byts = 2 * (P + m * sum(r + c for blk in st.layers for _, lay, _ in blk.values() for r, c in [lay.matrix_shape]))
+    byts = 2 * (P + m * sum(r + c for _, lay, _ in st.projections() for r, c in [lay.matrix_shape]))
     t_roof = max(byts / HBM, m * F / TC)
     print(json.dumps({"M": m, "ms_per_pass": ms, "tokens_per_s": m / (ms / 1e3), "t_roofline_ms": 1e3 * t_roof,
                       "frac_roofline": 1e3 * t_roof / ms, "finite": bool(torch.isfinite(st.x).all())}), flush=True)
