@@ -179,6 +179,21 @@ TNL_API tnl_status tnl_mlp_forward(const tnl_mlp* mlp, const void* x, int64_t m,
                                    void* y, int64_t ldy, void* workspace, size_t workspace_bytes,
                                    void* stream);
 
+/* Batched cyclic one-sided Jacobi sweeps, fp64, in place — the reference's only native
+ * component, `_jacobi_cy.jacobi_sweeps(work, rot, tol, max_sweeps) -> int`
+ * (pkg/src/minima/_jacobi_cy.pyx:11-53, selected by _backend.py:5-25, called from
+ * tensor_core.py:212 inside _jacobi_svd). `work` holds `batch` row-major problems of n rows
+ * x m (the columns being orthogonalised), `rot` `batch` problems of n x nv (rotations are
+ * accumulated into it); both device pointers, problem b at offset b*n*m / b*n*nv.
+ * `sweeps` (device, batch int32, may be NULL) receives each problem's sweep count. Same
+ * visiting order, skip rules and rotation formulas as the reference; dot products are
+ * summed in a different order (the latitude the reference grants _jacobi_py.py:7-8).
+ * Errors: TNL_ERR_SHAPE for n, m < 1 or nv < 0; TNL_ERR_ARG for null pointers, negative
+ * tol / max_sweeps. */
+TNL_API tnl_status tnl_jacobi_sweeps(double* work, double* rot, int64_t batch, int64_t n, int64_t m,
+                                     int64_t nv, double tol, int32_t max_sweeps, int32_t* sweeps,
+                                     void* stream);
+
 /* Number of libtnl kernel launches issued by this thread since the last reset
  * (evidence counter for benchmarks). */
 TNL_API int64_t tnl_launch_count(int32_t reset);

@@ -37,6 +37,7 @@ EXPORTED = (
     "tnl_reconstruct",
     "tnl_launch_count",
     "tnl_plan_set_trace",
+    "tnl_jacobi_sweeps",
     "tnl_stack_workspace_size",
     "tnl_stack_forward",
     "tnl_mlp_create",
@@ -130,6 +131,8 @@ def load():
         lib.tnl_mlp_forward.restype = ctypes.c_int
         lib.tnl_plan_set_trace.argtypes = [P, P]
         lib.tnl_plan_set_trace.restype = ctypes.c_int
+        lib.tnl_jacobi_sweeps.argtypes = [P, P, i64, i64, i64, i64, ctypes.c_double, ctypes.c_int32, P, P]
+        lib.tnl_jacobi_sweeps.restype = ctypes.c_int
         lib.tnl_launch_count.argtypes = [ctypes.c_int32]
         lib.tnl_launch_count.restype = i64
         for name in ("tnl_plan_create", "tnl_plan_create_rows", "tnl_plan_destroy", "tnl_plan_query",

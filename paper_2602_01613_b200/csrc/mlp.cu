@@ -6,12 +6,22 @@
 //   h   = silu(T_g A_g^T) * (T_u A_u^T)          (M x 25600 — the expensive intermediate)
 //   T_d = h B_d^T                                 (contracts the 25600 intermediate)
 //   y   = T_d A_d^T
-// This kernel fuses the middle two lines: per (128-token tile, slice of the intermediate)
-// it streams 64-column chunks of A_g, A_u, B_d through an smem ring; G and U land in
-// double-buffered TMEM accumulators, the epilogue warps apply SiLU*mul and write the bf16
-// h chunk straight into a 128B-swizzled smem operand, and the next MMA folds it into the
-// T_d accumulator (TMEM). h never touches HBM; only the (M x r_d) partial T_d is reduced
-// into global memory (fp32, vector reductions).
+// The kernels here fuse the middle two lines: per (128-token tile, slice of the intermediate)
+// they stream 64-column chunks of A_g, A_u, B_d through an smem ring; G and U land in TMEM
+// accumulators, epilogue warps apply SiLU*mul (one MUFU tanh per element) and hand the bf16 h
+// chunk to the next MMA, which folds it into the T_d accumulator (TMEM). h never touches HBM;
+// only the (M x r_d) partial T_d of each slice is reduced into global memory (fp32 vector reds).
+//
+// Three variants, chosen by the host (launch_mlp_mid / launch_mlp_mid_pair):
+//   mlp_mid_pair_kernel  2x1 CTA pairs, cta_group::2 M=256 MMAs, T in TMEM, h via an smem ring,
+//                        separate G/U and D issuer warps (default; see its comment block)
+//   mlp_mid_ts_kernel    one CTA, T and h in TMEM (TS-mode MMAs)   — pair layout does not fit
+//   mlp_mid_kernel       one CTA, everything from smem (SS MMAs)   — TS layout does not fit
+// Measured on cfg3 (5120 -> 25600 -> 5120, TT r64, M = 8192): block 0.163 ms (pair) vs 0.170
+// (TS) vs 0.26 (SS, first version) vs 0.51 unfused vs 4.6 dense cuBLAS; the pair kernel sits
+// between two floors of similar size — the SFU (8192 tanh per chunk and CTA, 8 cycles per warp
+// instruction) and the tensor pipe (>= ~44 cycles per tcgen05.mma at N <= 64,
+// tools/ubench/mma*.cu).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -425,7 +435,6 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           tc_fence_after();
           const uint32_t th = tmem + jb.idx * 128;
           const uint64_t bd = smem_desc_sw128(smem_u32(sR + (size_t)js.idx * L.stage + L.bd_off));
-          if (!(a.dbg & 4))
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             mma_bf16_ts(tTD, th + (k >> 1) * 32 + (k & 1) * 8, bd + 2 * k, idesc_d, (j > 0 || k > 0) ? 1u : 0u);
@@ -445,13 +454,11 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           tc_fence_after();
           uint8_t* st = sR + (size_t)s * L.stage;
           const uint32_t tG = tmem + b * 128, tU = tG + 64;
-          if (!(a.dbg & 2))
           for (int k = 0; k < L.kg; ++k) {
             const uint64_t bd = smem_desc_sw128(smem_u32(st + L.ag_off + k * WBLK));
 #pragma unroll
             for (int q = 0; q < 4; ++q) mma_bf16_ts(tG, tT + k * 32 + q * 8, bd + 2 * q, idesc_gu, (k | q) != 0);
           }
-          if (!(a.dbg & 2))
           for (int k = 0; k < L.ku; ++k) {
             const uint64_t bd = smem_desc_sw128(smem_u32(st + L.au_off + k * WBLK));
 #pragma unroll
@@ -510,10 +517,6 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           uint32_t hp[16];
-          if (a.dbg & 1) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) hp[e] = gr[32 * hf + 2 * e] ^ ur[32 * hf + 2 * e + 1];
-          } else
 #pragma unroll
           for (int e = 0; e < 16; ++e)
             hp[e] = pack_bf16x2(silu(__uint_as_float(gr[32 * hf + 2 * e])) * __uint_as_float(ur[32 * hf + 2 * e]),

@@ -15,7 +15,6 @@ struct MlpArgs {
   int32_t chunks_per_slice;
   float* td;           // fp32 [M][ld_td] partial-sum target (zeroed by the caller)
   int64_t ld_td;
-  int32_t dbg;                // experiment switches (0 in production)
   unsigned long long* trace;  // optional: CTA 0 per-chunk %globaltimer stamps [chunk][4]
 };
 

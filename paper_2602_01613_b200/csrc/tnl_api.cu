@@ -1764,13 +1764,27 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   a.td = td32;
   a.ld_td = B->rd;
   a.trace = B->g->trace;
-  if (const char* e = getenv("TNL_MLP_DBG")) a.dbg = atoi(e);
   if (cudaMemsetAsync(td32, 0, sizeof(float) * m * B->rd, st) != cudaSuccess) return fail(TNL_ERR_CUDA, "memset");
   if ((err = pair ? launch_mlp_mid_pair(tt, tag, tau, tbd, a, slices, st) : launch_mlp_mid(tt, tag, tau, tbd, a, slices, st)))
     return fail(TNL_ERR_CUDA, "MLP middle kernel launch: %s", cudaGetErrorString((cudaError_t)err));
   to_bf16(td32, td, m * B->rd, st);
   // 3. y = T_d . A_d^T
   return tc_step_p(B->d, td, B->rd, B->d->aout, B->d->r_pad, m, B->hidden, B->d->r_pad, y, ldy, false, 1, st);
+}
+
+tnl_status tnl_jacobi_sweeps(double* work, double* rot, int64_t batch, int64_t n, int64_t m, int64_t nv, double tol,
+                             int32_t max_sweeps, int32_t* sweeps, void* stream) {
+  if (batch < 0) return fail(TNL_ERR_ARG, "negative batch %lld", (long long)batch);
+  if (batch == 0) return TNL_OK;
+  if (n < 1 || m < 1 || nv < 0 || n > INT32_MAX || m > INT32_MAX || nv > INT32_MAX)
+    return fail(TNL_ERR_SHAPE, "jacobi problem shape n=%lld m=%lld nv=%lld", (long long)n, (long long)m,
+                (long long)nv);
+  if (!work || (nv > 0 && !rot)) return fail(TNL_ERR_ARG, "null argument");
+  if (!(tol >= 0.0) || max_sweeps < 0) return fail(TNL_ERR_ARG, "tol must be >= 0 and max_sweeps >= 0");
+  const int err = tnl::launch_jacobi_sweeps(work, rot, batch, (int)n, (int)m, (int)nv, tol, max_sweeps, sweeps,
+                                       static_cast<cudaStream_t>(stream));
+  if (err) return fail(TNL_ERR_CUDA, "jacobi launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
 }
 
 tnl_status tnl_plan_set_trace(tnl_plan* plan, void* device_buffer) {
