@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(192, 1)
             p.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
             p.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
             const int ch = ((cc % 64) / 8) + j;
-            *reinterpret_cast<uint4*>(rowp + ((ch ^ (lrow & 7)) << 4)) = p;
+            sts128(smem_u32(rowp) + ((ch ^ (lrow & 7)) << 4), p);
           }
         }
         tc_fence_before();

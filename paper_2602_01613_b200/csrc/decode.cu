@@ -33,7 +33,9 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
 
 template <int BN, int STAGES, bool ACT_F32>
 struct DecSmem {
-  static constexpr uint32_t B_STAGE = BN * BK * 2;          // bf16 activation operand
+  // bf16 activation operand: x K-major [BN tokens][64 k] (phase A, TMA) or T MN-major
+  // [64 kappa][128 B] (phase B: the kappa-major accumulator converted without a transpose)
+  static constexpr uint32_t B_STAGE = ACT_F32 ? 64 * 128 : BN * BK * 2;
   static constexpr uint32_t F_STAGE = ACT_F32 ? BK * BN * 4 : 0;  // fp32 staging [64 k][BN tokens]
   static constexpr uint32_t Y_BYTES = ACT_F32 ? BN * BM * 2 : 0;  // y tile [BN tokens][128 rows]
   static constexpr size_t bytes = 1024 + (size_t)STAGES * (A_STAGE + B_STAGE + F_STAGE) + Y_BYTES + 512;
@@ -136,7 +138,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      constexpr uint32_t idesc = ACT_F32 ? idesc_bf16_f32_bmn(BM, BN) : idesc_bf16_f32(BM, BN);
+      constexpr uint32_t bstep = ACT_F32 ? 128 : 2;  // descriptor advance per K=16
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         mbar_wait(&full[s], (i / STAGES) & 1);
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
         const uint64_t adesc = smem_desc_sw128(smem_u32(sA + s * A_STAGE));
         const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + s * B_STAGE));
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) mma_bf16_ss(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
+        for (int k = 0; k < BK / 16; ++k) mma_bf16_ss(tmem, adesc + 2 * k, bdesc + bstep * k, idesc, (i | k) != 0);
         mma_commit(&empty[s]);
       }
       mma_commit(done);
@@ -157,22 +160,29 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     pdl_wait();
     if (et == 0) TRACE(6);
     if constexpr (ACT_F32) {
-      // staged fp32 [64 kappa][BN tokens] -> bf16 SW128 operand [BN tokens][64 kappa]
+      // staged fp32 [64 kappa][BN tokens] -> bf16 MN-major SW128 operand [64 kappa][128 B]
+      constexpr int ITEMS = 64 * (BN / 4);  // (kappa, 4-token quad)
+      constexpr int PER = ITEMS >= DEC_EPI ? ITEMS / DEC_EPI : 1;
       for (int i = 0; i < nkb; ++i) {
         mbar_wait(&stg[i], 0);
-        const float* src = sF + i * (F_STAGE / 4);
-        uint8_t* dst = sB + i * B_STAGE;
-        for (int e = et; e < BN * 8; e += DEC_EPI) {
-          const int r = e % BN, c = e / BN;  // token r, kappa chunk c
-          float f[8];
+        const uint32_t src = smem_u32(sF) + i * F_STAGE;
+        const uint32_t dst = smem_u32(sB) + i * B_STAGE;
+        float4 v[PER];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) f[q] = src[(c * 8 + q) * BN + r];
-          uint4 p;
-          p.x = pack_bf16x2(f[0], f[1]);
-          p.y = pack_bf16x2(f[2], f[3]);
-          p.z = pack_bf16x2(f[4], f[5]);
-          p.w = pack_bf16x2(f[6], f[7]);
-          *reinterpret_cast<uint4*>(dst + sw128_off(r, c)) = p;
+        for (int u = 0; u < PER; ++u) {
+          const int e = et + u * DEC_EPI;
+          if (e < ITEMS) v[u] = lds128f(src + 16 * e);
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int e = et + u * DEC_EPI;
+          if (e < ITEMS) {
+            const int kap = e / (BN / 4), quad = e % (BN / 4);
+            uint2 p;
+            p.x = pack_bf16x2(v[u].x, v[u].y);
+            p.y = pack_bf16x2(v[u].z, v[u].w);
+            sts64(dst + sw128_off(kap, quad >> 1) + (quad & 1) * 8, p);
+          }
         }
         fence_proxy_async_smem();
         named_bar(1, DEC_EPI);
@@ -196,7 +206,12 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       if constexpr (ACT_F32) {
         // y tile staged [token][row] for one TMA store
 #pragma unroll
-        for (int e = 0; e < 16; ++e) sY[(c + e) * BM + lrow] = __float2bfloat16_rn(v[e]);
+        for (int e = 0; e < 16; ++e) {
+          const __nv_bfloat16 h = __float2bfloat16_rn(v[e]);
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(smem_u32(sY + (c + e) * BM + lrow)),
+                       "h"(*reinterpret_cast<const unsigned short*>(&h))
+                       : "memory");
+        }
       } else {
         if (!row_ok || c >= a.tokens) continue;
         const int n = min(16, a.tokens - c);

@@ -35,8 +35,8 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 template <int BN>
 struct FSmem {
   static constexpr uint32_t F_BLK = BN * 64 * 4;   // fp32 staging of 64 kappa x BN tokens
-  static constexpr uint32_t T_BLK = BN * 64 * 2;   // bf16 T operand block [BN][64]
-  static constexpr uint32_t X_BLK = BN * 64 * 2;   // bf16 x operand block [BN][64]
+  static constexpr uint32_t T_BLK = 64 * 128;      // bf16 T operand block, MN-major [64 kappa][128 B]
+  static constexpr uint32_t X_BLK = 64 * 128;      // bf16 x operand block, MN-major [64 k][128 B]
   static constexpr size_t bytes = 1024 + 4 * WBLK /*A_out*/ + 4 * WBLK /*B_in*/ + 4 * F_BLK +
                                   4 * T_BLK + 256;
 };
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(FT, 1)
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      constexpr uint32_t idesc = idesc_bf16_f32_bmn(128, BN);  // T and x operands are MN-major
       mbar_wait(wfull, 0);
       mbar_wait(tfull, 0);
       tc_fence_after();
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(FT, 1)
         const uint64_t ad = smem_desc_sw128(smem_u32(sWo + kb * WBLK));
         const uint64_t bd = smem_desc_sw128(smem_u32(sT + kb * SM::T_BLK));
 #pragma unroll
-        for (int k = 0; k < 4; ++k) mma_bf16_ss(tDB, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+        for (int k = 0; k < 4; ++k) mma_bf16_ss(tDB, ad + 2 * k, bd + 128 * k, idesc, (kb | k) != 0);
       }
       mma_commit(bdone);
       mbar_wait(xfull, 0);
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(FT, 1)
           const uint64_t ad = smem_desc_sw128(smem_u32(sWi + (t * 2 + h) * WBLK));
           const uint64_t bd = smem_desc_sw128(smem_u32(sX + h * SM::X_BLK));
 #pragma unroll
-          for (int k = 0; k < 4; ++k) mma_bf16_ss(tDA + t * BN, ad + 2 * k, bd + 2 * k, idesc, (h | k) != 0);
+          for (int k = 0; k < 4; ++k) mma_bf16_ss(tDA + t * BN, ad + 2 * k, bd + 128 * k, idesc, (h | k) != 0);
         }
       mma_commit(adone);
     }
@@ -148,24 +148,39 @@ __global__ void __launch_bounds__(FT, 1)
   } else {
     const int et = threadIdx.x - 64;
     pdl_wait();
-    // T_l: fp32 [64 kappa][BN tokens] -> bf16 SW128 [BN tokens][64 kappa] per k-block
+    if (et == 0) TRACE(11);
+    // T_l: fp32 [64 kappa][BN tokens] -> bf16 MN-major SW128 [64 kappa][128 B] per k-block
+    // (the accumulator's kappa-major layout is the MMA's MN-major B operand: no transpose)
+    // one float4 (4 tokens) per thread and step: the warp reads 512 contiguous bytes (no bank
+    // conflicts) and writes 8-byte halves of the swizzled 16-byte chunks
+    constexpr int ITEMS = 64 * (BN / 4);  // (kappa, 4-token quad) per block
+    constexpr int PER = ITEMS >= FEPI ? ITEMS / FEPI : 1;
     for (int kb = 0; kb < kbB; ++kb) {
-      mbar_wait(&stg[kb], 0);
-      const float* src = sF + kb * (SM::F_BLK / 4);
-      uint8_t* dst = sT + kb * SM::T_BLK;
-      for (int e = et; e < BN * 8; e += FEPI) {
-        const int r = e % BN, c = e / BN;
-        float f[8];
+      if (lane_id() == 0) mbar_wait(&stg[kb], 0);
+      __syncwarp();
+      if (et == 0 && kb == 0) TRACE(12);
+      const uint32_t src = smem_u32(sF) + kb * SM::F_BLK;
+      const uint32_t dst = smem_u32(sT) + kb * SM::T_BLK;
+      float4 v[PER];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) f[q] = src[(c * 8 + q) * BN + r];
-        uint4 p;
-        p.x = pack_bf16x2(f[0], f[1]);
-        p.y = pack_bf16x2(f[2], f[3]);
-        p.z = pack_bf16x2(f[4], f[5]);
-        p.w = pack_bf16x2(f[6], f[7]);
-        *reinterpret_cast<uint4*>(dst + sw128(r, c)) = p;
+      for (int u = 0; u < PER; ++u) {
+        const int e = et + u * FEPI;
+        if (e < ITEMS) v[u] = lds128f(src + 16 * e);
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int e = et + u * FEPI;
+        if (e < ITEMS) {
+          const int kap = e / (BN / 4), quad = e % (BN / 4);
+          uint2 p;
+          p.x = pack_bf16x2(v[u].x, v[u].y);
+          p.y = pack_bf16x2(v[u].z, v[u].w);
+          sts64(dst + sw128(kap, quad >> 1) + (quad & 1) * 8, p);
+        }
       }
     }
+    if (et == 0) TRACE(13);
+
     fence_proxy_async_smem();
     nbar(1, FEPI);
     if (et == 0) mbar_arrive(tfull);
@@ -180,17 +195,19 @@ __global__ void __launch_bounds__(FT, 1)
     tc_fence_after();
     if (et == 0) TRACE(6);
     {
-      uint8_t* xb = sX + (lrow >> 6) * SM::X_BLK;
-      const int ck = (lrow & 63) >> 3, cw = (lrow & 7) * 2;
+      // x operand of layer l+1, MN-major: K index = this CTA's row lrow, 128-byte row of tokens
 #pragma unroll 1
       for (int c = c_begin; c < c_begin + HALF && c < BN; c += 16) {
         float v[16];
         tmem_ld16(tDB + ((q * 32) << 16) + c, v);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int r = c + e;
-          *reinterpret_cast<__nv_bfloat16*>(xb + (r >> 3) * 1024 + (r & 7) * 128 + ((ck ^ (r & 7)) << 4) + cw) =
-              __float2bfloat16_rn(v[e]);
+        for (int j = 0; j < 2; ++j) {
+          uint4 p;
+          p.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+          p.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+          p.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+          p.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+          sts128(smem_u32(sX) + sw128(lrow, c / 8 + j), p);
         }
       }
     }

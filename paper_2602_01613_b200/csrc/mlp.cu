@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
           p.z = pack_bf16x2(h[4], h[5]);
           p.w = pack_bf16x2(h[6], h[7]);
           const int ch = cb / 8 + j;
-          *reinterpret_cast<uint4*>(rowp + ((ch ^ (lrow & 7)) << 4)) = p;
+          sts128(smem_u32(rowp) + ((ch ^ (lrow & 7)) << 4), p);
         }
         if (tr && i < 256) tr[1024 + i * 4 + 1] = globaltimer();
         fence_proxy_async_smem();
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
         uint32_t r[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((c ^ (lrow & 7)) << 4));
+          const uint4 v = lds128(smem_u32(rowp) + ((c ^ (lrow & 7)) << 4));
           r[4 * c] = v.x;
           r[4 * c + 1] = v.y;
           r[4 * c + 2] = v.z;
@@ -751,7 +751,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP_PAIR_THREADS, 1)
         uint32_t r[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((c ^ (lrow & 7)) << 4));
+          const uint4 v = lds128(smem_u32(rowp) + ((c ^ (lrow & 7)) << 4));
           r[4 * c] = v.x;
           r[4 * c + 1] = v.y;
           r[4 * c + 2] = v.z;
@@ -800,7 +800,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP_PAIR_THREADS, 1)
                             silu_mul(__uint_as_float(gr[8 * c + 5]), __uint_as_float(ur[8 * c + 5])));
           p.w = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 6]), __uint_as_float(ur[8 * c + 6])),
                             silu_mul(__uint_as_float(gr[8 * c + 7]), __uint_as_float(ur[8 * c + 7])));
-          *reinterpret_cast<uint4*>(rowp + ((c ^ (lrow & 7)) << 4)) = p;
+          sts128(smem_u32(rowp) + ((c ^ (lrow & 7)) << 4), p);
         }
         fence_proxy_async_smem();
         __syncwarp();

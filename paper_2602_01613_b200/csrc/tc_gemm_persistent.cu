@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(192, 1)
             p1.w = pack_bf16x2(v[14], v[15]);
             const int ch = c / 8;  // 16-byte chunk index within the 128-byte row
             uint8_t* rowp = stage + (lrow >> 3) * 1024 + (lrow & 7) * 128;
-            *reinterpret_cast<uint4*>(rowp + (((ch) ^ (lrow & 7)) << 4)) = p0;
-            *reinterpret_cast<uint4*>(rowp + (((ch + 1) ^ (lrow & 7)) << 4)) = p1;
+            sts128(smem_u32(rowp) + (((ch) ^ (lrow & 7)) << 4), p0);
+            sts128(smem_u32(rowp) + (((ch + 1) ^ (lrow & 7)) << 4), p1);
           }
           if (c0 + 64 >= BN) {  // all TMEM reads of this accumulator are done
             tc_fence_before();

@@ -37,7 +37,8 @@ for b in bufs:
 st.replay()
 torch.cuda.synchronize()
 EV = ["start", "setup", "w_issued", "pdl_passed", "mma_first", "mma_issued", "epi_pdl", "act_ready", "done", "stored", "end"]
-EVF = ["start", "setup", "w_issued", "pdl_passed", "T_landed", "T_converted", "B_done", "x_ready", "A_done", "reds_issued", "end"]
+EVF = ["start", "setup", "w_issued", "pdl_passed", "T_landed", "T_converted", "B_done", "x_ready", "A_done", "reds_issued", "end",
+       "epi_pdl", "stg0", "conv_loop_done"]
 t0 = None
 for li, (v, b) in enumerate(zip(vs, bufs)):
     arr = b.view(2, 1024, 16).cpu().numpy()
@@ -55,6 +56,9 @@ for li, (v, b) in enumerate(zip(vs, bufs)):
             col = blk[:, e]
             col = col[col > 0]
             if len(col) == 0:
+                continue
+            if nm.endswith("cycles"):
+                row.append(f"{nm}={int(col.min())}/{int(np.median(col))}/{int(col.max())}")
                 continue
             row.append(f"{nm}={(col.min()-t0)/1e3:.2f}/{(np.median(col)-t0)/1e3:.2f}/{(col.max()-t0)/1e3:.2f}")
         kind = "fused" if (ph == 1 and li + 1 < len(vs)) else "phase" + "AB"[ph]
