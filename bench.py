@@ -213,6 +213,21 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel (dec_fused_kernel) from the committed
+    `ncu --set full` capture (profiles/r01/ncu_dec_fused.json); (None, reason) if absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_dec_fused.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return (d["fused_mean_dram_bytes_per_launch"],
+                "dram__bytes_read.sum + dram__bytes_write.sum per dec_fused_kernel launch (mean over the cfg2 "
+                f"boundaries), ncu --set full capture {os.path.relpath(path)}; algorithmic weight bytes per launch "
+                f"{d['fused_mean_weight_bytes_per_launch']:.0f}")
+    except (OSError, KeyError, ValueError):
+        return None, "no ncu capture committed"
+
+
 def time_graph(replay, steps, warmup, torch, dist=None):
     for _ in range(warmup):
         replay()
@@ -406,7 +421,8 @@ def main():
             "peak_kind": peak_kind,
             "unit": "GB/s",
             "frac": achieved_gbs / hbm,
-            "traffic": None,
+            "traffic": ncu_traffic()[0],
+            "traffic_note": ncu_traffic()[1],
             "algorithmic_bytes_per_step": alg_bytes,
             "plan_weight_bytes_per_step": plan_bytes,
             "t_roofline_ms": 1e3 * t_roof,
