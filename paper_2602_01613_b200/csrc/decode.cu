@@ -136,6 +136,16 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
         tma_load_2d(sB + s * B_STAGE, &tmX, &full[s], (kb0 + i) * BK, 0);
       }
     }
+    __syncwarp();
+    if (a.zero_prev) {  // a buffer only the previous kernel read: zero this CTA's slice
+      pdl_wait();
+      const int64_t ncta = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+      const int64_t cta = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
+      const int64_t n4 = a.zero_prev_elems / 4, per = (n4 + ncta - 1) / ncta;
+      float4* z = reinterpret_cast<float4*>(a.zero_prev);
+      const int64_t e0 = cta * per, e1 = min(n4, e0 + per);
+      for (int64_t e = e0 + lane_id(); e < e1; e += 32) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t idesc = ACT_F32 ? idesc_bf16_f32_bmn(BM, BN) : idesc_bf16_f32(BM, BN);

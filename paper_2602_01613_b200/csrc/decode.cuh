@@ -40,6 +40,9 @@ struct DecArgs {
   // last-CTA zeroing of act_f32 (phase B)
   unsigned int* counter;
   int64_t zero_elems;
+  // cooperative zeroing (all CTAs, after the dependency wait) of a buffer the previous kernel read
+  float* zero_prev;
+  int64_t zero_prev_elems;
   // optional timeline (tnl_plan_set_trace): [cta][16] %globaltimer stamps
   unsigned long long* trace;
 };
@@ -60,10 +63,13 @@ struct FusedArgs {
   int32_t rows;        // rows of layer l == cols of layer l+1 (multiple of 128)
   int32_t kB;          // r_pad of layer l (<= 256)
   int32_t nA;          // r_pad of layer l+1 (<= 256)
-  float* t_in;         // T_l, kappa-major [kB][64], re-zeroed by the last CTA
-  unsigned int* cnt_in;
+  float* t_in;         // T_l, kappa-major [kB][64]
+  unsigned int* cnt_in;  // unused (kept for layout stability)
   float* t_out;        // T_{l+1}, kappa-major [nA][64], fp32 reductions
-  int64_t zero_elems;
+  int64_t zero_elems;  // floats of t_zero
+  float* t_zero;       // T_{l-1} (read by the previous kernel only): zeroed cooperatively, so it is
+                       // back at rest before it is accumulated again two boundaries later
+                       // (three rotating accumulators; no last-CTA tail, no counters)
   unsigned long long* trace;  // optional per-CTA %globaltimer stamps [cta][16]
 };
 // wo: A_out^l map (box {64, 128}, SW128); t: T_l fp32 map (box {BN, 64}); wi: B_in^{l+1}

@@ -113,12 +113,17 @@ __global__ void __launch_bounds__(FT, 1)
         mbar_arrive_expect_tx(&stg[kb], SM::F_BLK);
         tma_load_2d(reinterpret_cast<uint8_t*>(sF) + kb * SM::F_BLK, &tmT, &stg[kb], 0, kb * 64);
       }
-      // count this CTA's reads of T_l (off the epilogue's critical path)
       for (int kb = 0; kb < kbB; ++kb) mbar_wait(&stg[kb], 0);
       TRACE(4);
-      __threadfence();
-      *last_flag = (atomicAdd(a.cnt_in, 1u) == gridDim.x - 1) ? 1u : 0u;
-      mbar_arrive(flagbar);
+    }
+    __syncwarp();
+    // T_{l-1} was read only by the previous kernel, which has completed: zero this CTA's slice
+    if (a.t_zero) {
+      pdl_wait();
+      const int64_t n4 = a.zero_elems / 4, per = (n4 + gridDim.x - 1) / gridDim.x;
+      float4* z = reinterpret_cast<float4*>(a.t_zero);
+      const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(n4, e0 + per);
+      for (int64_t e = e0 + lane_id(); e < e1; e += 32) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   } else if (warp == 1) {
     if (elect_one()) {
@@ -240,13 +245,7 @@ __global__ void __launch_bounds__(FT, 1)
       }
     }
     if (et == 0) TRACE(9);
-    // the last CTA to read T_l re-zeroes it for its next use
-    mbar_wait(flagbar, 0);
-    if (*last_flag) {
-      float4* z = reinterpret_cast<float4*>(a.t_in);
-      for (int64_t e = et; e < a.zero_elems / 4; e += FEPI) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (et == 0) atomicExch(a.cnt_in, 0u);
-    }
+
   }
   tc_fence_before();
   __syncthreads();

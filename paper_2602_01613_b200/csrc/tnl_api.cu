@@ -1429,7 +1429,7 @@ static bool stack_fusable(const tnl_plan* const* plans, int32_t n, int64_t m) {
 }
 
 static size_t stack_ws_bytes(const tnl_plan* const* plans, int32_t n, int64_t m) {
-  if (stack_fusable(plans, n, m)) return 2 * round_up(sizeof(float) * 64 * 256, 256) + 256;
+  if (stack_fusable(plans, n, m)) return 3 * round_up(sizeof(float) * 64 * 256, 256) + 256;
   size_t mx = 0;
   int64_t width = 0;
   for (int i = 0; i < n; ++i) {
@@ -1541,8 +1541,11 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
   }
   char* base = static_cast<char*>(ws);
   const size_t slot = round_up(sizeof(float) * 64 * 256, 256);
-  float* tacc[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + slot)};
-  unsigned int* cnt = reinterpret_cast<unsigned int*>(base + 2 * slot);  // [2]
+  // three rotating zero-at-rest accumulators: boundary l reads T_l = tacc[l % 3], reduces into
+  // T_{l+1} = tacc[(l+1) % 3] and zeroes T_{l-1} = tacc[(l+2) % 3], which only boundary l-1 read
+  float* tacc[3] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + slot),
+                    reinterpret_cast<float*>(base + 2 * slot)};
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(base + 3 * slot);  // [1] (last phase B)
   const int bn = pick_bn(m);
   int err = 0;
   // layer 0, phase A
@@ -1574,7 +1577,7 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     tnl_plan* Q = Pv[l + 1];
     CUtensorMap two, tt, twi;
     if ((err = get_tmap(P, &two, P->aout, P->r_pad, P->rows, P->r_pad, 128)) ||
-        (err = get_tmap2(P, &tt, tacc[l & 1], true, 64, P->r_pad, 64, bn, 64, 0)) ||
+        (err = get_tmap2(P, &tt, tacc[l % 3], true, 64, P->r_pad, 64, bn, 64, 0)) ||
         (err = get_tmap(Q, &twi, Q->bin, Q->cols, Q->r_pad, Q->cols, 128)))
       return fail(TNL_ERR_CUDA, "tensor map (stack boundary) failed: %d", err);
     FusedArgs f;
@@ -1583,10 +1586,11 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     f.rows = (int32_t)P->rows;
     f.kB = (int32_t)P->r_pad;
     f.nA = (int32_t)Q->r_pad;
-    f.t_in = tacc[l & 1];
-    f.cnt_in = cnt + (l & 1);
-    f.t_out = tacc[(l + 1) & 1];
-    f.zero_elems = 64 * P->r_pad;
+    f.t_in = tacc[l % 3];
+    f.cnt_in = nullptr;
+    f.t_out = tacc[(l + 1) % 3];
+    f.t_zero = l >= 1 ? tacc[(l + 2) % 3] : nullptr;
+    f.zero_elems = l >= 1 ? 64 * Pv[l - 1]->r_pad : 0;
     f.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
     if ((err = launch_dec_fused(two, tt, twi, f, (int)(P->rows / 128), st)))
       return fail(TNL_ERR_CUDA, "stack boundary launch: %s", cudaGetErrorString((cudaError_t)err));
@@ -1598,7 +1602,7 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     const int64_t rows_local = P->row_end - P->row_begin;
     CUtensorMap tw2, tt, ty;
     if ((err = get_tmap(P, &tw2, P->aout, P->r_pad, rows_local, P->r_pad, 128)) ||
-        (err = get_tmap2(P, &tt, tacc[l & 1], true, 64, P->r_pad, 64, bn, 64, 0)) ||
+        (err = get_tmap2(P, &tt, tacc[l % 3], true, 64, P->r_pad, 64, bn, 64, 0)) ||
         (err = get_tmap2(P, &ty, y, false, rows_local, m, ldy, 128, bn, 0)))
       return fail(TNL_ERR_CUDA, "tensor map (stack phase B) failed: %d", err);
     DecArgs b;
@@ -1607,13 +1611,17 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     b.tokens = (int32_t)m;
     b.K = (int32_t)P->r_pad;
     b.kb_per_split = (int32_t)((P->r_pad + 63) / 64);
-    b.act_f32 = tacc[l & 1];
+    b.act_f32 = tacc[l % 3];
     b.act_ld = 64;
     b.out = y;
     b.ldo_i = 1;
     b.ldo_j = ldy;
-    b.counter = cnt + (l & 1);
+    b.counter = cnt;  // the last CTA re-zeroes T_{n-1}
     b.zero_elems = 64 * P->r_pad;
+    if (l >= 1) {  // T_{n-2}, read only by the last boundary kernel
+      b.zero_prev = tacc[(l + 2) % 3];
+      b.zero_prev_elems = 64 * Pv[l - 1]->r_pad;
+    }
     b.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
     if ((err = launch_dec_b(tw2, tt, ty, b, st)))
       return fail(TNL_ERR_CUDA, "stack phase B launch: %s", cudaGetErrorString((cudaError_t)err));
