@@ -57,12 +57,12 @@ __global__ void __launch_bounds__(FT, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + 4 * SM::T_BLK);
   uint64_t* wfull = bars;
   uint64_t* stg = bars + 1;  // [4]
-  uint64_t* tfull = bars + 5;
+  uint64_t* tfull = bars + 10;  // [4]: T block kb converted (one arrive per epilogue warp)
   uint64_t* bdone = bars + 6;
   uint64_t* xfull = bars + 7;
   uint64_t* adone = bars + 8;
   uint64_t* flagbar = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   uint32_t* last_flag = tmem_slot + 1;
 
   const int tile = blockIdx.x;
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(FT, 1)
     tma_prefetch_desc(&tmWi);
     mbar_init(wfull, 1);
     for (int s = 0; s < 4; ++s) mbar_init(&stg[s], 1);
-    mbar_init(tfull, 1);
+    for (int kb = 0; kb < 4; ++kb) mbar_init(&tfull[kb], FEPI / 32);
     mbar_init(bdone, 1);
     mbar_init(xfull, 1);
     mbar_init(adone, 1);
@@ -129,9 +129,9 @@ __global__ void __launch_bounds__(FT, 1)
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16_f32_bmn(128, BN);  // T and x operands are MN-major
       mbar_wait(wfull, 0);
-      mbar_wait(tfull, 0);
-      tc_fence_after();
-      for (int kb = 0; kb < kbB; ++kb) {
+      for (int kb = 0; kb < kbB; ++kb) {  // block kb as soon as it is converted
+        mbar_wait(&tfull[kb], 0);
+        tc_fence_after();
         const uint64_t ad = smem_desc_sw128(smem_u32(sWo + kb * WBLK));
         const uint64_t bd = smem_desc_sw128(smem_u32(sT + kb * SM::T_BLK));
 #pragma unroll
@@ -183,12 +183,11 @@ __global__ void __launch_bounds__(FT, 1)
           sts64(dst + sw128(kap, quad >> 1) + (quad & 1) * 8, p);
         }
       }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&tfull[kb]);
     }
     if (et == 0) TRACE(13);
-
-    fence_proxy_async_smem();
-    nbar(1, FEPI);
-    if (et == 0) mbar_arrive(tfull);
     if (et == 0) TRACE(5);
 
     const uint32_t q = warp & 3;
