@@ -286,3 +286,25 @@ class TestTruncatedSvdGPU:
         assert a.left.tobytes() == b.left.tobytes()
         assert a.values.tobytes() == b.values.tobytes()
         assert a.right.tobytes() == b.right.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,nv", [(6, 300, 6), (5, 40, 290), (33, 33, 33), (1, 8, 1)])
+def test_gpu_sweeps_generic_and_edge_shapes(n, m, nv):
+    """Rows longer than the register-resident variant (m or nv > 256 -> generic kernel), odd
+    sizes, and the single-row problem (no pair: one sweep, nothing rotated)."""
+    import torch
+
+    from paper_2602_01613_b200 import jacobi as J
+
+    rng = np.random.default_rng(n * 1000 + m + nv)
+    work = rng.standard_normal((2, n, m))
+    rot = rng.standard_normal((2, n, nv))
+    wt, rt = torch.tensor(work, device="cuda"), torch.tensor(rot, device="cuda")
+    sweeps = J.jacobi_sweeps_batched(wt, rt).cpu().numpy()
+    for i in range(2):
+        w0, r0 = work[i].copy(), rot[i].copy()
+        s0 = O.jacobi_sweeps(w0, r0, O.JACOBI_TOL, O.JACOBI_MAX_SWEEPS)
+        assert int(sweeps[i]) == s0
+        assert _close(w0, wt[i].cpu().numpy(), float(np.linalg.norm(work[i])))
+        assert _close(r0, rt[i].cpu().numpy(), float(np.linalg.norm(rot[i])))
