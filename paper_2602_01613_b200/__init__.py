@@ -28,6 +28,7 @@ from .layer import (
     reconstruct,
 )
 from .modes import balanced_split, default_mode_shape, maximal_ranks, param_count_formula, select_ranks
+from .contraction import flop_report, plan_contraction, relative_error, reshape_to_modes
 
 __all__ = [
     "CompressedLayer",
@@ -42,6 +43,10 @@ __all__ = [
     "default_mode_shape",
     "maximal_ranks",
     "select_ranks",
+    "relative_error",
+    "reshape_to_modes",
+    "plan_contraction",
+    "flop_report",
     "modes",
     "launch_count",
     "PLAN_AUTO",
