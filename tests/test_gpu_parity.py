@@ -376,3 +376,24 @@ def test_qwen_stack_fused_mlp_matches_unfused():
     torch.cuda.synchronize()
     assert torch.isfinite(xf.float()).all()
     assert rel(xu.float().cpu().numpy(), xf.float().cpu().numpy()) <= 2 * BF16_TOL
+
+
+@pytest.mark.parametrize("rg,rd,variant", [(64, 64, "pair"), (128, 64, "ts"), (64, 256, "ss"), (128, 256, "ss")])
+def test_mlp_kernel_variants(rg, rd, variant):
+    """Each middle-kernel variant (csrc/mlp.cu) against the oracle, selected by the rank layout:
+    pair (cut ranks <= 64 and r_d = 64: three TMEM G/U pairs), TS (T needs 128 TMEM columns:
+    two pairs), SS (r_d = 256 leaves no room for T in TMEM). M = 300: a ragged last tile and an
+    odd tile count (the pair grid pads to an even count)."""
+    from paper_2602_01613_b200.mlp import TNMLP
+
+    hid, inter = 512, 1024
+    Lg = O.synthetic_layer("tucker", (inter, hid), 1, (rg, rg), seed=52_001)
+    Lu = O.synthetic_layer("tucker", (inter, hid), 1, (rg, rg), seed=52_002)
+    Ld = O.synthetic_layer("tucker", (hid, inter), 1, (rd, rd), seed=52_003)
+    (g, Lgr), (u, Lur), (d, Ldr) = (to_layer(L, round_bf16=True) for L in (Lg, Lu, Ld))
+    mlp = TNMLP(g, u, d)
+    assert mlp.fused, variant
+    x = O.round_bf16(O.synthetic_x(300, hid, seed=52_004))
+    y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
+    torch.cuda.synchronize()
+    assert rel(_mlp_ref(Lgr, Lur, Ldr, x), y.float().cpu().numpy()) <= 2 * BF16_TOL
