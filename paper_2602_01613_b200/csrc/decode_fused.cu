@@ -220,27 +220,45 @@ __global__ void __launch_bounds__(FT, 1)
     nbar(1, FEPI);
     if (et == 0) mbar_arrive(xfull);
     if (et == 0) TRACE(7);
-    // D_A -> fp32 reductions into T_{l+1} (kappa-major [kappa][64])
+    // D_A -> fp32 reductions into T_{l+1} (kappa-major [kappa][64]). A thread holds one kappa
+    // row, so reducing straight from TMEM makes every 16-byte red its own L2 transaction (32
+    // per warp instruction); the partial is transposed through smem first (over the B_in blocks,
+    // free once adone fired; float4 slots XOR-swizzled by kappa & 7) so that each warp then
+    // reduces two contiguous 256-byte rows per instruction.
     mbar_wait(adone, 0);
     tc_fence_after();
     if (et == 0) TRACE(8);
+    constexpr int SLOTS = BN / 4;  // float4 slots per kappa row
+    const uint32_t stage = smem_u32(sWi);
+    auto slot_addr = [&](int kap, int sl) {
+      return stage + (uint32_t)(kap * SLOTS + (sl ^ (kap & 7 & (SLOTS - 1)))) * 16u;
+    };
     for (int t = 0; t < nT; ++t) {
       const int kap = t * 128 + lrow;
 #pragma unroll 1
       for (int c = c_begin; c < c_begin + HALF && c < BN; c += 16) {
         float v[16];
         tmem_ld16(tDA + t * BN + ((q * 32) << 16) + c, v);
-        if (kap >= a.nA || c >= a.tokens) continue;
-        const int n = min(16, a.tokens - c);
-        float* o = a.t_out + (int64_t)kap * 64 + c;
-        if (n == 16) {
+        if (kap >= a.nA) continue;
 #pragma unroll
-          for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (e < n) atomicAdd(o + e, v[e]);
+        for (int j = 0; j < 4; ++j) {
+          uint4 p;
+          p.x = __float_as_uint(v[4 * j]);
+          p.y = __float_as_uint(v[4 * j + 1]);
+          p.z = __float_as_uint(v[4 * j + 2]);
+          p.w = __float_as_uint(v[4 * j + 3]);
+          sts128(slot_addr(kap, c / 4 + j), p);
         }
+      }
+    }
+    nbar(1, FEPI);
+    {
+      const int tok_slots = (a.tokens + 3) / 4 < SLOTS ? (a.tokens + 3) / 4 : SLOTS;
+      for (int e = et; e < a.nA * SLOTS; e += FEPI) {
+        const int kap = e / SLOTS, sl = e % SLOTS;
+        if (sl >= tok_slots) continue;
+        const float4 v = lds128f(slot_addr(kap, sl));
+        red_add_v4(a.t_out + (int64_t)kap * 64 + sl * 4, v.x, v.y, v.z, v.w);
       }
     }
     if (et == 0) TRACE(9);
