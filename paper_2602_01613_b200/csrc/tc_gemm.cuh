@@ -25,6 +25,18 @@ struct TcGemmArgs {
   int32_t out_mode;
 };
 
+// dual_gemm.cu: h (M x N) = silu(T[:, :kg] A_g^T) * (T[:, u_off : u_off + ku] A_u^T), bf16.
+struct DualArgs {
+  int32_t M, N;      // tokens, intermediate width (multiple of 64)
+  int32_t kg, ku;    // contraction lengths (cut ranks, zero-padded by TMA to 64)
+  int32_t u_off;     // column of T where the up block starts
+};
+// t: T map (box {64, 128}); g / u: A_g / A_u maps (box {64, 64}: each CTA of a pair loads half the
+// rows of an output tile); h: output map (box {64, 128}, SW128). 2x1 clusters over token tiles.
+int launch_dual_silu(const CUtensorMap& t, const CUtensorMap& g, const CUtensorMap& u, const CUtensorMap& h,
+                     const DualArgs& a, cudaStream_t st);
+bool dual_silu_ok(const DualArgs& a);  // kg + ku <= 512 (resident T tile), N % 64 == 0
+
 // Encodes a 2-D bf16 K-major tensor map: `rows` rows of `k` elements with a
 // row pitch of `ld` elements, boxes of 64 (K) x box_rows. Returns 0 on success.
 int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t k, int64_t rows, int64_t ld,

@@ -1453,11 +1453,32 @@ struct tnl_mlp {
   tnl_plan* u = nullptr;
   tnl_plan* d = nullptr;
   bool fused = false;
+  bool dual = false;  // gate/up output GEMMs + SiLU*mul in one kernel (ranks the fused path cannot hold)
   int64_t hidden = 0, inter = 0, rg = 0, ru = 0, rd = 0;
   __nv_bfloat16* bgu = nullptr;  // [B_g (rg rows) ; B_u (ru rows)] x hidden
 };
 
 namespace tnl {
+
+// T_gu = x . [B_g; B_u]^T (M x (rg + ru) bf16): the concatenated cut activation of gate and up
+static tnl_status mlp_tgu(tnl_mlp* B, const void* x, int64_t m, int64_t ldx, float* tgu32, __nv_bfloat16* tgu,
+                          cudaStream_t st) {
+  const int64_t rgu = B->rg + B->ru;
+  const int64_t tiles1 = ((m + 127) / 128) * ((rgu + 255) / 256);
+  const int64_t kb = (B->hidden + 63) / 64;
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb / 8));
+  tnl_status s;
+  if (rgu <= 128 && ((m + 127) / 128) * ((rgu + 63) / 64) >= 96) {
+    // enough 64-wide output tiles to fill the SMs: no split-K, bf16 straight from the epilogue
+    return tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st, 64);
+  }
+  if (splits > 1) {
+    if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu32, rgu, true, splits, st))) return s;
+    to_bf16(tgu32, tgu, m * rgu, st);
+    return TNL_OK;
+  }
+  return tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st);
+}
 
 static void mlp_ws_layout(const tnl_mlp* B, int64_t M, size_t off[4], size_t* total) {
   size_t bytes = 0;
@@ -1471,6 +1492,12 @@ static void mlp_ws_layout(const tnl_mlp* B, int64_t M, size_t off[4], size_t* to
     off[1] = take(2 * M * (B->rg + B->ru));              // T_gu bf16
     off[2] = take(sizeof(float) * M * B->rd);            // T_d fp32 (slice reductions)
     off[3] = take(2 * M * B->rd);                        // T_d bf16
+  } else if (B->dual && M > kSwapMaxM) {
+    size_t a, b, c;
+    off[0] = take(ws_layout(B->d, M, &a, &b, &c));       // down's layer workspace
+    off[1] = take(sizeof(float) * M * (B->rg + B->ru));  // T_gu fp32 (split-K)
+    off[2] = take(2 * M * (B->rg + B->ru));              // T_gu bf16
+    off[3] = take(2 * M * B->inter);                     // h
   } else {
     size_t a, b, c, mx = 0;
     for (const tnl_plan* P : {B->g, B->u, B->d}) mx = std::max(mx, ws_layout(P, M, &a, &b, &c));
@@ -1661,7 +1688,17 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
     a.rd = (int32_t)B->rd;
     if (mlp_mid_smem(a) > 227 * 1024) B->fused = false;
   }
-  if (B->fused) {
+  // ranks the on-chip middle kernel cannot hold: gate/up output GEMMs fused with SiLU*mul
+  B->dual = !B->fused && !(flags & 1) && cut(gate) && cut(up) && B->inter % 64 == 0 && B->hidden % 8 == 0;
+  if (B->dual) {
+    DualArgs da;
+    memset(&da, 0, sizeof da);
+    da.N = (int32_t)B->inter;
+    da.kg = (int32_t)gate->r_pad;
+    da.ku = (int32_t)up->r_pad;
+    B->dual = dual_silu_ok(da);
+  }
+  if (B->fused || B->dual) {
     const size_t bytes = 2 * (B->rg + B->ru) * B->hidden;
     CUDA_TRY(cudaMalloc(&B->bgu, bytes));
     CUDA_TRY(cudaMemset(B->bgu, 0, bytes));
@@ -1702,6 +1739,34 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   if (B->fused && prefill && ((reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8 ||
                               (reinterpret_cast<uintptr_t>(x) & 15) || ldx % 8))
     return fail(TNL_ERR_SHAPE, "fused MLP needs 16-byte aligned x/y with row pitches % 8 == 0");
+  if (B->dual && prefill && !((reinterpret_cast<uintptr_t>(x) & 15) || ldx % 8)) {
+    // 1. T_gu = x . [B_g; B_u]^T   2. h = silu(T_g A_g^T) * (T_u A_u^T) in one kernel   3. y = down(h)
+    const int64_t rgu = B->rg + B->ru;
+    void* lws = w + off[0];
+    size_t a_, b_, c_;
+    const size_t lbytes = ws_layout(B->d, m, &a_, &b_, &c_);
+    float* tgu32 = reinterpret_cast<float*>(w + off[1]);
+    __nv_bfloat16* tgu = reinterpret_cast<__nv_bfloat16*>(w + off[2]);
+    __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(w + off[3]);
+    tnl_status s = mlp_tgu(B, x, m, ldx, tgu32, tgu, st);
+    if (s) return s;
+    CUtensorMap tt, tg, tu, th;
+    int err;
+    if ((err = get_tmap(B->g, &tt, tgu, rgu, m, rgu, 128)) ||
+        (err = get_tmap(B->g, &tg, B->g->aout, B->g->r_pad, B->inter, B->g->r_pad, 64)) ||
+        (err = get_tmap(B->u, &tu, B->u->aout, B->u->r_pad, B->inter, B->u->r_pad, 64)) ||
+        (err = get_tmap2(B->g, &th, h, false, B->inter, m, B->inter, 64, 128, 128)))
+      return fail(TNL_ERR_CUDA, "tensor map (MLP dual) failed: %d", err);
+    DualArgs da;
+    da.M = (int32_t)m;
+    da.N = (int32_t)B->inter;
+    da.kg = (int32_t)B->g->r_pad;
+    da.ku = (int32_t)B->u->r_pad;
+    da.u_off = (int32_t)B->rg;
+    if ((err = launch_dual_silu(tt, tg, tu, th, da, st)))
+      return fail(TNL_ERR_CUDA, "MLP dual kernel launch: %s", cudaGetErrorString((cudaError_t)err));
+    return tnl_forward(B->d, h, m, B->inter, y, ldy, lws, lbytes, stream);
+  }
   if (!B->fused || !prefill) {
     // unfused: three layer forwards + a SiLU*mul kernel
     void* lws = w + off[0];
@@ -1723,18 +1788,7 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   __nv_bfloat16* td = reinterpret_cast<__nv_bfloat16*>(w + off[3]);
   tnl_status s;
   // 1. T_gu = x . [B_g; B_u]^T
-  const int64_t tiles1 = ((m + 127) / 128) * ((rgu + 255) / 256);
-  const int64_t kb = (B->hidden + 63) / 64;
-  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb / 8));
-  if (((m + 127) / 128) * ((rgu + 63) / 64) >= 96) {
-    // enough 64-wide output tiles to fill the SMs: no split-K, bf16 straight from the epilogue
-    if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st, 64))) return s;
-  } else if (splits > 1) {
-    if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu32, rgu, true, splits, st))) return s;
-    to_bf16(tgu32, tgu, m * rgu, st);
-  } else if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st))) {
-    return s;
-  }
+  if ((s = mlp_tgu(B, x, m, ldx, tgu32, tgu, st))) return s;
   // 2. T_d = (silu(T_g A_g^T) * (T_u A_u^T)) B_d^T, h on chip
   MlpArgs a;
   memset(&a, 0, sizeof a);

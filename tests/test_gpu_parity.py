@@ -397,3 +397,22 @@ def test_mlp_kernel_variants(rg, rd, variant):
     y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
     torch.cuda.synchronize()
     assert rel(_mlp_ref(Lgr, Lur, Ldr, x), y.float().cpu().numpy()) <= 2 * BF16_TOL
+
+
+@pytest.mark.parametrize("rg,rd,m", [(256, 256, 300), (256, 64, 129), (192, 128, 300), (256, 256, 5)])
+def test_mlp_dual_path(rg, rd, m):
+    """Ranks the on-chip middle kernel cannot hold: gate/up output GEMMs + SiLU*mul in one kernel
+    (csrc/dual_gemm.cu), then the down layer; M = 5 takes the decode path (three layers)."""
+    from paper_2602_01613_b200.mlp import TNMLP
+
+    hid, inter = 512, 1024 + 64  # intermediate not a multiple of the 128-wide tile
+    Lg = O.synthetic_layer("tucker", (inter, hid), 1, (rg, rg), seed=53_001)
+    Lu = O.synthetic_layer("tucker", (inter, hid), 1, (rg, rg), seed=53_002)
+    Ld = O.synthetic_layer("tucker", (hid, inter), 1, (rd, rd), seed=53_003)
+    (g, Lgr), (u, Lur), (d, Ldr) = (to_layer(L, round_bf16=True) for L in (Lg, Lu, Ld))
+    mlp = TNMLP(g, u, d)
+    assert not mlp.fused
+    x = O.round_bf16(O.synthetic_x(m, hid, seed=53_004))
+    y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
+    torch.cuda.synchronize()
+    assert rel(_mlp_ref(Lgr, Lur, Ldr, x), y.float().cpu().numpy()) <= 2 * BF16_TOL
