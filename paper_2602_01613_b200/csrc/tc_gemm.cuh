@@ -58,4 +58,9 @@ int launch_tc_gemm_persistent(const CUtensorMap& a, const CUtensorMap& b, const 
                               const TcGemmArgs& args, int bn, int splits, int max_ctas, bool pdl,
                               cudaStream_t st);
 
+// CTA-pair variant (tc_gemm_pair.cu): 256 x bn tiles over 2x1 clusters, bn in {128, 256};
+// `b` must be a map with box {64, bn / 2} (each CTA loads half of the B tile).
+int launch_tc_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcGemmArgs& args,
+                        int bn, int splits, cudaStream_t st);
+
 }  // namespace tnl

@@ -1285,7 +1285,17 @@ static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void*
     if ((err = get_tmap2(P, &tc, out, false, N, M, ldo, 64, 128, 128)))
       return fail(TNL_ERR_CUDA, "tensor map (output) failed: %d", err);
   }
-  err = launch_tc_gemm_persistent(ta, tb, tc, a, bn, splits, 148, true, st);
+  // CTA pairs (M=256 MMAs, each CTA streams half of the weight tile) once there are two token
+  // tiles and a wide enough weight tile; TNL_PAIR_GEMM=0 disables
+  static const bool pair_env = !(getenv("TNL_PAIR_GEMM") && atoi(getenv("TNL_PAIR_GEMM")) == 0);
+  if (pair_env && M >= 256 && bn == 256) {
+    CUtensorMap tbh;
+    if ((err = get_tmap(P, &tbh, W, K, N, ldw, bn / 2)))
+      return fail(TNL_ERR_CUDA, "tensor map (pair step) failed: %d", err);
+    err = launch_tc_gemm_pair(ta, tbh, tc, a, bn, splits, st);
+  } else {
+    err = launch_tc_gemm_persistent(ta, tb, tc, a, bn, splits, 148, true, st);
+  }
   if (err) return fail(TNL_ERR_CUDA, "persistent gemm launch: %s", cudaGetErrorString((cudaError_t)err));
   return TNL_OK;
 }
