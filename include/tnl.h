@@ -194,6 +194,12 @@ TNL_API tnl_status tnl_jacobi_sweeps(double* work, double* rot, int64_t batch, i
                                      int64_t nv, double tol, int32_t max_sweeps, int32_t* sweeps,
                                      void* stream);
 
+/* Decoder-stack plumbing (not part of the reference's TN path; used by the Qwen3 stack driver):
+ * x <- x + o (skipped when o == NULL), h <- x / sqrt(mean(x^2) + eps) per row, bf16 [m][n]
+ * with row pitches ldx / ldo / ldh (multiples of 8), n % 8 == 0, n <= 8192. One pass. */
+TNL_API tnl_status tnl_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, void* h, int64_t ldh,
+                                   int64_t m, int64_t n, float eps, void* stream);
+
 /* Number of libtnl kernel launches issued by this thread since the last reset
  * (evidence counter for benchmarks). */
 TNL_API int64_t tnl_launch_count(int32_t reset);

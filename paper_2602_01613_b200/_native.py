@@ -38,6 +38,7 @@ EXPORTED = (
     "tnl_launch_count",
     "tnl_plan_set_trace",
     "tnl_jacobi_sweeps",
+    "tnl_add_rmsnorm",
     "tnl_stack_workspace_size",
     "tnl_stack_forward",
     "tnl_mlp_create",
@@ -133,6 +134,8 @@ def load():
         lib.tnl_plan_set_trace.restype = ctypes.c_int
         lib.tnl_jacobi_sweeps.argtypes = [P, P, i64, i64, i64, i64, ctypes.c_double, ctypes.c_int32, P, P]
         lib.tnl_jacobi_sweeps.restype = ctypes.c_int
+        lib.tnl_add_rmsnorm.argtypes = [P, i64, P, i64, P, i64, i64, i64, ctypes.c_float, P]
+        lib.tnl_add_rmsnorm.restype = ctypes.c_int
         lib.tnl_launch_count.argtypes = [ctypes.c_int32]
         lib.tnl_launch_count.restype = i64
         for name in ("tnl_plan_create", "tnl_plan_create_rows", "tnl_plan_destroy", "tnl_plan_query",

@@ -10,6 +10,10 @@ namespace tnl {
 void count_launch(int64_t n = 1);
 int64_t launch_count(bool reset);
 
+// rmsnorm.cu: x += o (o may be NULL); h = x / rms(x)   (decoder-stack plumbing)
+int launch_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, void* h, int64_t ldh, int64_t m, int64_t n,
+                       float eps, cudaStream_t st);
+
 // jacobi.cu: batched one-sided Jacobi sweeps (tnl_jacobi_sweeps)
 int launch_jacobi_sweeps(double* work, double* rot, int64_t batch, int n, int m, int nv, double tol, int max_sweeps,
                          int32_t* sweeps, cudaStream_t st);

@@ -1052,6 +1052,8 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
 // ---------------------------------------------------------------------------
 static constexpr int64_t kSwapMaxM = 64;  // tokens: swap-AB (weights on the M side) below this
 
+constexpr size_t kDecHeadBytes = sizeof(float) * 64 * 256;  // decode accumulator (r_pad <= 256)
+
 static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b0, size_t* o_b1) {
   size_t bytes = 0;
   auto take = [&](size_t n) {
@@ -1067,11 +1069,14 @@ static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b
     *o_f32 = (rows_local != P->rows) ? take(sizeof(float) * M * P->rows) : 0;
     return bytes;
   }
-  // decode accumulator + counter (zero at rest: the caller zero-fills the workspace once)
-  if (P->decode_max_m) {
-    take(sizeof(float) * 64 * P->r_pad);
-    take(256);
-  }
+  // decode accumulator + counter (zero at rest: the caller zero-fills the workspace once). The
+  // head has the same size for every decode-capable plan (the 64 x 256 fp32 maximum) so plans
+  // sharing one workspace (stacks, MLP blocks) never place scratch inside another plan's
+  // zero-at-rest accumulator.
+  // (reserved even by plans without a decode path, whose prefill scratch would otherwise land
+  // in the head of a decode-capable plan sharing the workspace)
+  take(kDecHeadBytes);
+  take(256);
   int64_t kmax = P->r_pad;
   if (P->tucker_chain) kmax = std::max(P->r0p, P->r1p);
   *o_f32 = take(sizeof(float) * M * kmax);
@@ -1183,14 +1188,13 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
                                  int64_t ldy, void* ws, cudaStream_t st) {
   // decode accumulator (64 x r_pad fp32, zero at rest) and counter live at the workspace head
   float* tacc = static_cast<float*>(ws);
-  unsigned int* counter =
-      reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + round_up(sizeof(float) * 64 * P->r_pad, 256));
+  unsigned int* counter = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + kDecHeadBytes);
   const int64_t rows_local = P->row_end - P->row_begin;
   int err = 0;
   const bool use_chain = P->plan_large == TNL_PLAN_CHAIN && P->chain_ok;
   if (M <= 8 && !use_chain && (P->flags & TNL_PLAN_GEMV)) {
     // CUDA-core GEMV variant; T goes to the (non-accumulating) scratch after the accumulator
-    float* t = reinterpret_cast<float*>(static_cast<char*>(ws) + round_up(sizeof(float) * 64 * P->r_pad, 256) + 256);
+    float* t = reinterpret_cast<float*>(static_cast<char*>(ws) + kDecHeadBytes + 256);
     err = launch_gemv_a(P->bin, P->cols, (int)P->r_pad, (int)P->cols, static_cast<const __nv_bfloat16*>(x), ldx,
                         (int)M, t, P->r_pad, st);
     if (err) return fail(TNL_ERR_CUDA, "gemv_a launch: %s", cudaGetErrorString((cudaError_t)err));
@@ -1497,7 +1501,10 @@ static void mlp_ws_layout(const tnl_mlp* B, int64_t M, size_t off[4], size_t* to
     bytes += round_up((int64_t)n, 256);
     return o;
   };
+  // every layout keeps the decode head (zero-at-rest accumulators of the three layers' decode
+  // calls, and of any other plan sharing the workspace) untouched
   if (B->fused && M > kSwapMaxM) {
+    take(kDecHeadBytes + 256);
     off[0] = take(sizeof(float) * M * (B->rg + B->ru));  // T_gu fp32 (split-K)
     off[1] = take(2 * M * (B->rg + B->ru));              // T_gu bf16
     off[2] = take(sizeof(float) * M * B->rd);            // T_d fp32 (slice reductions)
@@ -1842,6 +1849,17 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   to_bf16(td32, td, m * B->rd, st);
   // 3. y = T_d . A_d^T
   return tc_step_p(B->d, td, B->rd, B->d->aout, B->d->r_pad, m, B->hidden, B->d->r_pad, y, ldy, false, 1, st);
+}
+
+tnl_status tnl_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, void* h, int64_t ldh, int64_t m,
+                           int64_t n, float eps, void* stream) {
+  if (!x || !h) return fail(TNL_ERR_ARG, "null argument");
+  if (m < 0 || n <= 0 || n % 8 || n > 8192 || ldx % 8 || ldh % 8 || (o && ldo % 8))
+    return fail(TNL_ERR_SHAPE, "add_rmsnorm: m=%lld n=%lld (n % 8 == 0, n <= 8192, pitches % 8 == 0)",
+                (long long)m, (long long)n);
+  const int err = launch_add_rmsnorm(x, ldx, o, ldo, h, ldh, m, n, eps, static_cast<cudaStream_t>(stream));
+  if (err) return fail(TNL_ERR_CUDA, "add_rmsnorm launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
 }
 
 tnl_status tnl_jacobi_sweeps(double* work, double* rot, int64_t batch, int64_t n, int64_t m, int64_t nv, double tol,

@@ -15,14 +15,19 @@ output is taken to be q). Pre-norm as in Qwen3 (RMSNorm without learned scale), 
   h = rms(x); x = x + Ld(silu(Lg(h)) * Lu(h))
 The projections run through libtnl (tnl_forward); the MLP half runs as one ``TNMLP`` block
 (tnl_mlp_forward: gate/up/SiLU*mul/down fused with h on chip for prefill-sized M and
-merged-cut ranks <= 128, else three layers around a SiLU*mul kernel); residual adds are torch
-element-wise plumbing. ``capture(m)`` records one whole pass into a CUDA graph.
+merged-cut ranks <= 128, the dual gate/up kernel for larger ranks, else three layers around a
+SiLU*mul kernel); each residual add is fused with the next RMSNorm into one pass
+(``tnl_add_rmsnorm``: x += o; h = rms(x)). All plans and MLP blocks share one workspace.
+``capture(m)`` records one whole pass into a CUDA graph.
 """
 
 from __future__ import annotations
 
 import torch
 
+import ctypes
+
+from . import _native as N
 from . import synthetic as S
 from .mlp import TNMLP
 from .modes import default_mode_shape
@@ -99,22 +104,31 @@ class QwenTNStack:
         mk = lambda n: torch.empty((m, n), dtype=self.dtype, device=self.device)  # noqa: E731
         return {"h": mk(HIDDEN), "q": mk(QDIM), "k": mk(KVDIM), "v": mk(KVDIM), "o": mk(HIDDEN), "d": mk(HIDDEN)}
 
+    @staticmethod
+    def add_rmsnorm(x: torch.Tensor, o, h: torch.Tensor, eps: float = 1e-6) -> None:
+        """x += o (if o is not None); h = x / rms(x) — one pass (tnl_add_rmsnorm)."""
+        m, n = x.shape
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        optr = ctypes.c_void_p(o.data_ptr()) if o is not None else None
+        N.check(N.load().tnl_add_rmsnorm(ctypes.c_void_p(x.data_ptr()), x.stride(0), optr,
+                                         o.stride(0) if o is not None else 0, ctypes.c_void_p(h.data_ptr()),
+                                         h.stride(0), m, n, float(eps), ctypes.c_void_p(stream)))
+
     def forward(self, x: torch.Tensor, bufs=None) -> torch.Tensor:
         """One pass of all layers; x (M x 5120) is updated in place (residual stream)."""
         m = x.shape[0]
         ws = self.workspace(m)
         b = bufs or self._buffers(m)
-        rms = lambda t: torch.nn.functional.rms_norm(t, (HIDDEN,), eps=1e-6)  # noqa: E731
-        for blk in self.layers:
-            b["h"].copy_(rms(x))
+        for li, blk in enumerate(self.layers):
+            # x += previous MLP output; h = rms(x)   (fused residual add + RMSNorm, one pass)
+            self.add_rmsnorm(x, b["d"] if li else None, b["h"])
             blk["q"][2].forward(b["h"], out=b["q"], ws=ws)
             blk["k"][2].forward(b["h"], out=b["k"], ws=ws)
             blk["v"][2].forward(b["h"], out=b["v"], ws=ws)
             blk["o"][2].forward(b["q"], out=b["o"], ws=ws)  # attention core: pass-through
-            x.add_(b["o"])
-            b["h"].copy_(rms(x))
+            self.add_rmsnorm(x, b["o"], b["h"])
             blk["mlp"].forward(b["h"], out=b["d"], ws=ws)
-            x.add_(b["d"])
+        x.add_(b["d"])
         return x
 
     def capture(self, m: int):

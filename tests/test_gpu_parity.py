@@ -416,3 +416,37 @@ def test_mlp_dual_path(rg, rd, m):
     y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
     torch.cuda.synchronize()
     assert rel(_mlp_ref(Lgr, Lur, Ldr, x), y.float().cpu().numpy()) <= 2 * BF16_TOL
+
+
+@pytest.mark.parametrize("m,n,with_o", [(1, 5120, True), (300, 5120, True), (17, 1024, False), (64, 8192, True)])
+def test_add_rmsnorm(m, n, with_o):
+    """Stack plumbing: x += o; h = x / rms(x) (one pass) vs torch (fp32 reference on the bf16 sum)."""
+    from paper_2602_01613_b200.qwen_stack import QwenTNStack
+
+    torch.manual_seed(m + n)
+    x = torch.randn(m, n, device=DEV).to(torch.bfloat16)
+    o = torch.randn(m, n, device=DEV).to(torch.bfloat16) if with_o else None
+    ref_x = (x.float() + o.float()).to(torch.bfloat16) if with_o else x.clone()
+    ref_h = torch.nn.functional.rms_norm(ref_x.float(), (n,), eps=1e-6)
+    h = torch.empty_like(x)
+    QwenTNStack.add_rmsnorm(x, o, h)
+    torch.cuda.synchronize()
+    assert torch.equal(x, ref_x)
+    assert rel(ref_h.cpu().numpy(), h.float().cpu().numpy()) <= 1e-2
+
+
+def test_qwen_stack_decode_matches_prefill():
+    """Regression: every plan and MLP block of a stack share one workspace; decode (M <= 64) must
+    give the same tokens as the prefill path (per-token independence), which failed when an MLP's
+    scratch overlapped a wider plan's zero-at-rest decode accumulator."""
+    from paper_2602_01613_b200.qwen_stack import QwenTNStack
+
+    st = QwenTNStack(8)
+    torch.manual_seed(3)
+    x = (0.5 * torch.randn(300, 5120, device=DEV)).to(torch.bfloat16)
+    xp, xd = x.clone(), x[:64].clone()
+    st.forward(xp)
+    st.forward(xd)
+    torch.cuda.synchronize()
+    assert torch.isfinite(xd.float()).all()
+    assert rel(xp[:64].float().cpu().numpy(), xd.float().cpu().numpy()) <= 2 * BF16_TOL
