@@ -450,3 +450,17 @@ def test_qwen_stack_decode_matches_prefill():
     torch.cuda.synchronize()
     assert torch.isfinite(xd.float()).all()
     assert rel(xp[:64].float().cpu().numpy(), xd.float().cpu().numpy()) <= 2 * BF16_TOL
+
+
+@pytest.mark.parametrize("spec", [("tucker", (5120, 5120), 1, (256, 256)), ("tr", (5120, 5120), 1, (16, 16)),
+                                  ("tucker", (8192, 5120), 1, (256, 256))])
+@pytest.mark.parametrize("m", [256, 300, 600])
+def test_prefill_pair_gemm(spec, m):
+    """Rank-256 prefill steps take the CTA-pair GEMM (csrc/tc_gemm_pair.cu): 256-row tiles, an odd
+    token-tile count (300: the pair's second tile is past M) and split-K (600: step 1 reduces in
+    fp32 over K-splits), vs the oracle; plus the chain plan (three Tucker-2 steps)."""
+    fam, ms, rm, ranks = spec
+    L = O.synthetic_layer(fam, ms, rm, ranks, seed=54_000 + m)
+    check_bf16(L, m, seed=54_100 + m)
+    if fam == "tucker":
+        check_bf16(L, m, seed=54_200 + m, flags=tnl.PLAN_CHAIN)
