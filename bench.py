@@ -390,6 +390,44 @@ def main():
                               "plan": pl.info["plan_large_name"]}
             del xs, yp
 
+    # secondary: cfg1 (BASELINE configs[0]) TT (64,64|64,64) r32, M=16 — fp32 generic chain (the
+    # reference-precision path, CUDA-core bound) and bf16 plans; 8 distinct layers (> L2? no: 2 MB)
+    cfg1 = None
+    if not args.no_prefill:
+        cfg1 = {}
+        lays = [S.make_layer("tt", (64, 64, 64, 64), 2, (32, 32, 32), seed=10_000 + 100 * i) for i in range(8)]
+        x16 = torch.randn(16, 4096, device="cuda")
+        props = torch.cuda.get_device_properties(0)
+        clk_ghz = (clocks or {}).get("sm_max_mhz", 1965.0) / 1e3
+        fp32_peak = props.multi_processor_count * 128 * 2 * clk_ghz / 1e3  # TFLOP/s (FFMA)
+        for dt, name in ((torch.float32, "fp32"), (torch.bfloat16, "bf16")):
+            pls = [l.plan(dt) for l in lays]
+            xs = x16.to(dt)
+            wss = [p.workspace(16) for p in pls]
+            outs = [torch.empty(16, 4096, device="cuda", dtype=dt) for _ in pls]
+
+            def c1():
+                for p, w_, o_ in zip(pls, wss, outs):
+                    p.forward(xs, out=o_, ws=w_)
+
+            s1 = torch.cuda.Stream()
+            s1.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s1):
+                c1()
+            torch.cuda.current_stream().wait_stream(s1)
+            g1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1, stream=s1):
+                c1()
+            ms1 = time_graph(g1.replay, 200, 10, torch, None) / len(lays)
+            c1_bytes = (4 if dt == torch.float32 else 2) * (tnl.param_count(lays[0]) + 16 * 8192)
+            c1_flops = 16 * lays[0].chain_flops_per_token()
+            peak_t = fp32_peak if dt == torch.float32 else tc
+            c1_troof = max(c1_bytes / (hbm * 1e9), c1_flops / (peak_t * 1e12))
+            cfg1[name] = {"us_per_layer": 1e3 * ms1, "tokens_per_s": 16 / (ms1 / 1e3), "chain_TFLOPs": c1_flops / (ms1 / 1e3) / 1e12,
+                          "frac_roofline": c1_troof / (ms1 / 1e3), "roofline_peak": (f"fp32 CUDA-core {fp32_peak:.1f} TFLOP/s"
+                                                                                   if name == "fp32" else "bf16 tensor / HBM"),
+                          "plan": pls[0].info["plan_small_name"]}
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         times, names = cpu_reference_sample(M, 7)
@@ -439,6 +477,7 @@ def main():
         "speedup_vs_dense": (value / dense["value"]) if dense else None,
         "breakdown": breakdown,
         "prefill_cfg3": prefill,
+        "cfg1_m16": cfg1,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -23,6 +23,7 @@ from .layer import (
     NativePlan,
     apply_compressed,
     compression_ratio,
+    from_compressed_layer,
     layer_to_matrix,
     param_count,
     reconstruct,
@@ -35,6 +36,7 @@ __all__ = [
     "NativePlan",
     "apply_compressed",
     "compression_ratio",
+    "from_compressed_layer",
     "layer_to_matrix",
     "param_count",
     "param_count_formula",

@@ -24,9 +24,11 @@ __device__ __forceinline__ float ld_as_float<__nv_bfloat16>(const __nv_bfloat16*
   return __bfloat162float(*p);
 }
 
+// grid.x = output tiles (x batch), grid.y = K-splits: split z reduces p in [z * pspan, (z+1) * pspan)
+// and, when gridDim.y > 1, adds its partial with fp32 atomics into a pre-zeroed (or accumulating) C
 template <typename TA, typename TB, typename TC>
 __global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tiles_i,
-                                                           int64_t tiles_j) {
+                                                           int64_t tiles_j, int64_t pspan) {
   __shared__ float sA[TP][TI + 4];
   __shared__ float sB[TP][TJ + 4];
   const int64_t tile = blockIdx.x;
@@ -47,7 +49,8 @@ __global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tile
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
 
-  for (int64_t p0 = 0; p0 < s.P; p0 += TP) {
+  const int64_t pbeg = blockIdx.y * pspan, pend = min(s.P, pbeg + pspan);
+  for (int64_t p0 = pbeg; p0 < pend; p0 += TP) {
     // A tile: TI x TP, B tile: TP x TJ  (256 threads, 4 elements each)
     for (int e = threadIdx.x; e < TI * TP; e += 256) {
       int ii, pp;
@@ -59,7 +62,7 @@ __global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tile
         pp = e / TI;
       }
       const int64_t gi = i0 + ii, gp = p0 + pp;
-      sA[pp][ii] = (gi < s.I && gp < s.P) ? ld_as_float(A + gi * s.sai + gp * s.sap) : 0.f;
+      sA[pp][ii] = (gi < s.I && gp < pend) ? ld_as_float(A + gi * s.sai + gp * s.sap) : 0.f;
     }
     for (int e = threadIdx.x; e < TP * TJ; e += 256) {
       int jj, pp;
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tile
         jj = e / TP;
       }
       const int64_t gj = j0 + jj, gp = p0 + pp;
-      sB[pp][jj] = (gj < s.J && gp < s.P) ? ld_as_float(B + gp * s.sbp + gj * s.sbj) : 0.f;
+      sB[pp][jj] = (gj < s.J && gp < pend) ? ld_as_float(B + gp * s.sbp + gj * s.sbj) : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -99,7 +102,9 @@ __global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tile
       if (gj >= s.J) continue;
       TC* dst = C + gi * s.sci + gj * s.scj;
       if constexpr (sizeof(TC) == 4) {
-        if (s.accumulate)
+        if (gridDim.y > 1)
+          atomicAdd(dst, acc[x][y]);
+        else if (s.accumulate)
           *dst += acc[x][y];
         else
           *dst = acc[x][y];
@@ -110,21 +115,30 @@ __global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tile
   }
 }
 
+__global__ void zero_strided_kernel(float* C, GStep s) {
+  const int64_t n = s.b1 * s.b2 * s.I * s.J;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e % s.J, i = (e / s.J) % s.I, bb = e / (s.J * s.I);
+    C[(bb / s.b2) * s.sc1 + (bb % s.b2) * s.sc2 + i * s.sci + j * s.scj] = 0.f;
+  }
+}
+
 template <typename TA, typename TB>
-int launch_c(const GStep& s, int64_t tiles_i, int64_t tiles_j, int64_t blocks, cudaStream_t st) {
+int launch_c(const GStep& s, int64_t tiles_i, int64_t tiles_j, int64_t blocks, int64_t splits, cudaStream_t st) {
+  const int64_t pspan = (s.P + splits - 1) / splits;
+  const dim3 grid((unsigned)blocks, (unsigned)splits, 1);
   if (s.c_dt == DT_F32)
-    generic_step_kernel<TA, TB, float><<<(unsigned)blocks, 256, 0, st>>>(s, tiles_i, tiles_j);
+    generic_step_kernel<TA, TB, float><<<grid, 256, 0, st>>>(s, tiles_i, tiles_j, pspan);
   else
-    generic_step_kernel<TA, TB, __nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(s, tiles_i,
-                                                                                 tiles_j);
+    generic_step_kernel<TA, TB, __nv_bfloat16><<<grid, 256, 0, st>>>(s, tiles_i, tiles_j, pspan);
   count_launch();
   return (int)cudaGetLastError();
 }
 
 template <typename TA>
-int launch_b(const GStep& s, int64_t ti, int64_t tj, int64_t blocks, cudaStream_t st) {
-  if (s.b_dt == DT_F32) return launch_c<TA, float>(s, ti, tj, blocks, st);
-  return launch_c<TA, __nv_bfloat16>(s, ti, tj, blocks, st);
+int launch_b(const GStep& s, int64_t ti, int64_t tj, int64_t blocks, int64_t splits, cudaStream_t st) {
+  if (s.b_dt == DT_F32) return launch_c<TA, float>(s, ti, tj, blocks, splits, st);
+  return launch_c<TA, __nv_bfloat16>(s, ti, tj, blocks, splits, st);
 }
 
 }  // namespace
@@ -146,8 +160,20 @@ int launch_generic_step(const GStep& in, cudaStream_t stream) {
   const int64_t tiles_i = (s.I + TI - 1) / TI, tiles_j = (s.J + TJ - 1) / TJ;
   const int64_t blocks = tiles_i * tiles_j * s.b1 * s.b2;
   if (blocks > 0x7fffffffLL) return (int)cudaErrorInvalidConfiguration;
-  if (s.a_dt == DT_F32) return launch_b<float>(s, tiles_i, tiles_j, blocks, stream);
-  return launch_b<__nv_bfloat16>(s, tiles_i, tiles_j, blocks, stream);
+  // few output tiles and a long contraction (e.g. cfg1's T = C . t1 step: one 64x64 tile, P = 2048):
+  // split P over CTAs and reduce with fp32 atomics (fp32 C only; summation order changes, the
+  // exactness contract is fp32 rounding, not bitwise)
+  int64_t splits = 1;
+  if (s.c_dt == DT_F32 && blocks < 148 && s.P >= 4 * TP * 2)
+    splits = std::max<int64_t>(1, std::min<int64_t>((2 * 148 + blocks - 1) / blocks, s.P / (4 * TP)));
+  if (splits > 1 && !s.accumulate) {
+    const int64_t n = s.b1 * s.b2 * s.I * s.J;
+    zero_strided_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, stream>>>(
+        static_cast<float*>(s.C), s);
+    count_launch();
+  }
+  if (s.a_dt == DT_F32) return launch_b<float>(s, tiles_i, tiles_j, blocks, splits, stream);
+  return launch_b<__nv_bfloat16>(s, tiles_i, tiles_j, blocks, splits, stream);
 }
 
 }  // namespace tnl

@@ -227,6 +227,7 @@ class NativePlan:
         N.check(self.lib.tnl_plan_query(self.handle, ctypes.byref(info)))
         self.info = {f: getattr(info, f) for f, _ in N.PlanInfo._fields_}
         self.info["plan_large_name"] = N.PLAN_NAMES.get(info.plan_large, str(info.plan_large))
+        self.info["plan_small_name"] = N.PLAN_NAMES.get(info.plan_small, str(info.plan_small))
         self.rows_local = info.row_end - info.row_begin
         self._ws = None
 
@@ -298,6 +299,16 @@ class NativePlan:
 
 
 # --- module functions (reference API) ------------------------------------------
+
+
+def from_compressed_layer(ref_layer) -> CompressedLayer:
+    """Adapter from a reference ``minima.tn_decompositions.CompressedLayer`` (`:66-80`), or any
+    object with the same fields, to this package's layer. Arrays are taken by
+    reference, as the reference does; validation runs with the reference's messages."""
+    return CompressedLayer(
+        str(ref_layer.family), tuple(int(s) for s in ref_layer.mode_shape), int(ref_layer.row_mode_count),
+        matrix=getattr(ref_layer, "matrix", None), core=getattr(ref_layer, "core", None),
+        factors=list(getattr(ref_layer, "factors", None) or []), cores=list(getattr(ref_layer, "cores", None) or []))
 
 
 def reconstruct(layer: CompressedLayer, dtype=None, device=None):

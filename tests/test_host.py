@@ -88,3 +88,31 @@ def test_flop_accounting_matches_oracle():
         layer = tnl.CompressedLayer(fam, ms, rm, core=L.core, factors=L.factors, cores=L.cores)
         assert layer.chain_flops_per_token() == O.chain_flops_per_token(L)
         assert layer.cut_rank == O.cut_rank(L)
+
+
+def test_from_compressed_layer_adapter(golden):
+    """a reference-shaped layer object (same fields as
+    minima.tn_decompositions.CompressedLayer, tn_decompositions.py:66-80) converts 1:1."""
+    from dataclasses import dataclass, field
+
+    @dataclass
+    class RefLayer:  # the reference dataclass's field set
+        family: str
+        mode_shape: tuple
+        row_mode_count: int
+        matrix: object = None
+        core: object = None
+        factors: list = field(default_factory=list)
+        cores: list = field(default_factory=list)
+
+    index, arrays = golden
+    for rec in index["forward"]:
+        kw = golden_layer_kwargs(rec, arrays)
+        ref = RefLayer(**kw)
+        layer = tnl.from_compressed_layer(ref)
+        assert (layer.family, layer.mode_shape, layer.row_mode_count) == (ref.family, tuple(ref.mode_shape),
+                                                                          ref.row_mode_count)
+        assert layer.ranks == tnl.CompressedLayer(**kw).ranks
+        assert tnl.param_count(layer) == O.param_count(O.OracleLayer(**kw))
+    with pytest.raises(tnl.ShapeError):
+        tnl.from_compressed_layer(RefLayer("tt", (4, 4), 1, cores=[np.zeros((1, 4, 2)), np.zeros((3, 4, 1))]))
