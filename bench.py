@@ -48,7 +48,7 @@ def peaks():
 # ---------------------------------------------------------------------------
 
 
-def cpu_reference_sample(m: int, steps: int, variants=None):
+def cpu_reference_sample(m: int, steps: int, variants=None, chain: bool = False):
     """Time the reference algorithm on host cores; one cfg2 layer per step, cycling variants.
 
     The reference's only forward is ``layer_to_matrix(L) @ x`` (tn_decompositions.py:364-365,
@@ -75,7 +75,7 @@ def cpu_reference_sample(m: int, steps: int, variants=None):
     for i in range(steps):
         name, L = layers[i % len(layers)]
         t0 = time.perf_counter()
-        y = O.apply_reference(L, x)
+        y = O.apply_chain(L, x) if chain else O.apply_reference(L, x)
         times.append(time.perf_counter() - t0)
         names.append(name)
         assert y.shape == (5120, m)
@@ -431,7 +431,11 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu:
         times, names = cpu_reference_sample(M, 7)
+        ctimes, _ = cpu_reference_sample(M, 7, chain=True)
         cpu = {"value": M * len(times) / sum(times), "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+               "chain_path": {"value": M * len(ctimes) / sum(ctimes), "unit": "tokens/s",
+                              "what": "reference-semantics core-by-core chain (SURVEY Appendix A) in float64, "
+                                      "same layers and threads (SURVEY 8(d) CPU row ii)"},
                "sample": f"one layer of each of the 7 cfg2 variants at M={M}, reference algorithm "
                          "layer_to_matrix(L) @ x in float64 (oracle port), numpy/OpenBLAS threads",
                "per_variant_s": {n: t for n, t in zip(names, times)}}
