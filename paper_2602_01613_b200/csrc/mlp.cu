@@ -873,7 +873,8 @@ int launch_mlp_mid(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMa
 namespace tnl {
 
 bool mlp_pair_ok(const MlpArgs& a) {
-  if (getenv("TNL_MLP_NOPAIR")) return false;
+  static const bool nopair = getenv("TNL_MLP_NOPAIR") != nullptr;  // A/B switch for measurements
+  if (nopair) return false;
   const MlpPairLayout L = mlp_pair_layout(a);
   return L.nb >= 2 && L.total <= 227 * 1024 && a.rg % 64 == 0 && a.ru % 64 == 0 && a.rd % 64 == 0 &&
          a.rg <= 128 && a.ru <= 128 && a.rd <= 256 && a.inter % CH == 0;

@@ -1836,7 +1836,8 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
       const int64_t cost = waves * ((nchunks + s - 1) / s + 4);
       if (cost < best) best = cost, slices = (int)s;
     }
-    if (const char* e = getenv("TNL_MLP_SLICES")) slices = std::max(1, atoi(e));
+    static const int env_slices = getenv("TNL_MLP_SLICES") ? atoi(getenv("TNL_MLP_SLICES")) : 0;  // A/B switch
+    if (env_slices > 0) slices = env_slices;
   }
   a.chunks_per_slice = (int32_t)((nchunks + slices - 1) / slices);
   slices = (int)((nchunks + a.chunks_per_slice - 1) / a.chunks_per_slice);
