@@ -1053,6 +1053,12 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
 static constexpr int64_t kSwapMaxM = 64;  // tokens: swap-AB (weights on the M side) below this
 
 constexpr size_t kDecHeadBytes = sizeof(float) * 64 * 256;  // decode accumulator (r_pad <= 256)
+// one decode slot = accumulator + counter + the GEMV variant's T scratch (M <= 8, r_pad <= 256).
+// Every workspace layout reserves kDecSlots slots at fixed offsets, so a decode call may run on
+// slot 1 (a forked stream) concurrently with one on slot 0 (MLP gate || up) and no layout ever
+// places scratch inside a zero-at-rest accumulator.
+constexpr size_t kDecSlotBytes = kDecHeadBytes + 256 + sizeof(float) * 8 * 256;
+constexpr int kDecSlots = 2;
 
 static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b0, size_t* o_b1) {
   size_t bytes = 0;
@@ -1075,8 +1081,7 @@ static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b
   // zero-at-rest accumulator.
   // (reserved even by plans without a decode path, whose prefill scratch would otherwise land
   // in the head of a decode-capable plan sharing the workspace)
-  take(kDecHeadBytes);
-  take(256);
+  take(kDecSlots * kDecSlotBytes);
   int64_t kmax = P->r_pad;
   if (P->tucker_chain) kmax = std::max(P->r0p, P->r1p);
   *o_f32 = take(sizeof(float) * M * kmax);
@@ -1470,6 +1475,9 @@ struct tnl_mlp {
   bool dual = false;  // gate/up output GEMMs + SiLU*mul in one kernel (ranks the fused path cannot hold)
   int64_t hidden = 0, inter = 0, rg = 0, ru = 0, rd = 0;
   __nv_bfloat16* bgu = nullptr;  // [B_g (rg rows) ; B_u (ru rows)] x hidden
+  // decode: up runs on a forked stream (workspace slot 1) concurrently with gate (slot 0)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace tnl {
@@ -1504,7 +1512,7 @@ static void mlp_ws_layout(const tnl_mlp* B, int64_t M, size_t off[4], size_t* to
   // every layout keeps the decode head (zero-at-rest accumulators of the three layers' decode
   // calls, and of any other plan sharing the workspace) untouched
   if (B->fused && M > kSwapMaxM) {
-    take(kDecHeadBytes + 256);
+    take(kDecSlots * kDecSlotBytes);
     off[0] = take(sizeof(float) * M * (B->rg + B->ru));  // T_gu fp32 (split-K)
     off[1] = take(2 * M * (B->rg + B->ru));              // T_gu bf16
     off[2] = take(sizeof(float) * M * B->rd);            // T_d fp32 (slice reductions)
@@ -1715,6 +1723,9 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
     da.ku = (int32_t)up->r_pad;
     B->dual = dual_silu_ok(da);
   }
+  CUDA_TRY(cudaStreamCreateWithFlags(&B->side, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&B->ev_join, cudaEventDisableTiming));
   if (B->fused || B->dual) {
     const size_t bytes = 2 * (B->rg + B->ru) * B->hidden;
     CUDA_TRY(cudaMalloc(&B->bgu, bytes));
@@ -1729,6 +1740,9 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
 tnl_status tnl_mlp_destroy(tnl_mlp* B) {
   if (!B) return TNL_OK;
   cudaFree(B->bgu);
+  if (B->ev_fork) cudaEventDestroy(B->ev_fork);
+  if (B->ev_join) cudaEventDestroy(B->ev_join);
+  if (B->side) cudaStreamDestroy(B->side);
   delete B;
   return TNL_OK;
 }
@@ -1791,9 +1805,22 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
     for (const tnl_plan* P : {B->g, B->u, B->d}) lbytes = std::max(lbytes, ws_layout(P, m, &a_, &b_, &c_));
     __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(w + off[1]);
     __nv_bfloat16* u = reinterpret_cast<__nv_bfloat16*>(w + off[2]);
-    tnl_status s = tnl_forward(B->g, x, m, ldx, g, B->inter, lws, lbytes, stream);
+    // decode: gate and up are independent given x -> up runs on the forked stream with
+    // workspace slot 1 (its own zero-at-rest accumulator); TNL_MLP_SERIAL=1 disables
+    static const bool serial = getenv("TNL_MLP_SERIAL") && atoi(getenv("TNL_MLP_SERIAL")) == 1;
+    const bool fork = !serial && m <= kDecMaxM && B->u->decode_max_m && B->inter % 8 == 0;
+    tnl_status su = TNL_OK;
+    if (fork) {
+      if (cudaEventRecord(B->ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(B->side, B->ev_fork, 0) != cudaSuccess)
+        return fail(TNL_ERR_CUDA, "MLP fork failed");
+      su = forward_decode(B->u, x, m, ldx, u, B->inter, static_cast<char*>(lws) + kDecSlotBytes, B->side);
+      if (cudaEventRecord(B->ev_join, B->side) != cudaSuccess) return fail(TNL_ERR_CUDA, "MLP join failed");
+    }
+    tnl_status s = su ? su : tnl_forward(B->g, x, m, ldx, g, B->inter, lws, lbytes, stream);
+    // join even on failure, so a capturing stream is never left forked
+    if (fork && cudaStreamWaitEvent(st, B->ev_join, 0) != cudaSuccess && !s) return fail(TNL_ERR_CUDA, "MLP join failed");
     if (s) return s;
-    if ((s = tnl_forward(B->u, x, m, ldx, u, B->inter, lws, lbytes, stream))) return s;
+    if (!fork && (s = tnl_forward(B->u, x, m, ldx, u, B->inter, lws, lbytes, stream))) return s;
     silu_mul_bf16<<<grid_for(m * B->inter / 8), 256, 0, st>>>(g, u, m * B->inter / 8);
     count_launch();
     return tnl_forward(B->d, g, m, B->inter, y, ldy, lws, lbytes, stream);

@@ -78,6 +78,10 @@ class QwenTNStack:
                                fused=fused_mlp)
             self.layers.append(blk)
         self._ws = None
+        self._ws_side = None
+        self._side = None
+        # decode: k and v (independent of q given h) run on a forked stream with their own workspace
+        self.concurrent_kv = True
 
     def param_count(self) -> int:
         from .layer import param_count
@@ -100,6 +104,14 @@ class QwenTNStack:
             self._ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws
 
+    def _side_workspace(self, m: int):
+        need = max(max(blk[n][2].workspace_bytes(m) for n in ("k", "v")) for blk in self.layers)
+        if self._ws_side is None or self._ws_side.numel() < need:
+            self._ws_side = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        return self._ws_side
+
     def _buffers(self, m: int):
         mk = lambda n: torch.empty((m, n), dtype=self.dtype, device=self.device)  # noqa: E731
         return {"h": mk(HIDDEN), "q": mk(QDIM), "k": mk(KVDIM), "v": mk(KVDIM), "o": mk(HIDDEN), "d": mk(HIDDEN)}
@@ -119,13 +131,27 @@ class QwenTNStack:
         m = x.shape[0]
         ws = self.workspace(m)
         b = bufs or self._buffers(m)
+        fork = self.concurrent_kv and m <= 64
+        if fork:
+            ws_side = self._side_workspace(m)
+            cur = torch.cuda.current_stream(self.device)
         for li, blk in enumerate(self.layers):
             # x += previous MLP output; h = rms(x)   (fused residual add + RMSNorm, one pass)
             self.add_rmsnorm(x, b["d"] if li else None, b["h"])
+            if fork:
+                # k, v on the forked stream (own zero-at-rest workspace), q -> o on this one;
+                # joined before h is overwritten
+                self._side.wait_stream(cur)
+                with torch.cuda.stream(self._side):
+                    blk["k"][2].forward(b["h"], out=b["k"], ws=ws_side)
+                    blk["v"][2].forward(b["h"], out=b["v"], ws=ws_side)
+            else:
+                blk["k"][2].forward(b["h"], out=b["k"], ws=ws)
+                blk["v"][2].forward(b["h"], out=b["v"], ws=ws)
             blk["q"][2].forward(b["h"], out=b["q"], ws=ws)
-            blk["k"][2].forward(b["h"], out=b["k"], ws=ws)
-            blk["v"][2].forward(b["h"], out=b["v"], ws=ws)
             blk["o"][2].forward(b["q"], out=b["o"], ws=ws)  # attention core: pass-through
+            if fork:
+                cur.wait_stream(self._side)
             self.add_rmsnorm(x, b["o"], b["h"])
             blk["mlp"].forward(b["h"], out=b["d"], ws=ws)
         x.add_(b["d"])
