@@ -10,6 +10,27 @@ namespace tnl {
 void count_launch(int64_t n = 1);
 int64_t launch_count(bool reset);
 
+// Launch with programmatic dependent launch allowed (the kernel must griddepcontrol.wait before
+// touching its predecessor's outputs): a plumbing kernel between two TN kernels then launches
+// while its predecessor drains, and releases its own successor early.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  count_launch();
+  return e;
+}
+
 // rmsnorm.cu: x += o (o may be NULL); h = x / rms(x)   (decoder-stack plumbing)
 int launch_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, void* h, int64_t ldh, int64_t m, int64_t n,
                        float eps, cudaStream_t st);

@@ -21,6 +21,10 @@ __global__ void __launch_bounds__(RT) add_rmsnorm_kernel(__nv_bfloat16* __restri
                                                          const __nv_bfloat16* __restrict__ o, int64_t ldo,
                                                          __nv_bfloat16* __restrict__ h, int64_t ldh, int n,
                                                          float eps) {
+  // PDL: wait for the producer of x / o, then let the consumer of h launch (it prefetches its
+  // weights and waits for this grid before reading h)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t row = blockIdx.x;
   uint4* xr = reinterpret_cast<uint4*>(x + row * ldx);
   const uint4* orow = o ? reinterpret_cast<const uint4*>(o + row * ldo) : nullptr;
@@ -80,11 +84,8 @@ int launch_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, void* h
                        float eps, cudaStream_t st) {
   if (n % 8 || n > 8 * RT * RMAXV || ldx % 8 || (o && ldo % 8) || ldh % 8) return (int)cudaErrorInvalidValue;
   if (m == 0) return 0;
-  add_rmsnorm_kernel<<<(unsigned)m, RT, 0, st>>>(static_cast<__nv_bfloat16*>(x), ldx,
-                                                  static_cast<const __nv_bfloat16*>(o), ldo,
-                                                  static_cast<__nv_bfloat16*>(h), ldh, (int)n, eps);
-  count_launch();
-  return (int)cudaGetLastError();
+  return (int)launch_pdl(add_rmsnorm_kernel, dim3((unsigned)m), dim3(RT), 0, st, static_cast<__nv_bfloat16*>(x), ldx,
+                         static_cast<const __nv_bfloat16*>(o), ldo, static_cast<__nv_bfloat16*>(h), ldh, (int)n, eps);
 }
 
 }  // namespace tnl

@@ -132,6 +132,9 @@ static void to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_
 }
 // unfused MLP fallback: g <- silu(g) * u (bf16, 8 elements per thread)
 __global__ void silu_mul_bf16(__nv_bfloat16* g, const __nv_bfloat16* u, int64_t n8) {
+  // PDL (launch_pdl): wait for gate/up, release the down projection's weight prefetch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
     uint4 gv = reinterpret_cast<uint4*>(g)[e];
     const uint4 uv = reinterpret_cast<const uint4*>(u)[e];
@@ -1821,8 +1824,8 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
     if (fork && cudaStreamWaitEvent(st, B->ev_join, 0) != cudaSuccess && !s) return fail(TNL_ERR_CUDA, "MLP join failed");
     if (s) return s;
     if (!fork && (s = tnl_forward(B->u, x, m, ldx, u, B->inter, lws, lbytes, stream))) return s;
-    silu_mul_bf16<<<grid_for(m * B->inter / 8), 256, 0, st>>>(g, u, m * B->inter / 8);
-    count_launch();
+    if (launch_pdl(silu_mul_bf16, dim3(grid_for(m * B->inter / 8)), dim3(256), 0, st, g, u, m * B->inter / 8))
+      return fail(TNL_ERR_CUDA, "silu_mul launch failed");
     return tnl_forward(B->d, g, m, B->inter, y, ldy, lws, lbytes, stream);
   }
   const int64_t rgu = B->rg + B->ru;
