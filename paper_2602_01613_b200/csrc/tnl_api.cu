@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -1481,6 +1482,7 @@ struct tnl_mlp {
   // decode: up runs on a forked stream (workspace slot 1) concurrently with gate (slot 0)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::mutex fork_mu;  // the fork/join section reuses the events: one caller at a time
 };
 
 namespace tnl {
@@ -1813,6 +1815,8 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
     static const bool serial = getenv("TNL_MLP_SERIAL") && atoi(getenv("TNL_MLP_SERIAL")) == 1;
     const bool fork = !serial && m <= kDecMaxM && B->u->decode_max_m && B->inter % 8 == 0;
     tnl_status su = TNL_OK;
+    std::unique_lock<std::mutex> lk(B->fork_mu, std::defer_lock);
+    if (fork) lk.lock();
     if (fork) {
       if (cudaEventRecord(B->ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(B->side, B->ev_fork, 0) != cudaSuccess)
         return fail(TNL_ERR_CUDA, "MLP fork failed");
