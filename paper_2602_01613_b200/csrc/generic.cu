@@ -50,33 +50,47 @@ __global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tile
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
 
   const int64_t pbeg = blockIdx.y * pspan, pend = min(s.P, pbeg + pspan);
+  // A tile: TI x TP, B tile: TP x TJ (256 threads, 4 elements each). The next tile is loaded into
+  // registers before the current one is consumed, so the global latency of iteration k+1 hides
+  // behind the FMAs of iteration k (short chains: cfg1's steps have 2-4 iterations per CTA).
+  constexpr int EA = TI * TP / 256, EB = TP * TJ / 256;
+  int a_ii[EA], a_pp[EA], b_jj[EB], b_pp[EB];
+#pragma unroll
+  for (int u = 0; u < EA; ++u) {
+    const int e = threadIdx.x + u * 256;
+    a_pp[u] = s.sap == 1 ? e % TP : e / TI;  // contiguous along p: consecutive threads walk p
+    a_ii[u] = s.sap == 1 ? e / TP : e % TI;
+  }
+#pragma unroll
+  for (int u = 0; u < EB; ++u) {
+    const int e = threadIdx.x + u * 256;
+    b_jj[u] = s.sbj == 1 ? e % TJ : e / TP;
+    b_pp[u] = s.sbj == 1 ? e / TJ : e % TP;
+  }
+  float ra[EA], rb[EB];
+  auto fetch = [&](int64_t p0) {
+#pragma unroll
+    for (int u = 0; u < EA; ++u) {
+      const int64_t gi = i0 + a_ii[u], gp = p0 + a_pp[u];
+      ra[u] = (gi < s.I && gp < pend) ? ld_as_float(A + gi * s.sai + gp * s.sap) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < EB; ++u) {
+      const int64_t gj = j0 + b_jj[u], gp = p0 + b_pp[u];
+      rb[u] = (gj < s.J && gp < pend) ? ld_as_float(B + gp * s.sbp + gj * s.sbj) : 0.f;
+    }
+  };
+  // PDL: the operands may be the previous step's output
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (pbeg < pend) fetch(pbeg);
   for (int64_t p0 = pbeg; p0 < pend; p0 += TP) {
-    // A tile: TI x TP, B tile: TP x TJ  (256 threads, 4 elements each)
-    for (int e = threadIdx.x; e < TI * TP; e += 256) {
-      int ii, pp;
-      if (s.sap == 1) {  // contiguous along p: let consecutive threads walk p
-        pp = e % TP;
-        ii = e / TP;
-      } else {
-        ii = e % TI;
-        pp = e / TI;
-      }
-      const int64_t gi = i0 + ii, gp = p0 + pp;
-      sA[pp][ii] = (gi < s.I && gp < pend) ? ld_as_float(A + gi * s.sai + gp * s.sap) : 0.f;
-    }
-    for (int e = threadIdx.x; e < TP * TJ; e += 256) {
-      int jj, pp;
-      if (s.sbj == 1) {
-        jj = e % TJ;
-        pp = e / TJ;
-      } else {
-        pp = e % TP;
-        jj = e / TP;
-      }
-      const int64_t gj = j0 + jj, gp = p0 + pp;
-      sB[pp][jj] = (gj < s.J && gp < pend) ? ld_as_float(B + gp * s.sbp + gj * s.sbj) : 0.f;
-    }
+#pragma unroll
+    for (int u = 0; u < EA; ++u) sA[a_pp[u]][a_ii[u]] = ra[u];
+#pragma unroll
+    for (int u = 0; u < EB; ++u) sB[b_pp[u]][b_jj[u]] = rb[u];
     __syncthreads();
+    if (p0 + TP < pend) fetch(p0 + TP);
 #pragma unroll
     for (int pp = 0; pp < TP; ++pp) {
       float a[4], b[4];
@@ -116,6 +130,8 @@ __global__ void __launch_bounds__(256) generic_step_kernel(GStep s, int64_t tile
 }
 
 __global__ void zero_strided_kernel(float* C, GStep s) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t n = s.b1 * s.b2 * s.I * s.J;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e % s.J, i = (e / s.J) % s.I, bb = e / (s.J * s.I);
@@ -128,11 +144,9 @@ int launch_c(const GStep& s, int64_t tiles_i, int64_t tiles_j, int64_t blocks, i
   const int64_t pspan = (s.P + splits - 1) / splits;
   const dim3 grid((unsigned)blocks, (unsigned)splits, 1);
   if (s.c_dt == DT_F32)
-    generic_step_kernel<TA, TB, float><<<grid, 256, 0, st>>>(s, tiles_i, tiles_j, pspan);
-  else
-    generic_step_kernel<TA, TB, __nv_bfloat16><<<grid, 256, 0, st>>>(s, tiles_i, tiles_j, pspan);
-  count_launch();
-  return (int)cudaGetLastError();
+    return (int)launch_pdl(generic_step_kernel<TA, TB, float>, grid, dim3(256), 0, st, s, tiles_i, tiles_j, pspan);
+  return (int)launch_pdl(generic_step_kernel<TA, TB, __nv_bfloat16>, grid, dim3(256), 0, st, s, tiles_i, tiles_j,
+                         pspan);
 }
 
 template <typename TA>
@@ -168,9 +182,9 @@ int launch_generic_step(const GStep& in, cudaStream_t stream) {
     splits = std::max<int64_t>(1, std::min<int64_t>((2 * 148 + blocks - 1) / blocks, s.P / (4 * TP)));
   if (splits > 1 && !s.accumulate) {
     const int64_t n = s.b1 * s.b2 * s.I * s.J;
-    zero_strided_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, stream>>>(
-        static_cast<float*>(s.C), s);
-    count_launch();
+    if (cudaError_t e = launch_pdl(zero_strided_kernel, dim3((unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8)),
+                                   dim3(256), 0, stream, static_cast<float*>(s.C), s))
+      return (int)e;
   }
   if (s.a_dt == DT_F32) return launch_b<float>(s, tiles_i, tiles_j, blocks, splits, stream);
   return launch_b<__nv_bfloat16>(s, tiles_i, tiles_j, blocks, splits, stream);

@@ -26,7 +26,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <mutex>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -208,6 +207,9 @@ struct tnl_plan {
   int32_t ch_na = 0, ch_nb = 0, ch_r0 = 0, ch_c = 0, ch_cpad = 0, ch_b = 0, ch_bpad = 0;
 
   float* gen_w_out = nullptr;       // generic dense rows slice (fp32) for sharded generic plans
+  // fp32 merged cut (CUDA-core FFMA): B_in (r_cut x cols), A_out rows (rows_local x r_cut)
+  float* bin32 = nullptr;
+  float* aout32 = nullptr;
   int32_t plan_large = TNL_PLAN_GENERIC, plan_small = TNL_PLAN_GENERIC;
   int32_t decode_max_m = 0;
   int64_t max_state = 0;  // generic chain: max intermediate elements per token
@@ -926,6 +928,11 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
       if (flags & TNL_PLAN_CHAIN) large = TNL_PLAN_CHAIN;
     }
   }
+  // fp32: the merged cut on CUDA cores (two FFMA steps through an r_cut-wide fp32 T) whenever it
+  // needs fewer flops than the core-by-core chain; TNL_PLAN_GENERIC / _CHAIN keep the chain
+  const bool cut32 = !bf16 && P->family != TNL_FAMILY_DENSE && !(flags & (TNL_PLAN_GENERIC | TNL_PLAN_CHAIN)) &&
+                     P->cut_flops <= P->chain_flops;
+  if (cut32) large = TNL_PLAN_CUT;
   P->plan_large = large;
   P->plan_small = large;
   P->decode_max_m = (tc_ok && P->family != TNL_FAMILY_DENSE && round_up(P->r_cut, 16) <= 256 &&
@@ -951,6 +958,13 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   if (large == TNL_PLAN_CUT && dense) {
     off_w = bytes;
     bytes += round_up(rows_local * P->cols * 2, 256);
+  }
+  size_t off_b32 = 0, off_a32 = 0;
+  if (cut32) {
+    off_b32 = bytes;
+    bytes += round_up(P->r_cut * P->cols * 4, 256);
+    off_a32 = bytes;
+    bytes += round_up(rows_local * P->r_cut * 4, 256);
   }
   size_t off_chd = 0, off_chc = 0;
   if (P->chain_ok) {
@@ -1004,6 +1018,14 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     cudaFree(fb);
     cudaFree(fa);
     if (s2 != TNL_OK) return s2;
+  }
+  if (cut32) {
+    P->bin32 = reinterpret_cast<float*>(base + off_b32);
+    P->aout32 = reinterpret_cast<float*>(base + off_a32);
+    tnl_status s1 = build_panel_f32(P.get(), SEG_INPUT, P->bin32, st);
+    if (s1 == TNL_OK) s1 = build_panel_f32(P.get(), SEG_OUTPUT, P->aout32, st);
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (s1 != TNL_OK) return s1;
   }
   if (P->chain_ok) {
     const int64_t na = P->ch_na, nb = P->ch_nb, r0 = P->ch_r0, c = P->ch_c, cp = P->ch_cpad,
@@ -1415,6 +1437,37 @@ static tnl_status forward_generic(tnl_plan* P, const void* x, int64_t M, int64_t
   if (ws_bytes < need) return fail(TNL_ERR_ARG, "workspace %zu < required %zu bytes", ws_bytes, need);
   char* w = static_cast<char*>(ws);
   const int dt = P->compute_dtype == TNL_BF16 ? DT_BF16 : DT_F32;
+  if (P->bin32) {
+    // fp32 merged cut: T[kappa][m] = sum_j B_in[kappa][j] x[m][j] (split-K FFMA, fp32 atomics),
+    // then y[m][i] = sum_kappa A_out[i][kappa] T[kappa][m]
+    float* t = reinterpret_cast<float*>(w + o_f32);
+    const int64_t rl = P->row_end - P->row_begin;
+    GStep a = mk(1, 1, P->r_cut, P->cols, M);
+    a.A = P->bin32;
+    a.sai = P->cols;
+    a.sap = 1;
+    a.B = x;
+    a.b_dt = dt;
+    a.sbp = 1;
+    a.sbj = ldx;
+    a.C = t;
+    a.sci = M;
+    a.scj = 1;
+    GStep b = mk(1, 1, rl, P->r_cut, M);
+    b.A = P->aout32;
+    b.sai = P->r_cut;
+    b.sap = 1;
+    b.B = t;
+    b.sbp = M;
+    b.sbj = 1;
+    b.C = y;
+    b.c_dt = dt;
+    b.sci = 1;
+    b.scj = ldy;
+    if (launch_generic_step(a, st) || launch_generic_step(b, st))
+      return fail(TNL_ERR_CUDA, "fp32 cut step launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return TNL_OK;
+  }
   const int64_t rows_local = P->row_end - P->row_begin;
   ChainIO io;
   io.in = Operand{x, dt, ldx, 1};
@@ -1983,7 +2036,7 @@ tnl_status tnl_forward(const tnl_plan* plan, const void* x, int64_t m, int64_t l
   if (ldx < P->cols) return fail(TNL_ERR_SHAPE, "ldx %lld < cols %lld", (long long)ldx, (long long)P->cols);
   if (ldy < P->row_end - P->row_begin) return fail(TNL_ERR_SHAPE, "ldy too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (P->plan_large == TNL_PLAN_GENERIC)
+  if (P->plan_large == TNL_PLAN_GENERIC || P->compute_dtype != TNL_BF16)
     return forward_generic(P, x, m, ldx, y, ldy, workspace, workspace_bytes, st);
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (ldx % 8))
     return fail(TNL_ERR_SHAPE, "tensor-core plan needs 16-byte aligned x with ldx %% 8 == 0");

@@ -70,6 +70,20 @@ def test_golden_fp32_generic(golden):
         assert rel(y.T, out) <= FP32_TOL, (rec["family"], rec["mode_shape"], rel(y.T, out))
 
 
+def test_golden_fp32_auto(golden):
+    """fp32 AUTO plans (the FFMA merged cut where it needs fewer flops than the chain) against the
+    reference outputs, same 1e-5 bar as the chain."""
+    index, arrays = golden
+    names = set()
+    for rec in index["forward"] + index["decomp"]:
+        layer = tnl.CompressedLayer(**golden_layer_kwargs(rec, arrays))
+        x, y = arrays[rec["x"]], arrays[rec["y"]]
+        out = run(layer, x.T, torch.float32, tnl.PLAN_AUTO)
+        names.add(layer.plan(torch.float32).info["plan_large_name"])
+        assert rel(y.T, out) <= FP32_TOL, (rec["family"], rec["mode_shape"], rel(y.T, out))
+    assert "cut" in names
+
+
 @pytest.mark.parametrize("flags", [tnl.PLAN_AUTO, tnl.PLAN_CUT, tnl.PLAN_CHAIN, tnl.PLAN_GENERIC])
 def test_golden_bf16_plans(golden, flags):
     index, arrays = golden
@@ -110,6 +124,7 @@ def test_cfg1_tt_fp32():
     for flags in (tnl.PLAN_AUTO, tnl.PLAN_GENERIC):
         y = run(layer, x, torch.float32, flags)
         assert rel(ref, y) <= FP32_TOL
+    assert layer.plan(torch.float32).info["plan_large_name"] == "cut"  # FFMA merged cut (fewer flops)
     # bf16 variant of cfg1 (merged cut and the tcgen05 core-by-core chain)
     check_bf16(L, 16, seed=11)
     check_bf16(L, 16, seed=11, flags=tnl.PLAN_CHAIN)
@@ -416,6 +431,45 @@ def test_mlp_dual_path(rg, rd, m):
     y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
     torch.cuda.synchronize()
     assert rel(_mlp_ref(Lgr, Lur, Ldr, x), y.float().cpu().numpy()) <= 2 * BF16_TOL
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_mlp_decode_fork_shared_workspace(fused):
+    """Decode MLP (M <= 64): up runs on a forked stream with workspace slot 1 while gate uses
+    slot 0. Prefill and decode calls alternate on ONE workspace (prefill scratch must never land in
+    either slot's zero-at-rest accumulator), and the decode call also runs as a CUDA graph."""
+    from paper_2602_01613_b200.mlp import TNMLP
+
+    Lg = O.synthetic_layer("tucker", (1024, 512), 1, (64, 64), seed=54_001)
+    Lu = O.synthetic_layer("tt", (32, 32, 16, 32), 2, (16, 32, 16), seed=54_002)
+    Ld = O.synthetic_layer("tucker", (512, 1024), 1, (128, 128), seed=54_003)
+    (g, Lgr), (u, Lur), (d, Ldr) = (to_layer(L, round_bf16=True) for L in (Lg, Lu, Ld))
+    mlp = TNMLP(g, u, d, fused=fused)
+    ws = torch.zeros(max(mlp.workspace_bytes(m) for m in (300, 64, 16, 1)), dtype=torch.uint8, device=DEV)
+    for i, m in enumerate((16, 300, 1, 64, 300, 16, 16)):
+        x = O.round_bf16(O.synthetic_x(m, 512, seed=54_010 + i))
+        y = mlp.forward(torch.tensor(x, dtype=torch.bfloat16, device=DEV), ws=ws)
+        torch.cuda.synchronize()
+        assert rel(_mlp_ref(Lgr, Lur, Ldr, x), y.float().cpu().numpy()) <= 2 * BF16_TOL, (i, m)
+    # graph capture of the forked decode call, replayed twice on new inputs
+    x = O.round_bf16(O.synthetic_x(16, 512, seed=54_100))
+    xd = torch.tensor(x, dtype=torch.bfloat16, device=DEV)
+    yd = torch.empty(16, 512, dtype=torch.bfloat16, device=DEV)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        mlp.forward(xd, out=yd, ws=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=s):
+        mlp.forward(xd, out=yd, ws=ws)
+    for k in range(2):
+        x = O.round_bf16(O.synthetic_x(16, 512, seed=54_200 + k))
+        xd.copy_(torch.tensor(x, dtype=torch.bfloat16))
+        gr.replay()
+        torch.cuda.synchronize()
+        assert rel(_mlp_ref(Lgr, Lur, Ldr, x), yd.float().cpu().numpy()) <= 2 * BF16_TOL, k
 
 
 @pytest.mark.parametrize("m,n,with_o", [(1, 5120, True), (300, 5120, True), (17, 1024, False), (64, 8192, True)])
