@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(so):
         s, o = so
-        cmd = [nvcc()] + NVCC_FLAGS + ["-c", s, "-o", o]
+        cmd = [nvcc()] + NVCC_FLAGS + os.environ.get("TNL_NVCC_EXTRA", "").split() + ["-c", s, "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -67,8 +67,13 @@ __global__ void __launch_bounds__(FT, 1)
 
   const int tile = blockIdx.x;
   unsigned long long* tr = a.trace ? a.trace + 16 * blockIdx.x : nullptr;
+#ifdef TNL_TRACE_CLOCK  // SM-local cycle stamps (diagnostic builds)
+#define TRACE(ev) \
+  if (tr) tr[ev] = clock64();
+#else
 #define TRACE(ev) \
   if (tr) tr[ev] = globaltimer();
+#endif
   if (threadIdx.x == 0) TRACE(0);
   const int kbB = (a.kB + 63) / 64;
   const int nT = (a.nA + 127) / 128;
@@ -109,12 +114,6 @@ __global__ void __launch_bounds__(FT, 1)
       TRACE(2);
       pdl_wait();
       TRACE(3);
-      for (int kb = 0; kb < kbB; ++kb) {
-        mbar_arrive_expect_tx(&stg[kb], SM::F_BLK);
-        tma_load_2d(reinterpret_cast<uint8_t*>(sF) + kb * SM::F_BLK, &tmT, &stg[kb], 0, kb * 64);
-      }
-      for (int kb = 0; kb < kbB; ++kb) mbar_wait(&stg[kb], 0);
-      TRACE(4);
     }
     __syncwarp();
     // T_{l-1} was read only by the previous kernel, which has completed: zero this CTA's slice
@@ -131,6 +130,7 @@ __global__ void __launch_bounds__(FT, 1)
       mbar_wait(wfull, 0);
       for (int kb = 0; kb < kbB; ++kb) {  // block kb as soon as it is converted
         mbar_wait(&tfull[kb], 0);
+        if (kb == kbB - 1) TRACE(15);
         tc_fence_after();
         const uint64_t ad = smem_desc_sw128(smem_u32(sWo + kb * WBLK));
         const uint64_t bd = smem_desc_sw128(smem_u32(sT + kb * SM::T_BLK));
@@ -155,39 +155,48 @@ __global__ void __launch_bounds__(FT, 1)
     pdl_wait();
     if (et == 0) TRACE(11);
     // T_l: fp32 [64 kappa][BN tokens] -> bf16 MN-major SW128 [64 kappa][128 B] per k-block
-    // (the accumulator's kappa-major layout is the MMA's MN-major B operand: no transpose)
-    // one float4 (4 tokens) per thread and step: the warp reads 512 contiguous bytes (no bank
-    // conflicts) and writes 8-byte halves of the swizzled 16-byte chunks
-    constexpr int ITEMS = 64 * (BN / 4);  // (kappa, 4-token quad) per block
+    // (the accumulator's kappa-major layout is the MMA's MN-major B operand: no transpose).
+    // Read straight from L2 by all epilogue threads: every 16-byte load of every block is in
+    // flight at once (a TMA box per block lands at ~14 B/cycle, one after the other), then one
+    // proxy fence publishes all converted blocks. One float4 = 4 tokens of one kappa row; a warp
+    // reads 512 contiguous bytes and writes 8-byte halves of the swizzled 16-byte chunks.
+    constexpr int QPR = BN / 4;                  // float4 quads per kappa row
+    constexpr int ITEMS = 64 * QPR;              // per k-block
     constexpr int PER = ITEMS >= FEPI ? ITEMS / FEPI : 1;
-    for (int kb = 0; kb < kbB; ++kb) {
-      if (lane_id() == 0) mbar_wait(&stg[kb], 0);
-      __syncwarp();
-      if (et == 0 && kb == 0) TRACE(12);
-      const uint32_t src = smem_u32(sF) + kb * SM::F_BLK;
-      const uint32_t dst = smem_u32(sT) + kb * SM::T_BLK;
-      float4 v[PER];
+    {
+      float4 v[4][PER];
 #pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int e = et + u * FEPI;
-        if (e < ITEMS) v[u] = lds128f(src + 16 * e);
-      }
+      for (int kb = 0; kb < 4; ++kb)
 #pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int e = et + u * FEPI;
-        if (e < ITEMS) {
-          const int kap = e / (BN / 4), quad = e % (BN / 4);
-          uint2 p;
-          p.x = pack_bf16x2(v[u].x, v[u].y);
-          p.y = pack_bf16x2(v[u].z, v[u].w);
-          sts64(dst + sw128(kap, quad >> 1) + (quad & 1) * 8, p);
+        for (int u = 0; u < PER; ++u) {
+          const int e = et + u * FEPI;
+          const int kap = kb * 64 + e / QPR, quad = e % QPR;
+          v[kb][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (kb < kbB && e < ITEMS && kap < a.kB) v[kb][u] = ldg128_cg(a.t_in + (int64_t)kap * 64 + quad * 4);
+        }
+      if (et == 0) TRACE(12);
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        if (kb >= kbB) break;
+        const uint32_t dst = smem_u32(sT) + kb * SM::T_BLK;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int e = et + u * FEPI;
+          if (e < ITEMS) {
+            const int kap = e / QPR, quad = e % QPR;
+            uint2 p;
+            p.x = pack_bf16x2(v[kb][u].x, v[kb][u].y);
+            p.y = pack_bf16x2(v[kb][u].z, v[kb][u].w);
+            sts64(dst + sw128(kap, quad >> 1) + (quad & 1) * 8, p);
+          }
         }
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&tfull[kb]);
+      if (lane_id() == 0)
+        for (int kb = 0; kb < kbB; ++kb) mbar_arrive(&tfull[kb]);
+      if (et == 0) TRACE(14);
     }
-    if (et == 0) TRACE(13);
     if (et == 0) TRACE(5);
 
     const uint32_t q = warp & 3;

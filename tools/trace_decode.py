@@ -15,6 +15,8 @@ from paper_2602_01613_b200.stack import TNStack
 ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, default=64)
 ap.add_argument("--variants", default="2,2,2,0,0,0")
+ap.add_argument("--cycles", action="store_true", help="library built with -DTNL_TRACE_CLOCK: stamps are SM cycles, "
+                "reported relative to each CTA's pdl_passed")
 a = ap.parse_args()
 vs = [int(t) for t in a.variants.split(",")]
 layers = []
@@ -38,7 +40,7 @@ st.replay()
 torch.cuda.synchronize()
 EV = ["start", "setup", "w_issued", "pdl_passed", "mma_first", "mma_issued", "epi_pdl", "act_ready", "done", "stored", "end"]
 EVF = ["start", "setup", "w_issued", "pdl_passed", "T_landed", "T_converted", "B_done", "x_ready", "A_done", "reds_issued", "end",
-       "epi_pdl", "stg0", "conv_loop_done"]
+       "epi_pdl", "stg0", "stg_last", "conv0_done", "mma_has_last"]
 t0 = None
 for li, (v, b) in enumerate(zip(vs, bufs)):
     arr = b.view(2, 1024, 16).cpu().numpy()
@@ -48,6 +50,20 @@ for li, (v, b) in enumerate(zip(vs, bufs)):
         if not used.any():
             continue
         blk = blk[used].astype(np.int64)
+        if a.cycles and ph == 1 and li + 1 < len(vs):
+            ref = blk[:, 3].copy()
+            for e in range(blk.shape[1]):
+                blk[:, e] = np.where(blk[:, e] > 0, blk[:, e] - ref + 10**9, 0)
+            row = []
+            for e, nm in enumerate(EVF):
+                col = blk[:, e]
+                col = col[col > 0] - 10**9
+                if len(col):
+                    row.append(f"{nm}={int(col.min())}/{int(np.median(col))}/{int(col.max())}")
+            print(f"L{li} v{v} fused-cycles ctas={used.sum()}: " + " ".join(row))
+            continue
+        if a.cycles:
+            continue
         if t0 is None:
             t0 = blk[:, 0].min()
         row = []
