@@ -502,7 +502,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": world * M * L / (ms_e2e / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": e2e_stack.h2d_bytes, "d2h_bytes_per_step": e2e_stack.d2h_bytes,
-                "ms_per_step": ms_e2e, "api": "TNStack CUDA graph: pinned H2D + 70 tnl_forward per token group + D2H"},
+                "ms_per_step": ms_e2e, "api": "TNStack CUDA graph: per token group, pinned host x -> tnl_copy_async (SM-driven H2D) -> the 70-layer chain -> tnl_copy_async D2H to pinned host y"},
         "gpu_launches": launches_per_step * args.steps,
         "launches_per_step": launches_per_step,
         "clocks": clocks,

@@ -200,6 +200,13 @@ TNL_API tnl_status tnl_jacobi_sweeps(double* work, double* rot, int64_t batch, i
 TNL_API tnl_status tnl_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, void* h, int64_t ldh,
                                    int64_t m, int64_t n, float eps, void* stream);
 
+/* Stream-ordered copy of `bytes` executed by the SMs (H2D / D2H / D2D): either pointer may be
+ * pinned host memory (cudaHostAlloc / torch pin_memory — mapped into the unified address
+ * space), both 16-byte aligned. PDL-launched, so in a decode graph the next TN kernel prefetches
+ * its weights while the activations arrive, and no memcpy node breaks the launch chain. Used for
+ * the host I/O of a decode step (the reference has no device path; its forward is host numpy). */
+TNL_API tnl_status tnl_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+
 /* Number of libtnl kernel launches issued by this thread since the last reset
  * (evidence counter for benchmarks). */
 TNL_API int64_t tnl_launch_count(int32_t reset);

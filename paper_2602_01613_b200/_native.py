@@ -39,6 +39,7 @@ EXPORTED = (
     "tnl_plan_set_trace",
     "tnl_jacobi_sweeps",
     "tnl_add_rmsnorm",
+    "tnl_copy_async",
     "tnl_stack_workspace_size",
     "tnl_stack_forward",
     "tnl_mlp_create",
@@ -136,6 +137,8 @@ def load():
         lib.tnl_jacobi_sweeps.restype = ctypes.c_int
         lib.tnl_add_rmsnorm.argtypes = [P, i64, P, i64, P, i64, i64, i64, ctypes.c_float, P]
         lib.tnl_add_rmsnorm.restype = ctypes.c_int
+        lib.tnl_copy_async.argtypes = [P, P, ctypes.c_size_t, P]
+        lib.tnl_copy_async.restype = ctypes.c_int
         lib.tnl_launch_count.argtypes = [ctypes.c_int32]
         lib.tnl_launch_count.restype = i64
         for name in ("tnl_plan_create", "tnl_plan_create_rows", "tnl_plan_destroy", "tnl_plan_query",

@@ -35,6 +35,9 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 int launch_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, void* h, int64_t ldh, int64_t m, int64_t n,
                        float eps, cudaStream_t st);
 
+// hostio.cu: SM-driven copy (either side may be mapped pinned host memory), 16-byte aligned
+int launch_copy16(void* dst, const void* src, size_t bytes, int sms, cudaStream_t st);
+
 // jacobi.cu: batched one-sided Jacobi sweeps (tnl_jacobi_sweeps)
 int launch_jacobi_sweeps(double* work, double* rot, int64_t batch, int n, int m, int nv, double tol, int max_sweeps,
                          int32_t* sweeps, cudaStream_t st);

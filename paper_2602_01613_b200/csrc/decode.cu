@@ -110,23 +110,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       TRACE(2);
       pdl_wait();
       TRACE(3);
-      for (int i = 0; i < npre; ++i) {
-        if (ACT_F32) {  // fp32 accumulator rows kappa in [k-block], all tokens
-          mbar_arrive_expect_tx(&stg[i], F_STAGE);
-          tma_load_2d(reinterpret_cast<uint8_t*>(sF) + i * F_STAGE, &tmX, &stg[i], 0, (kb0 + i) * BK);
-        } else {
-          tma_load_2d(sB + i * B_STAGE, &tmX, &full[i], (kb0 + i) * BK, 0);
-        }
-      }
-      if (ACT_F32 && a.counter) {
-        // every accumulator read of this CTA has landed -> count it here, off the
-        // epilogue's critical path; the epilogue reads last_flag at the very end
-        for (int i = 0; i < npre; ++i) mbar_wait(&stg[i], 0);
-        __threadfence();
-        const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-        *last_flag = (atomicAdd(a.counter, 1u) == total - 1) ? 1u : 0u;
-        mbar_arrive(flagbar);
-      }
+      if (!ACT_F32)  // (phase B: the epilogue warps read the fp32 accumulator themselves)
+        for (int i = 0; i < npre; ++i) tma_load_2d(sB + i * B_STAGE, &tmX, &full[i], (kb0 + i) * BK, 0);
       for (int i = npre; i < nkb; ++i) {  // (phase A only: ACT_F32 keeps nkb <= STAGES)
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
@@ -170,33 +155,50 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     pdl_wait();
     if (et == 0) TRACE(6);
     if constexpr (ACT_F32) {
-      // staged fp32 [64 kappa][BN tokens] -> bf16 MN-major SW128 operand [64 kappa][128 B]
-      constexpr int ITEMS = 64 * (BN / 4);  // (kappa, 4-token quad)
+      // fp32 accumulator [64 kappa][BN tokens] per k-block -> bf16 MN-major SW128 operand
+      // [64 kappa][128 B] (no transpose). All 16-byte L2 loads of all blocks are in flight at
+      // once (instead of one TMA box per block landing after the other), one proxy fence.
+      constexpr int QPR = BN / 4;
+      constexpr int ITEMS = 64 * QPR;  // (kappa, 4-token quad) per block
       constexpr int PER = ITEMS >= DEC_EPI ? ITEMS / DEC_EPI : 1;
-      for (int i = 0; i < nkb; ++i) {
-        mbar_wait(&stg[i], 0);
-        const uint32_t src = smem_u32(sF) + i * F_STAGE;
-        const uint32_t dst = smem_u32(sB) + i * B_STAGE;
-        float4 v[PER];
+      static_assert(STAGES >= 4, "phase B holds every k-block of the accumulator");
+      float4 v[4][PER];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
           const int e = et + u * DEC_EPI;
-          if (e < ITEMS) v[u] = lds128f(src + 16 * e);
+          const int kap = (kb0 + i) * BK + e / QPR, quad = e % QPR;
+          v[i][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (i < nkb && e < ITEMS && kap < a.K) v[i][u] = ldg128_cg(a.act_f32 + (int64_t)kap * a.act_ld + quad * 4);
         }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i >= nkb) break;
+        const uint32_t dst = smem_u32(sB) + i * B_STAGE;
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
           const int e = et + u * DEC_EPI;
           if (e < ITEMS) {
-            const int kap = e / (BN / 4), quad = e % (BN / 4);
+            const int kap = e / QPR, quad = e % QPR;
             uint2 p;
-            p.x = pack_bf16x2(v[u].x, v[u].y);
-            p.y = pack_bf16x2(v[u].z, v[u].w);
+            p.x = pack_bf16x2(v[i][u].x, v[i][u].y);
+            p.y = pack_bf16x2(v[i][u].z, v[i][u].w);
             sts64(dst + sw128_off(kap, quad >> 1) + (quad & 1) * 8, p);
           }
         }
-        fence_proxy_async_smem();
-        named_bar(1, DEC_EPI);
-        if (et == 0) mbar_arrive(&full[i]);
+      }
+      fence_proxy_async_smem();
+      named_bar(1, DEC_EPI);
+      if (et == 0) {
+        for (int i = 0; i < nkb; ++i) mbar_arrive(&full[i]);
+        if (a.counter) {
+          // every accumulator read of this CTA has completed (the values were consumed above):
+          // count it; the last CTA re-zeroes the accumulator at the very end
+          __threadfence();
+          const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+          *last_flag = (atomicAdd(a.counter, 1u) == total - 1) ? 1u : 0u;
+        }
       }
       if (et == 0) TRACE(7);
     }
@@ -244,8 +246,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
         tma_store_2d(&tmY, sY, tile_m * BM, 0);
         tma_store_commit();
       }
-      if (a.counter) {
-        mbar_wait(flagbar, 0);  // producer lane wrote last_flag before arriving
+      if (a.counter) {  // last_flag was written by et 0 before the named barrier above
         if (*last_flag) {
           float4* z = reinterpret_cast<float4*>(const_cast<float*>(a.act_f32));
           for (int64_t e = et; e < a.zero_elems / 4; e += DEC_EPI) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);

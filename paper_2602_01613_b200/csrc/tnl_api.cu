@@ -1950,6 +1950,27 @@ tnl_status tnl_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, voi
   return TNL_OK;
 }
 
+tnl_status tnl_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes && (!dst || !src)) return fail(TNL_ERR_ARG, "null argument");
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15)
+    return fail(TNL_ERR_ARG, "copy_async: dst and src must be 16-byte aligned");
+  for (const void* p : {static_cast<const void*>(dst), src}) {
+    cudaPointerAttributes at;
+    if (bytes && (cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type == cudaMemoryTypeUnregistered)) {
+      cudaGetLastError();
+      return fail(TNL_ERR_ARG, "copy_async: %p is pageable host memory (the SMs can only reach pinned memory)", p);
+    }
+  }
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const int err = launch_copy16(dst, src, bytes, sms, static_cast<cudaStream_t>(stream));
+  if (err) return fail(TNL_ERR_CUDA, "copy_async launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
+}
+
 tnl_status tnl_jacobi_sweeps(double* work, double* rot, int64_t batch, int64_t n, int64_t m, int64_t nv, double tol,
                              int32_t max_sweeps, int32_t* sweeps, void* stream) {
   if (batch < 0) return fail(TNL_ERR_ARG, "negative batch %lld", (long long)batch);

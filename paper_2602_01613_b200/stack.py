@@ -94,9 +94,14 @@ class TNStack:
         main = torch.cuda.Stream(self.device)
         side = [torch.cuda.Stream(self.device) for _ in range(k)]
 
+        def copy(dst, src):  # SM-driven copy (tnl_copy_async): PDL-chained, no memcpy node
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            N.check(self._lib.tnl_copy_async(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(src.data_ptr()),
+                                             dst.numel() * dst.element_size(), ctypes.c_void_p(st)))
+
         def one_pass():
-            if host_io:
-                self.x_dev.copy_(self.x_host, non_blocking=True)
+            # host I/O per token group on the group's own stream: each group's chain starts when
+            # its rows have arrived and its D2H leaves as soon as its chain ends
             fork = torch.cuda.Event()
             fork.record(main)
             joins = []
@@ -104,14 +109,16 @@ class TNStack:
                 s = side[j]
                 s.wait_event(fork)
                 with torch.cuda.stream(s):
+                    if host_io:
+                        copy(self.x_dev[lo:hi], self.x_host[lo:hi])
                     self.forward(self.x_dev[lo:hi], out=self.y_dev[lo:hi], slot=j)
+                    if host_io:
+                        copy(self.y_host[lo:hi], self.y_dev[lo:hi])
                     e = torch.cuda.Event()
                     e.record(s)
                     joins.append(e)
             for e in joins:
                 main.wait_event(e)
-            if host_io:
-                self.y_host.copy_(self.y_dev, non_blocking=True)
 
         main.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(main):

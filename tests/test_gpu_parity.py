@@ -289,6 +289,52 @@ def test_stack_graph_replay_matches_eager():
     assert float(d) < 1e-2
 
 
+@pytest.mark.parametrize("mb", [1, 2, 3])
+def test_stack_graph_host_io_microbatches(mb):
+    """Host I/O through tnl_copy_async per token group (graph) == the eager device pass."""
+    from paper_2602_01613_b200.stack import TNStack
+
+    Ls = [O.synthetic_layer("tucker", (1024, 1024), 1, (64, 64), seed=46_100 + i) for i in range(3)]
+    st = TNStack([to_layer(L, round_bf16=True)[0] for L in Ls], torch.bfloat16)
+    x = torch.randn(37, 1024, device=DEV).to(torch.bfloat16)
+    ye = st.forward(x).clone()
+    st.capture(37, host_io=True, microbatches=mb)
+    st.x_host.copy_(x.cpu())
+    st.y_host.zero_()
+    st.replay()
+    torch.cuda.synchronize()
+    d = (st.y_host.float() - ye.cpu().float()).norm() / ye.cpu().float().norm()
+    assert float(d) < 1e-2
+    x2 = torch.randn(37, 1024, device=DEV).to(torch.bfloat16)  # new host input, same graph
+    st.x_host.copy_(x2.cpu())
+    st.replay()
+    torch.cuda.synchronize()
+    y2 = st.forward(x2)
+    d = (st.y_host.float() - y2.cpu().float()).norm() / y2.cpu().float().norm()
+    assert float(d) < 1e-2
+
+
+@pytest.mark.parametrize("nbytes", [16, 4096 + 7, 655360, 3 * 2**20 + 5])
+def test_copy_async_roundtrip(nbytes):
+    import ctypes
+
+    from paper_2602_01613_b200 import _native as N
+
+    lib = N.load()
+    src = torch.randint(0, 255, (nbytes,), dtype=torch.uint8).pin_memory()
+    dev = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+    back = torch.zeros(nbytes, dtype=torch.uint8).pin_memory()
+    s = torch.cuda.current_stream().cuda_stream
+    N.check(lib.tnl_copy_async(ctypes.c_void_p(dev.data_ptr()), ctypes.c_void_p(src.data_ptr()), nbytes, ctypes.c_void_p(s)))
+    N.check(lib.tnl_copy_async(ctypes.c_void_p(back.data_ptr()), ctypes.c_void_p(dev.data_ptr()), nbytes, ctypes.c_void_p(s)))
+    torch.cuda.synchronize()
+    assert torch.equal(dev.cpu(), src) and torch.equal(back, src)
+    pageable = torch.zeros(64, dtype=torch.uint8)
+    with pytest.raises(Exception):
+        N.check(lib.tnl_copy_async(ctypes.c_void_p(dev.data_ptr()), ctypes.c_void_p(pageable.data_ptr()), 64,
+                                   ctypes.c_void_p(s)))
+
+
 def test_chain_plan_selected_for_two_mode_inputs():
     L = O.synthetic_layer("tr", (64, 80, 64, 80), 2, (16, 16, 16, 16), seed=47_000)
     layer, _ = to_layer(L, round_bf16=True)
