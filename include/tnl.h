@@ -118,6 +118,7 @@ typedef struct {
 
 typedef struct tnl_plan tnl_plan;
 typedef struct tnl_mlp tnl_mlp;
+typedef struct tnl_chain tnl_chain;
 
 TNL_API int tnl_abi_version(void);
 TNL_API const char* tnl_last_error(void);
@@ -163,6 +164,24 @@ TNL_API tnl_status tnl_stack_workspace_size(const tnl_plan* const* plans, int32_
 TNL_API tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void* x,
                                      int64_t m, int64_t ldx, void* y, int64_t ldy, void* workspace,
                                      size_t workspace_bytes, void* stream);
+
+/* Cluster-resident decode of a chain of square bf16 merged-cut layers (D x D, D % 1024 == 0,
+ * D <= 6144, cut ranks padded to multiples of 64 <= 256): ONE 16-CTA thread-block cluster walks
+ * all n layers for up to 32 tokens; each CTA owns D/16 rows of every layer, the per-layer
+ * split-K reduction of the cut activations runs over distributed shared memory (no kernel
+ * boundary, no global accumulator, deterministic summation order) and a producer warp streams
+ * the weights, pre-swizzled into an arena at create time, ahead of the dependency chain.
+ * Independent token groups (other streams) run as independent clusters. No workspace.
+ * Same semantics as tnl_stack_forward over the same plans (the reference's forward is
+ * layer_to_matrix(L) @ x per layer, tn_decompositions.py:364 / sensitivity.py:154-160).
+ * TNL_ERR_UNSUPPORTED when the plans or the device do not qualify. */
+TNL_API tnl_status tnl_chain_create(const tnl_plan* const* plans, int32_t n, int32_t flags, tnl_chain** out);
+TNL_API tnl_status tnl_chain_forward(const tnl_chain* chain, const void* x, int64_t m, int64_t ldx, void* y,
+                                     int64_t ldy, void* stream);
+TNL_API tnl_status tnl_chain_destroy(tnl_chain* chain);
+/* Debug: per-layer clock64 stamps of the chain kernel into a device buffer of
+ * >= 16*256*8 int64 ([cta][layer][event]); NULL disables. */
+TNL_API tnl_status tnl_chain_set_trace(tnl_chain* chain, void* device_buffer);
 
 /* Qwen3 MLP block of three TN layers: y = down(silu(gate(x)) * up(x)).
  * For merged-cut bf16 plans (gate/up cut <= 128, down cut <= 256) and M > 64 the

@@ -40,6 +40,10 @@ EXPORTED = (
     "tnl_jacobi_sweeps",
     "tnl_add_rmsnorm",
     "tnl_copy_async",
+    "tnl_chain_create",
+    "tnl_chain_forward",
+    "tnl_chain_destroy",
+    "tnl_chain_set_trace",
     "tnl_stack_workspace_size",
     "tnl_stack_forward",
     "tnl_mlp_create",
@@ -139,6 +143,14 @@ def load():
         lib.tnl_add_rmsnorm.restype = ctypes.c_int
         lib.tnl_copy_async.argtypes = [P, P, ctypes.c_size_t, P]
         lib.tnl_copy_async.restype = ctypes.c_int
+        lib.tnl_chain_create.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(P)]
+        lib.tnl_chain_create.restype = ctypes.c_int
+        lib.tnl_chain_forward.argtypes = [P, P, i64, i64, P, i64, P]
+        lib.tnl_chain_forward.restype = ctypes.c_int
+        lib.tnl_chain_destroy.argtypes = [P]
+        lib.tnl_chain_destroy.restype = ctypes.c_int
+        lib.tnl_chain_set_trace.argtypes = [P, P]
+        lib.tnl_chain_set_trace.restype = ctypes.c_int
         lib.tnl_launch_count.argtypes = [ctypes.c_int32]
         lib.tnl_launch_count.restype = i64
         for name in ("tnl_plan_create", "tnl_plan_create_rows", "tnl_plan_destroy", "tnl_plan_query",

@@ -29,7 +29,7 @@ from .layer import CompressedLayer
 
 class TNStack:
     def __init__(self, layers: list[CompressedLayer], dtype=torch.bfloat16, device=None,
-                 flags: int = N.PLAN_AUTO):
+                 flags: int = N.PLAN_AUTO, cluster: bool = False):
         if not layers:
             raise ShapeError("empty stack")
         self.layers = layers
@@ -46,6 +46,24 @@ class TNStack:
         self.graph = None
         self._lib = N.load()
         self._handles = (ctypes.c_void_p * len(self.plans))(*[p.handle.value for p in self.plans])
+        # opt-in cluster-resident decode (tnl_chain_*: one 16-CTA cluster walks the whole chain,
+        # DSMEM reductions, bitwise-deterministic) when every layer qualifies (square bf16
+        # merged-cut layers); decode calls with M <= 32 then run as ONE kernel. Measured slower
+        # than the per-boundary kernels on the cfg2 bank (16 SMs cannot stream the weights fast
+        # enough), so it is not the default.
+        self.chain = None
+        if cluster and dtype == torch.bfloat16 and len(self.plans) >= 1:
+            h = ctypes.c_void_p()
+            if self._lib.tnl_chain_create(self._handles, len(self.plans), 0, ctypes.byref(h)) == 0:
+                self.chain = h
+
+    def __del__(self):
+        if getattr(self, "chain", None) is not None:
+            try:
+                self._lib.tnl_chain_destroy(self.chain)
+            except Exception:
+                pass
+            self.chain = None
 
     def workspace_bytes(self, m: int) -> int:
         n = ctypes.c_size_t()
@@ -69,10 +87,14 @@ class TNStack:
             x = x.contiguous()
         if out is None:
             out = torch.empty((m, self.rows), dtype=self.dtype, device=self.device)
-        ws = self.workspace(m, slot)
         stream = torch.cuda.current_stream(self.device).cuda_stream
         ldx = x.stride(0) if m > 1 else self.cols
         ldy = out.stride(0) if m > 1 else self.rows
+        if self.chain is not None and m <= 32:
+            N.check(self._lib.tnl_chain_forward(self.chain, ctypes.c_void_p(x.data_ptr()), m, ldx,
+                                                ctypes.c_void_p(out.data_ptr()), ldy, ctypes.c_void_p(stream)))
+            return out
+        ws = self.workspace(m, slot)
         N.check(self._lib.tnl_stack_forward(self._handles, len(self.plans), ctypes.c_void_p(x.data_ptr()), m, ldx,
                                             ctypes.c_void_p(out.data_ptr()), ldy, ctypes.c_void_p(ws.data_ptr()),
                                             ws.numel(), ctypes.c_void_p(stream)))
