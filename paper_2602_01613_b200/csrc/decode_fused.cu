@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(FT, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tDB = tmem, tDA = tmem + BN;  // D_A: nT blocks of BN columns
+  const uint32_t tDU = tmem + 192;             // gated boundary: the up projection's D_B (BN <= 64)
+  const int kg = a.kg;
   pdl_launch_dependents();
   if (threadIdx.x == 0) TRACE(1);
 
@@ -134,8 +136,11 @@ __global__ void __launch_bounds__(FT, 1)
         tc_fence_after();
         const uint64_t ad = smem_desc_sw128(smem_u32(sWo + kb * WBLK));
         const uint64_t bd = smem_desc_sw128(smem_u32(sT + kb * SM::T_BLK));
+        const bool up = kg && kb >= kg;
+        const uint32_t d = up ? tDU : tDB;
+        const int kk = up ? kb - kg : kb;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) mma_bf16_ss(tDB, ad + 2 * k, bd + 128 * k, idesc, (kb | k) != 0);
+        for (int k = 0; k < 4; ++k) mma_bf16_ss(d, ad + 2 * k, bd + 128 * k, idesc, (kk | k) != 0);
       }
       mma_commit(bdone);
       mbar_wait(xfull, 0);
@@ -213,6 +218,12 @@ __global__ void __launch_bounds__(FT, 1)
       for (int c = c_begin; c < c_begin + HALF && c < BN; c += 16) {
         float v[16];
         tmem_ld16(tDB + ((q * 32) << 16) + c, v);
+        if (kg) {  // h = silu(g) * u = g * u * sigmoid(g), fp32
+          float w[16];
+          tmem_ld16(tDU + ((q * 32) << 16) + c, w);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = v[e] * w[e] * __frcp_rn(1.f + __expf(-v[e]));
+        }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           uint4 p;

@@ -1085,7 +1085,7 @@ constexpr size_t kDecHeadBytes = sizeof(float) * 64 * 256;  // decode accumulato
 // slot 1 (a forked stream) concurrently with one on slot 0 (MLP gate || up) and no layout ever
 // places scratch inside a zero-at-rest accumulator.
 constexpr size_t kDecSlotBytes = kDecHeadBytes + 256 + sizeof(float) * 8 * 256;
-constexpr int kDecSlots = 2;
+constexpr int kDecSlots = 3;  // slots 0..2 double as the three rotating accumulators of a fused stack
 
 static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b0, size_t* o_b1) {
   size_t bytes = 0;
@@ -1506,7 +1506,7 @@ static bool stack_fusable(const tnl_plan* const* plans, int32_t n, int64_t m) {
 }
 
 static size_t stack_ws_bytes(const tnl_plan* const* plans, int32_t n, int64_t m) {
-  if (stack_fusable(plans, n, m)) return 3 * round_up(sizeof(float) * 64 * 256, 256) + 256;
+  if (stack_fusable(plans, n, m)) return kDecSlots * kDecSlotBytes;
   size_t mx = 0;
   int64_t width = 0;
   for (int i = 0; i < n; ++i) {
@@ -1533,6 +1533,10 @@ struct tnl_mlp {
   bool dual = false;  // gate/up output GEMMs + SiLU*mul in one kernel (ranks the fused path cannot hold)
   int64_t hidden = 0, inter = 0, rg = 0, ru = 0, rd = 0;
   __nv_bfloat16* bgu = nullptr;  // [B_g (rg rows) ; B_u (ru rows)] x hidden
+  // decode gated boundary (rg + ru <= 256): A_gu = [A_g | A_u] (inter x (rg + ru)); one phase A
+  // of the stacked [B_g; B_u], then ONE kernel does gate/up phase B, SiLU*mul and down's phase A
+  bool gated = false;
+  __nv_bfloat16* agu = nullptr;
   // decode: up runs on a forked stream (workspace slot 1) concurrently with gate (slot 0)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1651,12 +1655,14 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     return TNL_OK;
   }
   char* base = static_cast<char*>(ws);
-  const size_t slot = round_up(sizeof(float) * 64 * 256, 256);
   // three rotating zero-at-rest accumulators: boundary l reads T_l = tacc[l % 3], reduces into
-  // T_{l+1} = tacc[(l+1) % 3] and zeroes T_{l-1} = tacc[(l+2) % 3], which only boundary l-1 read
-  float* tacc[3] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + slot),
-                    reinterpret_cast<float*>(base + 2 * slot)};
-  unsigned int* cnt = reinterpret_cast<unsigned int*>(base + 3 * slot);  // [1] (last phase B)
+  // T_{l+1} = tacc[(l+1) % 3] and zeroes T_{l-1} = tacc[(l+2) % 3], which only boundary l-1 read.
+  // They are the accumulators of the workspace's three decode slots (and the last phase B uses
+  // slot 2's counter), so a stack can share a workspace with single-layer decode calls and MLP
+  // blocks without ever overlapping their scratch.
+  float* tacc[3] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + kDecSlotBytes),
+                    reinterpret_cast<float*>(base + 2 * kDecSlotBytes)};
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(base + 2 * kDecSlotBytes + kDecHeadBytes);
   const int bn = pick_bn(m);
   int err = 0;
   // layer 0, phase A
@@ -1741,6 +1747,84 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
 }
 
 
+// Decode MLP block in three launches: (1) T_gu = [B_g; B_u] x (stacked phase A, split-K fp32
+// reductions into decode slot 0), (2) the gated boundary kernel: per 128 intermediate rows,
+// g = A_g T_g and u = A_u T_u (tcgen05, TMEM), h = silu(g) * u on chip, T_d += B_d[:, rows] h
+// (reductions into slot 1), (3) down's phase B (re-zeroes T_d, zeroes T_gu). h never leaves the
+// SM; the path replaces gate/up phase B, the SiLU*mul kernel and down's phase A.
+static tnl_status mlp_decode_gated(tnl_mlp* B, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
+                                   char* head, cudaStream_t st) {
+  const int64_t rgu = B->rg + B->ru;
+  tnl_plan* D = B->d;
+  float* t0 = reinterpret_cast<float*>(head);
+  float* t1 = reinterpret_cast<float*>(head + kDecSlotBytes);
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(head + kDecSlotBytes + kDecHeadBytes);
+  const int bn = pick_bn(m);
+  int err;
+  {
+    CUtensorMap tw, tx;
+    if ((err = get_tmap(B->g, &tw, B->bgu, B->hidden, rgu, B->hidden, 128)) ||
+        (err = get_tmap(B->g, &tx, x, B->hidden, m, ldx, bn)))
+      return fail(TNL_ERR_CUDA, "tensor map (MLP decode phase A) failed: %d", err);
+    DecArgs a;
+    memset(&a, 0, sizeof a);
+    a.M_rows = (int32_t)rgu;
+    a.tokens = (int32_t)m;
+    a.K = (int32_t)B->hidden;
+    a.kb_per_split = 4;
+    const int splits = (int)(((B->hidden + 63) / 64 + 3) / 4);
+    a.out = t0;
+    a.ldo_i = 64;
+    a.ldo_j = 1;
+    a.out_f32_atomic = 1;
+    if ((err = launch_dec_a(tw, tx, a, splits, st)))
+      return fail(TNL_ERR_CUDA, "MLP decode phase A launch: %s", cudaGetErrorString((cudaError_t)err));
+  }
+  {
+    CUtensorMap two, tt, twi;
+    if ((err = get_tmap(B->g, &two, B->agu, rgu, B->inter, rgu, 128)) ||
+        (err = get_tmap2(B->g, &tt, t0, true, 64, rgu, 64, bn, 64, 0)) ||
+        (err = get_tmap(D, &twi, D->bin, B->inter, D->r_pad, B->inter, 128)))
+      return fail(TNL_ERR_CUDA, "tensor map (MLP gated boundary) failed: %d", err);
+    FusedArgs f;
+    memset(&f, 0, sizeof f);
+    f.tokens = (int32_t)m;
+    f.rows = (int32_t)B->inter;
+    f.kB = (int32_t)rgu;
+    f.nA = (int32_t)D->r_pad;
+    f.t_in = t0;
+    f.t_out = t1;
+    f.kg = (int32_t)(B->rg / 64);
+    if ((err = launch_dec_fused(two, tt, twi, f, (int)(B->inter / 128), st)))
+      return fail(TNL_ERR_CUDA, "MLP gated boundary launch: %s", cudaGetErrorString((cudaError_t)err));
+  }
+  {
+    CUtensorMap tw2, tt, ty;
+    if ((err = get_tmap(D, &tw2, D->aout, D->r_pad, D->rows, D->r_pad, 128)) ||
+        (err = get_tmap2(D, &tt, t1, true, 64, D->r_pad, 64, bn, 64, 0)) ||
+        (err = get_tmap2(D, &ty, y, false, D->rows, m, ldy, 128, bn, 0)))
+      return fail(TNL_ERR_CUDA, "tensor map (MLP decode phase B) failed: %d", err);
+    DecArgs b;
+    memset(&b, 0, sizeof b);
+    b.M_rows = (int32_t)D->rows;
+    b.tokens = (int32_t)m;
+    b.K = (int32_t)D->r_pad;
+    b.kb_per_split = (int32_t)((D->r_pad + 63) / 64);
+    b.act_f32 = t1;
+    b.act_ld = 64;
+    b.out = y;
+    b.ldo_i = 1;
+    b.ldo_j = ldy;
+    b.counter = cnt;  // the last CTA re-zeroes T_d
+    b.zero_elems = 64 * D->r_pad;
+    b.zero_prev = t0;  // T_gu, read only by the gated boundary kernel
+    b.zero_prev_elems = 64 * rgu;
+    if ((err = launch_dec_b(tw2, tt, ty, b, st)))
+      return fail(TNL_ERR_CUDA, "MLP decode phase B launch: %s", cudaGetErrorString((cudaError_t)err));
+  }
+  return TNL_OK;
+}
+
 tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_plan* down, int32_t flags,
                           tnl_mlp** out) {
   if (!gate || !up || !down || !out) return fail(TNL_ERR_ARG, "null argument");
@@ -1785,7 +1869,20 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
   CUDA_TRY(cudaStreamCreateWithFlags(&B->side, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&B->ev_join, cudaEventDisableTiming));
-  if (B->fused || B->dual) {
+  B->gated = !(flags & 1) && cut(gate) && cut(up) && cut(down) && gate->decode_max_m && up->decode_max_m &&
+              down->decode_max_m && B->rg + B->ru <= 256 && down->r_pad <= 256 && B->inter % 128 == 0 &&
+              B->hidden % 128 == 0;
+  if (B->gated) {
+    const int64_t rgu = B->rg + B->ru;
+    const size_t bytes = 2 * rgu * B->inter;
+    CUDA_TRY(cudaMalloc(&B->agu, bytes));
+    CUDA_TRY(cudaMemset(B->agu, 0, bytes));
+    CUDA_TRY(cudaMemcpy2D(B->agu, 2 * rgu, gate->aout, 2 * gate->r_pad, 2 * gate->r_pad, B->inter,
+                          cudaMemcpyDeviceToDevice));
+    CUDA_TRY(cudaMemcpy2D(B->agu + B->rg, 2 * rgu, up->aout, 2 * up->r_pad, 2 * up->r_pad, B->inter,
+                          cudaMemcpyDeviceToDevice));
+  }
+  if (B->fused || B->dual || B->gated) {
     const size_t bytes = 2 * (B->rg + B->ru) * B->hidden;
     CUDA_TRY(cudaMalloc(&B->bgu, bytes));
     CUDA_TRY(cudaMemset(B->bgu, 0, bytes));
@@ -1933,6 +2030,7 @@ tnl_status tnl_chain_destroy(tnl_chain* C) {
 tnl_status tnl_mlp_destroy(tnl_mlp* B) {
   if (!B) return TNL_OK;
   cudaFree(B->bgu);
+  cudaFree(B->agu);
   if (B->ev_fork) cudaEventDestroy(B->ev_fork);
   if (B->ev_join) cudaEventDestroy(B->ev_join);
   if (B->side) cudaStreamDestroy(B->side);
@@ -1991,6 +2089,10 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
       return fail(TNL_ERR_CUDA, "MLP dual kernel launch: %s", cudaGetErrorString((cudaError_t)err));
     return tnl_forward(B->d, h, m, B->inter, y, ldy, lws, lbytes, stream);
   }
+  static const bool no_gated = getenv("TNL_MLP_NO_GATED") && atoi(getenv("TNL_MLP_NO_GATED")) == 1;  // A/B
+  if (!prefill && B->gated && !no_gated && m <= kDecMaxM && !((reinterpret_cast<uintptr_t>(x) & 15) || ldx % 8) &&
+      !((reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8))
+    return mlp_decode_gated(B, x, m, ldx, y, ldy, w + off[0], st);
   if (!B->fused || !prefill) {
     // unfused: three layer forwards + a SiLU*mul kernel
     void* lws = w + off[0];

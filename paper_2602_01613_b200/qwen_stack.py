@@ -76,7 +76,11 @@ class QwenTNStack:
                 blk[name] = (kinds[name], layer, layer.plan(dtype, self.device))
             blk["mlp"] = TNMLP(blk["gate"][1], blk["up"][1], blk["down"][1], dtype=dtype, device=self.device,
                                fused=fused_mlp)
+            # decode: q -> (pass-through attention) -> o as one two-layer stack (one fused
+            # boundary kernel: q's output rows never leave the SM)
+            blk["qo"] = (ctypes.c_void_p * 2)(blk["q"][2].handle.value, blk["o"][2].handle.value)
             self.layers.append(blk)
+        self.fuse_qo = True
         self._ws = None
         self._ws_side = None
         self._side = None
@@ -106,10 +110,10 @@ class QwenTNStack:
 
     def _side_workspace(self, m: int):
         need = max(max(blk[n][2].workspace_bytes(m) for n in ("k", "v")) for blk in self.layers)
-        if self._ws_side is None or self._ws_side.numel() < need:
-            self._ws_side = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
+        if self._ws_side is None or self._ws_side[0].numel() < need:
+            self._ws_side = [torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device) for _ in range(2)]
         if self._side is None:
-            self._side = torch.cuda.Stream(self.device)
+            self._side = [torch.cuda.Stream(self.device) for _ in range(2)]
         return self._ws_side
 
     def _buffers(self, m: int):
@@ -139,19 +143,29 @@ class QwenTNStack:
             # x += previous MLP output; h = rms(x)   (fused residual add + RMSNorm, one pass)
             self.add_rmsnorm(x, b["d"] if li else None, b["h"])
             if fork:
-                # k, v on the forked stream (own zero-at-rest workspace), q -> o on this one;
-                # joined before h is overwritten
-                self._side.wait_stream(cur)
-                with torch.cuda.stream(self._side):
-                    blk["k"][2].forward(b["h"], out=b["k"], ws=ws_side)
-                    blk["v"][2].forward(b["h"], out=b["v"], ws=ws_side)
+                # k and v on two forked streams (own zero-at-rest workspaces): each is two kernels,
+                # shorter than the q -> o chain, so neither is on the critical path; joined before h is
+                # overwritten
+                for j, name in enumerate(("k", "v")):
+                    self._side[j].wait_stream(cur)
+                    with torch.cuda.stream(self._side[j]):
+                        blk[name][2].forward(b["h"], out=b[name], ws=ws_side[j])
             else:
                 blk["k"][2].forward(b["h"], out=b["k"], ws=ws)
                 blk["v"][2].forward(b["h"], out=b["v"], ws=ws)
-            blk["q"][2].forward(b["h"], out=b["q"], ws=ws)
-            blk["o"][2].forward(b["q"], out=b["o"], ws=ws)  # attention core: pass-through
+            if fork and self.fuse_qo:
+                st = torch.cuda.current_stream(self.device).cuda_stream
+                N.check(N.load().tnl_stack_forward(blk["qo"], 2, ctypes.c_void_p(b["h"].data_ptr()), m,
+                                                   b["h"].stride(0) if m > 1 else HIDDEN,
+                                                   ctypes.c_void_p(b["o"].data_ptr()),
+                                                   b["o"].stride(0) if m > 1 else HIDDEN,
+                                                   ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(st)))
+            else:
+                blk["q"][2].forward(b["h"], out=b["q"], ws=ws)
+                blk["o"][2].forward(b["q"], out=b["o"], ws=ws)  # attention core: pass-through
             if fork:
-                cur.wait_stream(self._side)
+                for sd in self._side:
+                    cur.wait_stream(sd)
             self.add_rmsnorm(x, b["o"], b["h"])
             blk["mlp"].forward(b["h"], out=b["d"], ws=ws)
         x.add_(b["d"])

@@ -452,6 +452,24 @@ def test_mlp_block_cfg3():
     assert rel(ref, y.float().cpu().numpy()) <= 2 * BF16_TOL
 
 
+@pytest.mark.parametrize("m", [1, 37, 64])
+def test_mlp_decode_gated_cfg3(m):
+    """Decode MLP (M <= 64) at the cfg3 shape through the gated boundary kernel (gate/up phase B,
+    SiLU*mul and down's phase A in one launch) vs the oracle; repeated calls (zero-at-rest slots)."""
+    from paper_2602_01613_b200.mlp import TNMLP
+
+    Ls = [O.synthetic_layer("tt", ms, 2, (64, 64, 64), seed=51_100 + i) for i, ms in
+          enumerate([(160, 160, 64, 80), (160, 160, 64, 80), (64, 80, 160, 160)])]
+    pairs = [to_layer(L, round_bf16=True) for L in Ls]
+    mlp = TNMLP(*[p[0] for p in pairs])
+    x = O.round_bf16(O.synthetic_x(m, 5120, seed=51_109))
+    xt = torch.tensor(x, dtype=torch.bfloat16, device=DEV)
+    ys = [mlp(xt).float().cpu().numpy() for _ in range(3)]
+    ref = _mlp_ref(*[p[1] for p in pairs], x)
+    for y in ys:
+        assert rel(ref, y) <= 2 * BF16_TOL
+
+
 def test_qwen_stack_fused_mlp_matches_unfused():
     """cfg4 driver: the stack with fused TNMLP blocks (TT r64 / TR4 layers) equals the unfused stack."""
     from paper_2602_01613_b200.qwen_stack import QwenTNStack

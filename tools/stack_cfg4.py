@@ -19,12 +19,14 @@ ap.add_argument("--ms", default="1,64,8192")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--unfused-mlp", action="store_true")
 ap.add_argument("--serial-kv", action="store_true", help="k/v on the main stream (no fork)")
+ap.add_argument("--no-fuse-qo", action="store_true", help="decode: q and o as two tnl_forward calls")
 a = ap.parse_args()
 HBM, TC = 6554.6e9, 1635e12
 
 t0 = time.time()
 st = QwenTNStack(a.layers, fused_mlp=not a.unfused_mlp)
 st.concurrent_kv = not a.serial_kv
+st.fuse_qo = not a.no_fuse_qo
 build_s = time.time() - t0
 P = st.param_count()
 F = st.chain_flops_per_token()
