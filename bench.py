@@ -418,6 +418,33 @@ def main():
                               "alg_GBps": byts / (ms_p / 1e3) / 1e9, "frac_hbm": byts / (ms_p / 1e3) / 1e9 / hbm,
                               "plan": pl.info["plan_large_name"]}
             del xs, yp
+        # the whole cfg3 MLP block (5120 -> 25600 -> 5120, TT r64 gate/up/down): fused path, h on chip
+        from paper_2602_01613_b200.mlp import TNMLP
+
+        g_, u_, d_ = (S.make_layer(f, ms_, rm, rk, seed=31_000 + i) for i, (f, ms_, rm, rk) in
+                      enumerate((S.CFG3_GATE, S.CFG3_GATE, S.CFG3_DOWN)))
+        blk = TNMLP(g_, u_, d_)
+        Mp = 8192
+        xs = [torch.randn(Mp, 5120, device="cuda").to(torch.bfloat16) for _ in range(4)]
+        yp = torch.empty(Mp, 5120, device="cuda", dtype=torch.bfloat16)
+        wsp = blk.workspace(Mp)
+        it = [0]
+
+        def mlp_step():
+            blk.forward(xs[it[0] % 4], out=yp, ws=wsp)
+            it[0] += 1
+
+        ms_b = time_graph(mlp_step, 20, 3, torch, None)
+        P3 = sum(tnl.param_count(l_) for l_ in (g_, u_, d_))
+        b_bytes = 2 * (P3 + Mp * (5120 + 5120))
+        b_flops = Mp * sum(l_.chain_flops_per_token() for l_ in (g_, u_, d_))
+        t_roof = max(b_bytes / (hbm * 1e9), b_flops / (tc * 1e12))
+        prefill["mlp_block"] = {"what": "Qwen3-32B MLP block y = down(silu(gate(x)) * up(x)), TT r64, one tnl_mlp_forward",
+                                "M": Mp, "ms": ms_b, "tokens_per_s": Mp / (ms_b / 1e3), "fused": bool(blk.fused),
+                                "t_roofline_ms": 1e3 * t_roof, "frac_roofline": t_roof / (ms_b / 1e3),
+                                "chain_TFLOPs": b_flops / (ms_b / 1e3) / 1e12}
+        blk.close()
+        del xs, yp
 
     # secondary: cfg1 (BASELINE configs[0]) TT (64,64|64,64) r32, M=16 — fp32 generic chain (the
     # reference-precision path, CUDA-core bound) and bf16 plans; 8 distinct layers (> L2? no: 2 MB)

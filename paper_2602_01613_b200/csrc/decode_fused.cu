@@ -41,7 +41,7 @@ struct FSmem {
                                   4 * T_BLK + 256;
 };
 
-template <int BN>
+template <int BN, bool GATED>
 __global__ void __launch_bounds__(FT, 1)
     dec_fused_kernel(const __grid_constant__ CUtensorMap tmWo, const __grid_constant__ CUtensorMap tmT,
                      const __grid_constant__ CUtensorMap tmWi, const FusedArgs a) {
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(FT, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tDB = tmem, tDA = tmem + BN;  // D_A: nT blocks of BN columns
   const uint32_t tDU = tmem + 192;             // gated boundary: the up projection's D_B (BN <= 64)
-  const int kg = a.kg;
+  const int kg = GATED ? a.kg : 0;
   pdl_launch_dependents();
   if (threadIdx.x == 0) TRACE(1);
 
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(FT, 1)
         tc_fence_after();
         const uint64_t ad = smem_desc_sw128(smem_u32(sWo + kb * WBLK));
         const uint64_t bd = smem_desc_sw128(smem_u32(sT + kb * SM::T_BLK));
-        const bool up = kg && kb >= kg;
+        const bool up = GATED && kb >= kg;
         const uint32_t d = up ? tDU : tDB;
         const int kk = up ? kb - kg : kb;
 #pragma unroll
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(FT, 1)
       for (int c = c_begin; c < c_begin + HALF && c < BN; c += 16) {
         float v[16];
         tmem_ld16(tDB + ((q * 32) << 16) + c, v);
-        if (kg) {  // h = silu(g) * u = g * u * sigmoid(g), fp32
+        if constexpr (GATED) {  // h = silu(g) * u = g * u * sigmoid(g), fp32
           float w[16];
           tmem_ld16(tDU + ((q * 32) << 16) + c, w);
 #pragma unroll
@@ -291,13 +291,13 @@ __global__ void __launch_bounds__(FT, 1)
 #undef TRACE
 }
 
-template <int BN>
+template <int BN, bool GATED>
 int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi, const FusedArgs& a,
                  int grid, cudaStream_t st) {
   constexpr size_t smem = FSmem<BN>::bytes;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dec_fused_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(dec_fused_kernel<BN, GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return (int)e;
     attr = true;
@@ -312,7 +312,7 @@ int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap&
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dec_fused_kernel<BN>, wo, t, wi, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dec_fused_kernel<BN, GATED>, wo, t, wi, a);
   count_launch();
   return (int)e;
 }
@@ -322,9 +322,14 @@ int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap&
 int launch_dec_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi, const FusedArgs& a,
                      int grid, cudaStream_t st) {
   if (a.kB > 256 || a.nA > 256 || a.rows % 128) return (int)cudaErrorInvalidValue;
-  if (a.tokens <= 16) return launch_fused<16>(wo, t, wi, a, grid, st);
-  if (a.tokens <= 32) return launch_fused<32>(wo, t, wi, a, grid, st);
-  return launch_fused<64>(wo, t, wi, a, grid, st);
+  if (a.kg) {
+    if (a.tokens <= 16) return launch_fused<16, true>(wo, t, wi, a, grid, st);
+    if (a.tokens <= 32) return launch_fused<32, true>(wo, t, wi, a, grid, st);
+    return launch_fused<64, true>(wo, t, wi, a, grid, st);
+  }
+  if (a.tokens <= 16) return launch_fused<16, false>(wo, t, wi, a, grid, st);
+  if (a.tokens <= 32) return launch_fused<32, false>(wo, t, wi, a, grid, st);
+  return launch_fused<64, false>(wo, t, wi, a, grid, st);
 }
 
 }  // namespace tnl
