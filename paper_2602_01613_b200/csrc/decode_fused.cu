@@ -32,29 +32,31 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
   return (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
 }
 
-template <int BN>
+// Shared memory, laid out by the boundary's actual block counts (kbB A_out / T blocks, nT B_in
+// tiles): A_out blocks | B_in blocks (later the D_A transpose stage) | x operand | T operand | bars
 struct FSmem {
-  static constexpr uint32_t F_BLK = BN * 64 * 4;   // fp32 staging of 64 kappa x BN tokens
-  static constexpr uint32_t T_BLK = 64 * 128;      // bf16 T operand block, MN-major [64 kappa][128 B]
-  static constexpr uint32_t X_BLK = 64 * 128;      // bf16 x operand block, MN-major [64 k][128 B]
-  static constexpr size_t bytes = 1024 + 4 * WBLK /*A_out*/ + 4 * WBLK /*B_in*/ + 4 * F_BLK +
-                                  4 * T_BLK + 256;
+  static constexpr uint32_t T_BLK = 64 * 128;  // bf16 T operand block, MN-major [64 kappa][128 B]
+  static constexpr uint32_t X_BLK = 64 * 128;  // bf16 x operand block, MN-major [64 k][128 B]
+  static size_t bytes(int kbB, int nT) {
+    return 1024 + (size_t)kbB * WBLK + (size_t)nT * 2 * WBLK + 2 * X_BLK + (size_t)kbB * T_BLK + 256;
+  }
 };
 
 template <int BN, bool GATED>
 __global__ void __launch_bounds__(FT, 1)
     dec_fused_kernel(const __grid_constant__ CUtensorMap tmWo, const __grid_constant__ CUtensorMap tmT,
                      const __grid_constant__ CUtensorMap tmWi, const FusedArgs a) {
-  using SM = FSmem<BN>;
+  using SM = FSmem;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sWo = smem;                   // kbB blocks
-  uint8_t* sWi = sWo + 4 * WBLK;         // nT x 2 blocks
-  float* sF = reinterpret_cast<float*>(sWi + 4 * WBLK);  // kbB fp32 staging blocks (then x operand)
-  uint8_t* sX = reinterpret_cast<uint8_t*>(sF);
-  uint8_t* sT = reinterpret_cast<uint8_t*>(sF) + 4 * SM::F_BLK;  // kbB bf16 T blocks
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + 4 * SM::T_BLK);
+  const int kbB = (a.kB + 63) / 64;
+  const int nT = (a.nA + 127) / 128;
+  uint8_t* sWo = smem;                    // kbB blocks
+  uint8_t* sWi = sWo + kbB * WBLK;        // nT x 2 blocks (then the D_A transpose stage)
+  uint8_t* sX = sWi + nT * 2 * WBLK;      // x operand: 2 blocks
+  uint8_t* sT = sX + 2 * SM::X_BLK;       // kbB bf16 T blocks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + kbB * SM::T_BLK);
   uint64_t* wfull = bars;
   uint64_t* stg = bars + 1;  // [4]
   uint64_t* tfull = bars + 10;  // [4]: T block kb converted (one arrive per epilogue warp)
@@ -75,8 +77,6 @@ __global__ void __launch_bounds__(FT, 1)
   if (tr) tr[ev] = globaltimer();
 #endif
   if (threadIdx.x == 0) TRACE(0);
-  const int kbB = (a.kB + 63) / 64;
-  const int nT = (a.nA + 127) / 128;
   const uint32_t warp = warp_id();
 
   if (warp == 0 && elect_one()) {
@@ -294,11 +294,14 @@ __global__ void __launch_bounds__(FT, 1)
 template <int BN, bool GATED>
 int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi, const FusedArgs& a,
                  int grid, cudaStream_t st) {
-  constexpr size_t smem = FSmem<BN>::bytes;
+  // plain boundaries (decode stacks: 40-64 CTAs) reserve the full layout, one CTA per SM; the gated
+  // MLP boundary (inter/128 = 200 CTAs at Qwen3 shapes) takes only what its ranks need, so two
+  // CTAs share an SM and the grid runs in one wave
+  const size_t smem = GATED ? FSmem::bytes((a.kB + 63) / 64, (a.nA + 127) / 128) : FSmem::bytes(4, 2);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(dec_fused_kernel<BN, GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                                         (int)FSmem::bytes(4, 2));
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
