@@ -120,6 +120,25 @@ typedef struct tnl_plan tnl_plan;
 typedef struct tnl_mlp tnl_mlp;
 typedef struct tnl_chain tnl_chain;
 
+/* Decoder-stack folds of the *_ex entry points (prefill, M > 64, bf16 cut plans):
+ *   y (+)= f(x'),   x'_m = x_m / sqrt(ss_in[m] / rms_n + rms_eps)   (RMSNorm, no learned scale)
+ * ss_in = per-token sum of squares of x (tnl_rms_stats); the cut activations are linear in x, so
+ * the normalisation is one scale per token row in the first step's epilogue / conversion.
+ * accumulate != 0: y += f(x') — the residual add rides on the last step's TMA store as a bulk
+ * reduce-add at L2 (bf16), so the residual stream is updated in place with no extra pass. Together
+ * they replace the decoder stack's residual-add + RMSNorm kernel (a read of x and o and a write of
+ * x and h per norm) by one statistics read of x. Not part of the reference's API (the reference has
+ * no decoder); used by the cfg4 stack driver. Other paths return TNL_ERR_UNSUPPORTED. */
+typedef struct {
+  int32_t accumulate;
+  const float* ss_in;
+  int32_t rms_n;
+  float rms_eps;
+} tnl_fwd_opts;
+
+/* ss[i] = sum_j x[i][j]^2 for a bf16 [m][n] matrix (row pitch ldx % 8 == 0, n % 8 == 0). */
+TNL_API tnl_status tnl_rms_stats(const void* x, int64_t ldx, int64_t m, int64_t n, float* ss, void* stream);
+
 TNL_API int tnl_abi_version(void);
 TNL_API const char* tnl_last_error(void);
 
@@ -143,6 +162,10 @@ TNL_API tnl_status tnl_workspace_size(const tnl_plan* plan, int64_t m, size_t* b
  * Concurrent calls (other streams) need distinct workspaces. */
 TNL_API tnl_status tnl_forward(const tnl_plan* plan, const void* x, int64_t m, int64_t ldx, void* y,
                        int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
+
+TNL_API tnl_status tnl_forward_ex(const tnl_plan* plan, const void* x, int64_t m, int64_t ldx, void* y,
+                                  int64_t ldy, void* workspace, size_t workspace_bytes, const tnl_fwd_opts* opts,
+                                  void* stream);
 
 /* End-to-end: host x (M x cols) -> H2D -> forward -> D2H -> host y (M x rows_local),
  * asynchronous on `stream` (host buffers should be pinned). m <= max_m. */
@@ -197,6 +220,10 @@ TNL_API tnl_status tnl_mlp_workspace_size(const tnl_mlp* mlp, int64_t m, size_t*
 TNL_API tnl_status tnl_mlp_forward(const tnl_mlp* mlp, const void* x, int64_t m, int64_t ldx,
                                    void* y, int64_t ldy, void* workspace, size_t workspace_bytes,
                                    void* stream);
+/* opts (tnl_fwd_opts): ss_in normalises the block's input, residual / ss_out apply to its output */
+TNL_API tnl_status tnl_mlp_forward_ex(const tnl_mlp* mlp, const void* x, int64_t m, int64_t ldx, void* y,
+                                      int64_t ldy, void* workspace, size_t workspace_bytes, const tnl_fwd_opts* opts,
+                                      void* stream);
 
 /* Batched cyclic one-sided Jacobi sweeps, fp64, in place — the reference's only native
  * component, `_jacobi_cy.jacobi_sweeps(work, rot, tol, max_sweeps) -> int`

@@ -40,6 +40,9 @@ EXPORTED = (
     "tnl_jacobi_sweeps",
     "tnl_add_rmsnorm",
     "tnl_copy_async",
+    "tnl_forward_ex",
+    "tnl_mlp_forward_ex",
+    "tnl_rms_stats",
     "tnl_chain_create",
     "tnl_chain_forward",
     "tnl_chain_destroy",
@@ -52,6 +55,17 @@ EXPORTED = (
     "tnl_mlp_workspace_size",
     "tnl_mlp_forward",
 )
+
+
+class FwdOpts(ctypes.Structure):
+    """tnl_fwd_opts (include/tnl.h): folded residual add / RMSNorm of a decoder stack (prefill)."""
+
+    _fields_ = [
+        ("accumulate", ctypes.c_int32),
+        ("ss_in", ctypes.c_void_p),
+        ("rms_n", ctypes.c_int32),
+        ("rms_eps", ctypes.c_float),
+    ]
 
 
 class LayerDesc(ctypes.Structure):
@@ -143,6 +157,13 @@ def load():
         lib.tnl_add_rmsnorm.restype = ctypes.c_int
         lib.tnl_copy_async.argtypes = [P, P, ctypes.c_size_t, P]
         lib.tnl_copy_async.restype = ctypes.c_int
+        OP = ctypes.POINTER(FwdOpts)
+        lib.tnl_forward_ex.argtypes = [P, P, i64, i64, P, i64, P, ctypes.c_size_t, OP, P]
+        lib.tnl_forward_ex.restype = ctypes.c_int
+        lib.tnl_mlp_forward_ex.argtypes = [P, P, i64, i64, P, i64, P, ctypes.c_size_t, OP, P]
+        lib.tnl_mlp_forward_ex.restype = ctypes.c_int
+        lib.tnl_rms_stats.argtypes = [P, i64, i64, i64, P, P]
+        lib.tnl_rms_stats.restype = ctypes.c_int
         lib.tnl_chain_create.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(P)]
         lib.tnl_chain_create.restype = ctypes.c_int
         lib.tnl_chain_forward.argtypes = [P, P, i64, i64, P, i64, P]

@@ -23,7 +23,19 @@ struct TcGemmArgs {
   void* out;
   int64_t ldo_i, ldo_j;
   int32_t out_mode;
+  // bf16 epilogue of the persistent / pair kernels (decoder-stack folds, tnl_fwd_opts):
+  int32_t reduce_add = 0;        // out += D (TMA bulk reduce-add at L2) instead of out = D
+  const float* ss_in = nullptr;  // D row i scaled by rsqrt(ss_in[i] / rms_n + rms_eps) (folded RMSNorm)
+  int32_t rms_n = 0;
+  float rms_eps = 0.f;
 };
+
+// Epilogue helper shared by the persistent and pair kernels (bf16 output mode): the folded-RMSNorm
+// scale of output row `row`.
+__device__ __forceinline__ float row_rms_scale(const TcGemmArgs& a, int row) {
+  if (!a.ss_in || row >= a.M) return 1.f;
+  return rsqrtf(__ldcg(a.ss_in + row) / (float)a.rms_n + a.rms_eps);
+}
 
 // dual_gemm.cu: h (M x N) = silu(T[:, :kg] A_g^T) * (T[:, u_off : u_off + ku] A_u^T), bf16.
 struct DualArgs {

@@ -149,6 +149,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const int lrow = q * 32 + lane_id();
       const int row = tm * PBM + lrow;
       if (args.out_mode == TC_OUT_BF16) {
+        const float rscale = row_rms_scale(args, row);
         for (int c0 = 0; c0 < BN; c0 += 64) {
           uint8_t* stage = sC + (chunk_ct & 1) * P_C_CHUNK;
           if (et == 0) tma_store_wait_read_le1();
@@ -157,6 +158,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           for (int c = 0; c < 64; c += 16) {
             float v[16];
             tmem_ld16(d + c0 + c, v);
+            if (args.ss_in) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) v[e] *= rscale;
+            }
             uint4 p0, p1;
             p0.x = pack_bf16x2(v[0], v[1]);
             p0.y = pack_bf16x2(v[2], v[3]);
@@ -181,7 +186,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           if (et == 0) {
             const int col = tn * BN + c0;
             if (col < args.N && tm * PBM < args.M) {
-              tma_store_2d(&tmC, stage, col, tm * PBM);
+              if (args.reduce_add)
+                tma_reduce_add_2d(&tmC, stage, col, tm * PBM);
+              else
+                tma_store_2d(&tmC, stage, col, tm * PBM);
               tma_store_commit();
             }
           }

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(192, 1)
       const int lrow = q * 32 + lane_id();
       const int row = tm * BM + lrow;
       if (args.out_mode == TC_OUT_BF16) {
+        const float rscale = row_rms_scale(args, row);
         for (int c0 = 0; c0 < BN; c0 += 64) {
           uint8_t* stage = sC + (chunk_ct & 1) * C_CHUNK;
           // the TMA store that used this staging buffer two chunks ago must have read it
@@ -156,6 +157,10 @@ __global__ void __launch_bounds__(192, 1)
           for (int c = 0; c < 64; c += 16) {
             float v[16];
             tmem_ld16(d + c0 + c, v);
+            if (args.ss_in) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) v[e] *= rscale;
+            }
             uint4 p0, p1;
             p0.x = pack_bf16x2(v[0], v[1]);
             p0.y = pack_bf16x2(v[2], v[3]);
@@ -180,7 +185,10 @@ __global__ void __launch_bounds__(192, 1)
           if (et == 0) {
             const int col = tn * BN + c0;
             if (col < args.N) {
-              tma_store_2d(&tmC, stage, col, tm * BM);
+              if (args.reduce_add)
+                tma_reduce_add_2d(&tmC, stage, col, tm * BM);
+              else
+                tma_store_2d(&tmC, stage, col, tm * BM);
               tma_store_commit();
             }
           }

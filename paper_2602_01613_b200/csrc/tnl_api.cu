@@ -123,6 +123,25 @@ __global__ void copy_2d_any(const void* src, int s_dt, int64_t s_r, int64_t s_c,
 }
 static int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
 // dense [rows][cols] fp32 -> bf16 (both contiguous)
+// [rows][cols] fp32 -> bf16 with row r scaled by rsqrt(ss[r] / n + eps) (folded RMSNorm of the
+// layer input: the cut activations are linear in x, so normalising them == normalising x)
+__global__ void f32_to_bf16_rowscale(const float4* __restrict__ src, uint4* __restrict__ dst, int64_t n8, int64_t cols8,
+                                     const float* __restrict__ ss, float inv_n, float eps) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
+    const float sc = rsqrtf(ss[e / cols8] * inv_n + eps);
+    const float4 a = src[2 * e], b = src[2 * e + 1];
+    __nv_bfloat162 o[4] = {__floats2bfloat162_rn(a.x * sc, a.y * sc), __floats2bfloat162_rn(a.z * sc, a.w * sc),
+                           __floats2bfloat162_rn(b.x * sc, b.y * sc), __floats2bfloat162_rn(b.z * sc, b.w * sc)};
+    dst[e] = *reinterpret_cast<uint4*>(o);
+  }
+}
+static void to_bf16_scaled(const float* src, __nv_bfloat16* dst, int64_t rows, int64_t cols, const tnl_fwd_opts* o,
+                           cudaStream_t st) {
+  const int64_t n8 = rows * cols / 8;
+  f32_to_bf16_rowscale<<<grid_for(n8), 256, 0, st>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<uint4*>(dst),
+                                                      n8, cols / 8, o->ss_in, 1.f / (float)o->rms_n, o->rms_eps);
+  count_launch();
+}
 static void to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st) {
   if (n % 8 == 0 && !(reinterpret_cast<uintptr_t>(src) & 15) && !(reinterpret_cast<uintptr_t>(dst) & 15))
     f32_to_bf16_v8<<<grid_for(n / 8), 256, 0, st>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<uint4*>(dst),
@@ -130,6 +149,33 @@ static void to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_
   else
     f32_to_bf16_2d<<<grid_for(n), 256, 0, st>>>(src, n, dst, n, 1, n);
   count_launch();
+}
+// ss[row] = sum_j x[row][j]^2 (one CTA per row; the folded RMSNorm's statistics)
+__global__ void __launch_bounds__(256) row_sumsq_bf16(const __nv_bfloat16* __restrict__ x, int64_t ldx, int64_t n,
+                                                      float* __restrict__ ss) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint4* r = reinterpret_cast<const uint4*>(x + (int64_t)blockIdx.x * ldx);
+  float s = 0.f;
+  for (int64_t c = threadIdx.x; c < n / 8; c += 256) {
+    const uint4 w = r[c];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 f = __bfloat1622float2(h[t]);
+      s = fmaf(f.x, f.x, fmaf(f.y, f.y, s));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  __shared__ float red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    ss[blockIdx.x] = t;
+  }
 }
 // unfused MLP fallback: g <- silu(g) * u (bf16, 8 elements per thread)
 __global__ void silu_mul_bf16(__nv_bfloat16* g, const __nv_bfloat16* u, int64_t n8) {
@@ -1294,7 +1340,8 @@ static tnl_status forward_decode(tnl_plan* P, const void* x, int64_t M, int64_t 
 // out_f32: fp32 split-K reductions into `out` (zeroed here); else bf16 via TMA store.
 static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void* W, int64_t ldw,
                             int64_t M, int64_t N, int64_t K, void* out, int64_t ldo, bool out_f32,
-                            int splits, cudaStream_t st, int bn_force = 0) {
+                            int splits, cudaStream_t st, int bn_force = 0, const tnl_fwd_opts* in_o = nullptr,
+                            const tnl_fwd_opts* out_o = nullptr) {
   const int bn = bn_force ? bn_force : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
   CUtensorMap ta, tb, tc;
   int err;
@@ -1320,6 +1367,12 @@ static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void*
     a.out_mode = TC_OUT_BF16;
     if ((err = get_tmap2(P, &tc, out, false, N, M, ldo, 64, 128, 128)))
       return fail(TNL_ERR_CUDA, "tensor map (output) failed: %d", err);
+    if (in_o && in_o->ss_in) {  // folded RMSNorm of X: scale the output rows
+      a.ss_in = in_o->ss_in;
+      a.rms_n = in_o->rms_n;
+      a.rms_eps = in_o->rms_eps;
+    }
+    if (out_o && out_o->accumulate) a.reduce_add = 1;  // out += D (TMA reduce-add)
   }
   // CTA pairs (M=256 MMAs, each CTA streams half of the weight tile) once there are two token
   // tiles and a wide enough weight tile; TNL_PAIR_GEMM=0 disables
@@ -1337,7 +1390,8 @@ static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void*
 }
 
 static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y, int64_t ldy,
-                             void* ws, size_t ws_bytes, cudaStream_t st) {
+                             void* ws, size_t ws_bytes, cudaStream_t st, const tnl_fwd_opts* o = nullptr) {
+  const bool fold = o && (o->accumulate || o->ss_in);
   size_t o_f32, o_b0, o_b1;
   size_t need = ws_layout(P, M, &o_f32, &o_b0, &o_b1);
   if (ws_bytes < need) return fail(TNL_ERR_ARG, "workspace %zu < required %zu bytes", ws_bytes, need);
@@ -1347,6 +1401,9 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
   __nv_bfloat16* t1 = reinterpret_cast<__nv_bfloat16*>(w + o_b1);
   const int64_t rows_local = P->row_end - P->row_begin;
   const bool swap = M <= kSwapMaxM;
+  if (fold && (M <= kSwapMaxM || P->family == TNL_FAMILY_DENSE || P->plan_large == TNL_PLAN_CHAIN ||
+               (reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8 || (P->r_pad % 8)))
+    return fail(TNL_ERR_UNSUPPORTED, "folded residual / RMSNorm: prefill (M > %lld) cut plans only", (long long)kSwapMaxM);
   if (M <= kDecMaxM && P->decode_max_m && !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0)
     return forward_decode(P, x, M, ldx, y, ldy, ws, st);
   tnl_status s;
@@ -1387,9 +1444,12 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     if (splits > 1) {
       s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, tf, k1, true, splits, st);
       if (s) return s;
-      to_bf16(tf, t0, M * k1, st);
+      if (o && o->ss_in)
+        to_bf16_scaled(tf, t0, M, k1, o, st);
+      else
+        to_bf16(tf, t0, M * k1, st);
     } else {
-      s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, 1, st);
+      s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, 1, st, 0, o, nullptr);
       if (s) return s;
     }
     const __nv_bfloat16* tcur = t0;
@@ -1400,8 +1460,9 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
       tcur = t1;
       kc = P->r0p;
     }
-    return tc_step_p(P, tcur, kc, wout, kc, M, rows_local, kc, y, ldy, false, 1, st);
+    return tc_step_p(P, tcur, kc, wout, kc, M, rows_local, kc, y, ldy, false, 1, st, 0, nullptr, o);
   }
+  if (fold) return fail(TNL_ERR_UNSUPPORTED, "folded residual / RMSNorm: needs the persistent prefill path");
   // first step: T = X . Win^T  (Win = B_in or U1^T), K = cols
   if (swap) {
     const int64_t tiles = (k1 + 127) / 128;
@@ -1547,7 +1608,7 @@ namespace tnl {
 
 // T_gu = x . [B_g; B_u]^T (M x (rg + ru) bf16): the concatenated cut activation of gate and up
 static tnl_status mlp_tgu(tnl_mlp* B, const void* x, int64_t m, int64_t ldx, float* tgu32, __nv_bfloat16* tgu,
-                          cudaStream_t st) {
+                          cudaStream_t st, const tnl_fwd_opts* in_o = nullptr) {
   const int64_t rgu = B->rg + B->ru;
   const int64_t tiles1 = ((m + 127) / 128) * ((rgu + 255) / 256);
   const int64_t kb = (B->hidden + 63) / 64;
@@ -1555,14 +1616,17 @@ static tnl_status mlp_tgu(tnl_mlp* B, const void* x, int64_t m, int64_t ldx, flo
   tnl_status s;
   if (rgu <= 128 && ((m + 127) / 128) * ((rgu + 63) / 64) >= 96) {
     // enough 64-wide output tiles to fill the SMs: no split-K, bf16 straight from the epilogue
-    return tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st, 64);
+    return tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st, 64, in_o);
   }
   if (splits > 1) {
     if ((s = tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu32, rgu, true, splits, st))) return s;
-    to_bf16(tgu32, tgu, m * rgu, st);
+    if (in_o && in_o->ss_in)
+      to_bf16_scaled(tgu32, tgu, m, rgu, in_o, st);
+    else
+      to_bf16(tgu32, tgu, m * rgu, st);
     return TNL_OK;
   }
-  return tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st);
+  return tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st, 0, in_o);
 }
 
 static void mlp_ws_layout(const tnl_mlp* B, int64_t M, size_t off[4], size_t* total) {
@@ -2047,10 +2111,34 @@ tnl_status tnl_mlp_workspace_size(const tnl_mlp* B, int64_t m, size_t* bytes) {
   return TNL_OK;
 }
 
+static tnl_status mlp_forward_impl(const tnl_mlp* Bc, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
+                                   void* ws, size_t ws_bytes, void* stream, const tnl_fwd_opts* o);
+
 tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
                            void* ws, size_t ws_bytes, void* stream) {
+  return mlp_forward_impl(Bc, x, m, ldx, y, ldy, ws, ws_bytes, stream, nullptr);
+}
+
+tnl_status tnl_mlp_forward_ex(const tnl_mlp* Bc, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
+                              void* ws, size_t ws_bytes, const tnl_fwd_opts* opts, void* stream) {
+  return mlp_forward_impl(Bc, x, m, ldx, y, ldy, ws, ws_bytes, stream, opts);
+}
+
+static tnl_status mlp_forward_impl(const tnl_mlp* Bc, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
+                                   void* ws, size_t ws_bytes, void* stream, const tnl_fwd_opts* o) {
   tnl_mlp* B = const_cast<tnl_mlp*>(Bc);
   if (!B || !x || !y) return fail(TNL_ERR_ARG, "null argument");
+  // folded RMSNorm of the block input (ss_in) and accumulation into its output
+  tnl_fwd_opts in_o = {}, out_o = {};
+  const bool fold = o && (o->accumulate || o->ss_in);
+  if (fold) {
+    in_o.ss_in = o->ss_in;
+    in_o.rms_n = o->rms_n;
+    in_o.rms_eps = o->rms_eps;
+    out_o.accumulate = o->accumulate;
+    if (m <= kSwapMaxM) return fail(TNL_ERR_UNSUPPORTED, "folded residual / RMSNorm: prefill (M > %lld) only", (long long)kSwapMaxM);
+    if (o->ss_in && o->rms_n <= 0) return fail(TNL_ERR_ARG, "rms_n must be > 0");
+  }
   if (m == 0) return TNL_OK;
   size_t off[4], need;
   mlp_ws_layout(B, m, off, &need);
@@ -2070,7 +2158,7 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
     float* tgu32 = reinterpret_cast<float*>(w + off[1]);
     __nv_bfloat16* tgu = reinterpret_cast<__nv_bfloat16*>(w + off[2]);
     __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(w + off[3]);
-    tnl_status s = mlp_tgu(B, x, m, ldx, tgu32, tgu, st);
+    tnl_status s = mlp_tgu(B, x, m, ldx, tgu32, tgu, st, fold ? &in_o : nullptr);
     if (s) return s;
     CUtensorMap tt, tg, tu, th;
     int err;
@@ -2087,12 +2175,27 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
     da.u_off = (int32_t)B->rg;
     if ((err = launch_dual_silu(tt, tg, tu, th, da, st)))
       return fail(TNL_ERR_CUDA, "MLP dual kernel launch: %s", cudaGetErrorString((cudaError_t)err));
+    if (fold) return forward_tc(B->d, h, m, B->inter, y, ldy, lws, lbytes, st, &out_o);
     return tnl_forward(B->d, h, m, B->inter, y, ldy, lws, lbytes, stream);
   }
   static const bool no_gated = getenv("TNL_MLP_NO_GATED") && atoi(getenv("TNL_MLP_NO_GATED")) == 1;  // A/B
   if (!prefill && B->gated && !no_gated && m <= kDecMaxM && !((reinterpret_cast<uintptr_t>(x) & 15) || ldx % 8) &&
       !((reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8))
     return mlp_decode_gated(B, x, m, ldx, y, ldy, w + off[0], st);
+  if (fold && !B->fused) {
+    // unfused prefill with folds: gate/up normalise their input, down adds the residual
+    void* lws = w + off[0];
+    size_t a_, b_, c_, lbytes = 0;
+    for (const tnl_plan* P : {B->g, B->u, B->d}) lbytes = std::max(lbytes, ws_layout(P, m, &a_, &b_, &c_));
+    __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(w + off[1]);
+    __nv_bfloat16* u = reinterpret_cast<__nv_bfloat16*>(w + off[2]);
+    tnl_status s;
+    if ((s = tnl_forward_ex(B->g, x, m, ldx, g, B->inter, lws, lbytes, &in_o, stream))) return s;
+    if ((s = tnl_forward_ex(B->u, x, m, ldx, u, B->inter, lws, lbytes, &in_o, stream))) return s;
+    if (launch_pdl(silu_mul_bf16, dim3(grid_for(m * B->inter / 8)), dim3(256), 0, st, g, u, m * B->inter / 8))
+      return fail(TNL_ERR_CUDA, "silu_mul launch failed");
+    return tnl_forward_ex(B->d, g, m, B->inter, y, ldy, lws, lbytes, &out_o, stream);
+  }
   if (!B->fused || !prefill) {
     // unfused: three layer forwards + a SiLU*mul kernel
     void* lws = w + off[0];
@@ -2128,8 +2231,8 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   float* td32 = reinterpret_cast<float*>(w + off[2]);
   __nv_bfloat16* td = reinterpret_cast<__nv_bfloat16*>(w + off[3]);
   tnl_status s;
-  // 1. T_gu = x . [B_g; B_u]^T
-  if ((s = mlp_tgu(B, x, m, ldx, tgu32, tgu, st))) return s;
+  // 1. T_gu = x . [B_g; B_u]^T   (rows scaled by 1/rms(x) when the block's RMSNorm is folded)
+  if ((s = mlp_tgu(B, x, m, ldx, tgu32, tgu, st, fold ? &in_o : nullptr))) return s;
   // 2. T_d = (silu(T_g A_g^T) * (T_u A_u^T)) B_d^T, h on chip
   MlpArgs a;
   memset(&a, 0, sizeof a);
@@ -2172,8 +2275,9 @@ tnl_status tnl_mlp_forward(const tnl_mlp* Bc, const void* x, int64_t m, int64_t 
   if ((err = pair ? launch_mlp_mid_pair(tt, tag, tau, tbd, a, slices, st) : launch_mlp_mid(tt, tag, tau, tbd, a, slices, st)))
     return fail(TNL_ERR_CUDA, "MLP middle kernel launch: %s", cudaGetErrorString((cudaError_t)err));
   to_bf16(td32, td, m * B->rd, st);
-  // 3. y = T_d . A_d^T
-  return tc_step_p(B->d, td, B->rd, B->d->aout, B->d->r_pad, m, B->hidden, B->d->r_pad, y, ldy, false, 1, st);
+  // 3. y = T_d . A_d^T  (+ residual, RMSNorm statistics of y when folded)
+  return tc_step_p(B->d, td, B->rd, B->d->aout, B->d->r_pad, m, B->hidden, B->d->r_pad, y, ldy, false, 1, st, 0,
+                   nullptr, fold ? &out_o : nullptr);
 }
 
 tnl_status tnl_add_rmsnorm(void* x, int64_t ldx, const void* o, int64_t ldo, void* h, int64_t ldh, int64_t m,
@@ -2205,6 +2309,18 @@ tnl_status tnl_copy_async(void* dst, const void* src, size_t bytes, void* stream
   }();
   const int err = launch_copy16(dst, src, bytes, sms, static_cast<cudaStream_t>(stream));
   if (err) return fail(TNL_ERR_CUDA, "copy_async launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
+}
+
+tnl_status tnl_rms_stats(const void* x, int64_t ldx, int64_t m, int64_t n, float* ss, void* stream) {
+  if (!x || !ss) return fail(TNL_ERR_ARG, "null argument");
+  if (m < 0 || n <= 0 || n % 8 || ldx % 8 || ldx < n || (reinterpret_cast<uintptr_t>(x) & 15))
+    return fail(TNL_ERR_SHAPE, "rms_stats: m=%lld n=%lld ldx=%lld (n, ldx %% 8 == 0, 16-byte aligned x)", (long long)m,
+                (long long)n, (long long)ldx);
+  if (m == 0) return TNL_OK;
+  if (launch_pdl(row_sumsq_bf16, dim3((unsigned)m), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                 static_cast<const __nv_bfloat16*>(x), ldx, n, ss))
+    return fail(TNL_ERR_CUDA, "rms_stats launch failed");
   return TNL_OK;
 }
 
@@ -2299,6 +2415,21 @@ tnl_status tnl_forward(const tnl_plan* plan, const void* x, int64_t m, int64_t l
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (ldx % 8))
     return fail(TNL_ERR_SHAPE, "tensor-core plan needs 16-byte aligned x with ldx %% 8 == 0");
   return forward_tc(P, x, m, ldx, y, ldy, workspace, workspace_bytes, st);
+}
+
+tnl_status tnl_forward_ex(const tnl_plan* plan, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
+                          void* workspace, size_t workspace_bytes, const tnl_fwd_opts* opts, void* stream) {
+  if (!opts || (!opts->accumulate && !opts->ss_in))
+    return tnl_forward(plan, x, m, ldx, y, ldy, workspace, workspace_bytes, stream);
+  tnl_plan* P = const_cast<tnl_plan*>(plan);
+  if (!P || !x || !y) return fail(TNL_ERR_ARG, "null argument");
+  if (m <= 0) return m == 0 ? TNL_OK : fail(TNL_ERR_SHAPE, "negative token count");
+  if (ldx < P->cols || ldy < P->row_end - P->row_begin) return fail(TNL_ERR_SHAPE, "row pitch too small");
+  if (opts->ss_in && opts->rms_n <= 0) return fail(TNL_ERR_ARG, "rms_n must be > 0");
+  if (P->plan_large == TNL_PLAN_GENERIC || P->compute_dtype != TNL_BF16 || (reinterpret_cast<uintptr_t>(x) & 15) ||
+      ldx % 8)
+    return fail(TNL_ERR_UNSUPPORTED, "folded residual / RMSNorm: bf16 tensor-core plans only");
+  return forward_tc(P, x, m, ldx, y, ldy, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), opts);
 }
 
 tnl_status tnl_forward_host(tnl_plan* P, const void* x_host, int64_t m, void* y_host, void* stream) {

@@ -81,6 +81,8 @@ class QwenTNStack:
             blk["qo"] = (ctypes.c_void_p * 2)(blk["q"][2].handle.value, blk["o"][2].handle.value)
             self.layers.append(blk)
         self.fuse_qo = True
+        # prefill: residual adds and RMSNorms folded into the projections' epilogues (tnl_fwd_opts)
+        self.fold_prefill = True
         self._ws = None
         self._ws_side = None
         self._side = None
@@ -118,7 +120,8 @@ class QwenTNStack:
 
     def _buffers(self, m: int):
         mk = lambda n: torch.empty((m, n), dtype=self.dtype, device=self.device)  # noqa: E731
-        return {"h": mk(HIDDEN), "q": mk(QDIM), "k": mk(KVDIM), "v": mk(KVDIM), "o": mk(HIDDEN), "d": mk(HIDDEN)}
+        return {"h": mk(HIDDEN), "q": mk(QDIM), "k": mk(KVDIM), "v": mk(KVDIM), "o": mk(HIDDEN), "d": mk(HIDDEN),
+                "ss": torch.zeros((2, m), dtype=torch.float32, device=self.device)}
 
     @staticmethod
     def add_rmsnorm(x: torch.Tensor, o, h: torch.Tensor, eps: float = 1e-6) -> None:
@@ -130,11 +133,43 @@ class QwenTNStack:
                                          o.stride(0) if o is not None else 0, ctypes.c_void_p(h.data_ptr()),
                                          h.stride(0), m, n, float(eps), ctypes.c_void_p(stream)))
 
+    def _forward_prefill_folded(self, x: torch.Tensor, b, ws) -> torch.Tensor:
+        """Prefill pass with the residual adds and RMSNorms folded into the TN kernels
+        (tnl_fwd_opts): per norm one statistics read of x (tnl_rms_stats) replaces the add+norm pass;
+        q/k/v and gate/up scale their cut activations by 1/rms(x); o and the MLP add their output
+        into x with the TMA store's reduce-add (residual stream updated in place)."""
+        lib = N.load()
+        m = x.shape[0]
+        st = ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        ss = b["ss"][0]
+        eps = 1e-6
+        o_norm = N.FwdOpts(0, ss.data_ptr(), HIDDEN, eps)
+        o_acc = N.FwdOpts(1, None, 0, 0.0)
+        o_both = N.FwdOpts(1, ss.data_ptr(), HIDDEN, eps)
+        for blk in self.layers:
+            N.check(lib.tnl_rms_stats(vp(x), x.stride(0), m, HIDDEN, vp(ss), st))
+            for name in ("k", "v", "q"):
+                pl = blk[name][2]
+                N.check(lib.tnl_forward_ex(pl.handle, vp(x), m, x.stride(0), vp(b[name]), b[name].stride(0),
+                                           vp(ws), ws.numel(), ctypes.byref(o_norm), st))
+            pl = blk["o"][2]  # attention core: pass-through; x += o
+            N.check(lib.tnl_forward_ex(pl.handle, vp(b["q"]), m, b["q"].stride(0), vp(x), x.stride(0), vp(ws),
+                                       ws.numel(), ctypes.byref(o_acc), st))
+            N.check(lib.tnl_rms_stats(vp(x), x.stride(0), m, HIDDEN, vp(ss), st))
+            N.check(lib.tnl_mlp_forward_ex(blk["mlp"].handle, vp(x), m, x.stride(0), vp(x), x.stride(0), vp(ws),
+                                           ws.numel(), ctypes.byref(o_both), st))  # x += mlp(norm(x))
+        return x
+
     def forward(self, x: torch.Tensor, bufs=None) -> torch.Tensor:
         """One pass of all layers; x (M x 5120) is updated in place (residual stream)."""
         m = x.shape[0]
         ws = self.workspace(m)
         b = bufs or self._buffers(m)
+        if self.fold_prefill and m > 64:
+            if "ss" not in b:
+                b["ss"] = torch.zeros((2, m), dtype=torch.float32, device=self.device)
+            return self._forward_prefill_folded(x, b, ws)
         fork = self.concurrent_kv and m <= 64
         if fork:
             ws_side = self._side_workspace(m)

@@ -583,6 +583,61 @@ def test_add_rmsnorm(m, n, with_o):
     assert rel(ref_h.cpu().numpy(), h.float().cpu().numpy()) <= 1e-2
 
 
+@pytest.mark.parametrize("spec", [("tucker", (5120, 5120), 1, (256, 256)), ("tt", (160, 160, 64, 80), 2, (64, 64, 64))])
+def test_forward_ex_folded_norm_accumulate(spec):
+    """tnl_forward_ex (prefill): y += f(x / rms(x)) with the statistics from tnl_rms_stats, vs the
+    unfolded path (normalised input through tnl_forward, then a torch add)."""
+    import ctypes
+
+    from paper_2602_01613_b200 import _native as N
+
+    f, ms, rm, rk = spec
+    L = O.synthetic_layer(f, ms, rm, rk, seed=52_000)
+    layer, _ = to_layer(L, round_bf16=True)
+    rows, cols = layer.matrix_shape
+    m = 300
+    torch.manual_seed(2)
+    x = (3 * torch.randn(m, cols, device=DEV)).to(torch.bfloat16)
+    r = torch.randn(m, rows, device=DEV).to(torch.bfloat16)
+    lib = N.load()
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ss = torch.empty(m, device=DEV)
+    N.check(lib.tnl_rms_stats(ctypes.c_void_p(x.data_ptr()), cols, m, cols, ctypes.c_void_p(ss.data_ptr()), s))
+    torch.cuda.synchronize()
+    want = (x.float() ** 2).sum(1)
+    assert rel(want.cpu().numpy(), ss.cpu().numpy()) <= 1e-5
+    h = (x.float() * torch.rsqrt(want[:, None] / cols + 1e-6)).to(torch.bfloat16)
+    pl = layer.plan(torch.bfloat16)
+    ref = pl.forward(h).float() + r.float()
+    y = r.clone()
+    ws = pl.workspace(m)
+    o = N.FwdOpts(1, ss.data_ptr(), cols, 1e-6)
+    N.check(lib.tnl_forward_ex(pl.handle, ctypes.c_void_p(x.data_ptr()), m, cols, ctypes.c_void_p(y.data_ptr()), rows,
+                               ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.byref(o), s))
+    torch.cuda.synchronize()
+    assert rel(ref.cpu().numpy(), y.float().cpu().numpy()) <= 1e-2
+
+
+@pytest.mark.parametrize("m", [300, 1024])
+def test_qwen_stack_folded_prefill(m):
+    """cfg4 prefill with the residual adds and RMSNorms folded into the projections' epilogues
+    equals the pass with separate add+norm kernels (bf16 pipelines; rounding differs)."""
+    from paper_2602_01613_b200.qwen_stack import QwenTNStack
+
+    st = QwenTNStack(6)  # Tucker-2 R256 MLP (dual path) on layers 0-1 / 4-5, TT r64 / TR4 fused on 2 / 3
+    torch.manual_seed(3)
+    x0 = torch.randn(m, 5120, device=DEV).to(torch.bfloat16)
+    outs = {}
+    for fold in (True, False):
+        st.fold_prefill = fold
+        x = x0.clone()
+        st.forward(x)
+        torch.cuda.synchronize()
+        assert torch.isfinite(x.float()).all()
+        outs[fold] = x.float().cpu().numpy()
+    assert rel(outs[False], outs[True]) <= BF16_TOL
+
+
 def test_qwen_stack_decode_matches_prefill():
     """Regression: every plan and MLP block of a stack share one workspace; decode (M <= 64) must
     give the same tokens as the prefill path (per-token independence), which failed when an MLP's

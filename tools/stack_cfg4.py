@@ -20,6 +20,7 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--unfused-mlp", action="store_true")
 ap.add_argument("--serial-kv", action="store_true", help="k/v on the main stream (no fork)")
 ap.add_argument("--no-fuse-qo", action="store_true", help="decode: q and o as two tnl_forward calls")
+ap.add_argument("--no-fold", action="store_true", help="prefill: separate residual-add + RMSNorm passes")
 a = ap.parse_args()
 HBM, TC = 6554.6e9, 1635e12
 
@@ -27,6 +28,7 @@ t0 = time.time()
 st = QwenTNStack(a.layers, fused_mlp=not a.unfused_mlp)
 st.concurrent_kv = not a.serial_kv
 st.fuse_qo = not a.no_fuse_qo
+st.fold_prefill = not a.no_fold
 build_s = time.time() - t0
 P = st.param_count()
 F = st.chain_flops_per_token()
