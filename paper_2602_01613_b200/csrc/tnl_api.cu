@@ -1441,7 +1441,13 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     const int64_t tiles1 = ((M + 127) / 128) * ((k1 + 255) / 256);
     const int64_t kb1 = (P->cols + 63) / 64;
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb1 / 8));
-    if (splits > 1) {
+    static const bool no_nsplit = getenv("TNL_STEP1_NSPLIT") && atoi(getenv("TNL_STEP1_NSPLIT")) == 0;  // A/B
+    if (!no_nsplit && splits > 1 && k1 >= 128 && k1 % 128 == 0 && ((M + 127) / 128) * 2 >= 96) {
+      // split the cut dimension instead of K: two half-width tiles per token tile, full K each ->
+      // no fp32 partials, no memset, no conversion pass (cfg4 q, Tucker-2 R256 at M=8192: 72.6 -> 65.2 us)
+      s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, 1, st, (int)(k1 / 2), o, nullptr);
+      if (s) return s;
+    } else if (splits > 1) {
       s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, tf, k1, true, splits, st);
       if (s) return s;
       if (o && o->ss_in)
