@@ -35,7 +35,7 @@ struct PairSmem {
   static constexpr size_t bytes = 1024 + (size_t)STAGES * (P_A_STAGE + B_STAGE) + 2 * P_C_CHUNK + 256;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool SCALE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcGemmArgs args, int tiles_m2, int tiles_n,
@@ -149,7 +149,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const int lrow = q * 32 + lane_id();
       const int row = tm * PBM + lrow;
       if (args.out_mode == TC_OUT_BF16) {
-        const float rscale = row_rms_scale(args, row);
+        const float rscale = SCALE ? row_rms_scale(args, row) : 1.f;
         for (int c0 = 0; c0 < BN; c0 += 64) {
           uint8_t* stage = sC + (chunk_ct & 1) * P_C_CHUNK;
           if (et == 0) tma_store_wait_read_le1();
@@ -158,7 +158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           for (int c = 0; c < 64; c += 16) {
             float v[16];
             tmem_ld16(d + c0 + c, v);
-            if (args.ss_in) {
+            if constexpr (SCALE) {  // folded RMSNorm of the step's input rows
 #pragma unroll
               for (int e = 0; e < 16; ++e) v[e] *= rscale;
             }
@@ -227,13 +227,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem);
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool SCALE>
 int launch_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcGemmArgs& args,
                 int splits, cudaStream_t st) {
   constexpr size_t smem = PairSmem<BN, STAGES>::bytes;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<BN, STAGES, SCALE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return (int)e;
     attr = true;
@@ -251,7 +251,7 @@ int launch_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<BN, STAGES>, a, b, c, args, tiles_m2, tiles_n, splits);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<BN, STAGES, SCALE>, a, b, c, args, tiles_m2, tiles_n, splits);
   count_launch();
   return (int)e;
 }
@@ -262,9 +262,9 @@ int launch_tc_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtens
                         int bn, int splits, cudaStream_t st) {
   switch (bn) {
     case 128:
-      return launch_pair<128, 6>(a, b, c, args, splits, st);
+      return args.ss_in ? launch_pair<128, 6, true>(a, b, c, args, splits, st) : launch_pair<128, 6, false>(a, b, c, args, splits, st);
     case 256:
-      return launch_pair<256, 5>(a, b, c, args, splits, st);
+      return args.ss_in ? launch_pair<256, 5, true>(a, b, c, args, splits, st) : launch_pair<256, 5, false>(a, b, c, args, splits, st);
     default:
       return (int)cudaErrorInvalidValue;
   }

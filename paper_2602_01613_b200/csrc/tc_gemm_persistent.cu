@@ -35,7 +35,7 @@ struct PSmem {
   static constexpr size_t bytes = 1024 + (size_t)STAGES * (A_STAGE + B_STAGE) + 2 * C_CHUNK + 256;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool SCALE>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA,
                               const __grid_constant__ CUtensorMap tmB,
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(192, 1)
       const int lrow = q * 32 + lane_id();
       const int row = tm * BM + lrow;
       if (args.out_mode == TC_OUT_BF16) {
-        const float rscale = row_rms_scale(args, row);
+        const float rscale = SCALE ? row_rms_scale(args, row) : 1.f;
         for (int c0 = 0; c0 < BN; c0 += 64) {
           uint8_t* stage = sC + (chunk_ct & 1) * C_CHUNK;
           // the TMA store that used this staging buffer two chunks ago must have read it
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(192, 1)
           for (int c = 0; c < 64; c += 16) {
             float v[16];
             tmem_ld16(d + c0 + c, v);
-            if (args.ss_in) {
+            if constexpr (SCALE) {  // folded RMSNorm of the step's input rows
 #pragma unroll
               for (int e = 0; e < 16; ++e) v[e] *= rscale;
             }
@@ -225,13 +225,13 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool SCALE>
 int launch_p(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcGemmArgs& args,
              int splits, int max_ctas, bool pdl, cudaStream_t st) {
   constexpr size_t smem = PSmem<BN, STAGES>::bytes;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_persistent_kernel<BN, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_persistent_kernel<BN, STAGES, SCALE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
     attr = true;
@@ -248,7 +248,7 @@ int launch_p(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, c
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_persistent_kernel<BN, STAGES>, a, b, c, args, tiles_m,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_persistent_kernel<BN, STAGES, SCALE>, a, b, c, args, tiles_m,
                                      tiles_n, splits);
   count_launch();
   return (int)e;
@@ -261,11 +261,11 @@ int launch_tc_gemm_persistent(const CUtensorMap& a, const CUtensorMap& b, const 
                               cudaStream_t st) {
   switch (bn) {
     case 64:
-      return launch_p<64, 8>(a, b, c, args, splits, max_ctas, pdl, st);
+      return args.ss_in ? launch_p<64, 8, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<64, 8, false>(a, b, c, args, splits, max_ctas, pdl, st);
     case 128:
-      return launch_p<128, 5>(a, b, c, args, splits, max_ctas, pdl, st);
+      return args.ss_in ? launch_p<128, 5, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<128, 5, false>(a, b, c, args, splits, max_ctas, pdl, st);
     case 256:
-      return launch_p<256, 3>(a, b, c, args, splits, max_ctas, pdl, st);
+      return args.ss_in ? launch_p<256, 3, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<256, 3, false>(a, b, c, args, splits, max_ctas, pdl, st);
     default:
       return (int)cudaErrorInvalidValue;
   }

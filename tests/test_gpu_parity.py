@@ -615,7 +615,8 @@ def test_forward_ex_folded_norm_accumulate(spec):
     N.check(lib.tnl_forward_ex(pl.handle, ctypes.c_void_p(x.data_ptr()), m, cols, ctypes.c_void_p(y.data_ptr()), rows,
                                ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.byref(o), s))
     torch.cuda.synchronize()
-    assert rel(ref.cpu().numpy(), y.float().cpu().numpy()) <= 1e-2
+    # y is accumulated in bf16 (TMA reduce-add): one extra bf16 rounding of the sum vs the fp32 ref
+    assert rel(ref.cpu().numpy(), y.float().cpu().numpy()) <= BF16_TOL
 
 
 @pytest.mark.parametrize("m", [300, 1024])
