@@ -40,9 +40,12 @@ struct FSmem {
   static size_t bytes(int kbB, int nT) {
     return 1024 + (size_t)kbB * WBLK + (size_t)nT * 2 * WBLK + 2 * X_BLK + (size_t)kbB * T_BLK + 256;
   }
+  // large gated boundary (gate + up cut > 256): B_in reuses the gate's A blocks once the gate MMAs
+  // have completed, so only the A_out blocks, x and T take space
+  static size_t bytes_large(int kbB) { return 1024 + (size_t)kbB * WBLK + 2 * X_BLK + (size_t)kbB * T_BLK + 256; }
 };
 
-template <int BN, bool GATED>
+template <int BN, bool GATED, int KMAX>
 __global__ void __launch_bounds__(FT, 1)
     dec_fused_kernel(const __grid_constant__ CUtensorMap tmWo, const __grid_constant__ CUtensorMap tmT,
                      const __grid_constant__ CUtensorMap tmWi, const FusedArgs a) {
@@ -52,19 +55,22 @@ __global__ void __launch_bounds__(FT, 1)
                                              ~uintptr_t(1023));
   const int kbB = (a.kB + 63) / 64;
   const int nT = (a.nA + 127) / 128;
+  constexpr bool LARGE = KMAX > 4;        // B_in aliases the gate's A blocks (loaded after their MMAs)
   uint8_t* sWo = smem;                    // kbB blocks
-  uint8_t* sWi = sWo + kbB * WBLK;        // nT x 2 blocks (then the D_A transpose stage)
-  uint8_t* sX = sWi + nT * 2 * WBLK;      // x operand: 2 blocks
+  uint8_t* sWi = LARGE ? sWo : sWo + kbB * WBLK;  // nT x 2 blocks (then the D_A transpose stage)
+  uint8_t* sX = LARGE ? sWo + kbB * WBLK : sWi + nT * 2 * WBLK;  // x operand: 2 blocks
   uint8_t* sT = sX + 2 * SM::X_BLK;       // kbB bf16 T blocks
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + kbB * SM::T_BLK);
   uint64_t* wfull = bars;
   uint64_t* stg = bars + 1;  // [4]
-  uint64_t* tfull = bars + 10;  // [4]: T block kb converted (one arrive per epilogue warp)
+  uint64_t* tfull = bars + 18;  // [8]: T block kb converted (one arrive per epilogue warp)
   uint64_t* bdone = bars + 6;
   uint64_t* xfull = bars + 7;
   uint64_t* adone = bars + 8;
   uint64_t* flagbar = bars + 9;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* gdone = bars + 16;   // LARGE: the gate's phase-B MMAs have completed (its A blocks are free)
+  uint64_t* wfull2 = bars + 17;  // LARGE: B_in landed
   uint32_t* last_flag = tmem_slot + 1;
 
   const int tile = blockIdx.x;
@@ -85,11 +91,13 @@ __global__ void __launch_bounds__(FT, 1)
     tma_prefetch_desc(&tmWi);
     mbar_init(wfull, 1);
     for (int s = 0; s < 4; ++s) mbar_init(&stg[s], 1);
-    for (int kb = 0; kb < 4; ++kb) mbar_init(&tfull[kb], FEPI / 32);
+    for (int kb = 0; kb < KMAX; ++kb) mbar_init(&tfull[kb], FEPI / 32);
     mbar_init(bdone, 1);
     mbar_init(xfull, 1);
     mbar_init(adone, 1);
     mbar_init(flagbar, 1);
+    mbar_init(gdone, 1);
+    mbar_init(wfull2, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<256>(tmem_slot);
@@ -106,16 +114,24 @@ __global__ void __launch_bounds__(FT, 1)
   if (warp == 0) {
     if (elect_one()) {
       // both layers' weights first (independent of the previous kernel)
-      mbar_arrive_expect_tx(wfull, (kbB + 2 * nT) * WBLK);
+      mbar_arrive_expect_tx(wfull, (kbB + (LARGE ? 0 : 2 * nT)) * WBLK);
       const uint64_t pol = policy_evict_first();
       for (int kb = 0; kb < kbB; ++kb)
         tma_load_2d_hint(sWo + kb * WBLK, &tmWo, wfull, kb * 64, tile * 128, pol);
-      for (int t = 0; t < nT; ++t)
-        for (int h = 0; h < 2; ++h)
-          tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull, tile * 128 + h * 64, t * 128, pol);
+      if (!LARGE)
+        for (int t = 0; t < nT; ++t)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull, tile * 128 + h * 64, t * 128, pol);
       TRACE(2);
       pdl_wait();
       TRACE(3);
+      if constexpr (LARGE) {  // B_in into the gate's A blocks once the gate MMAs have read them
+        mbar_wait(gdone, 0);
+        mbar_arrive_expect_tx(wfull2, 2 * nT * WBLK);
+        for (int t = 0; t < nT; ++t)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull2, tile * 128 + h * 64, t * 128, pol);
+      }
     }
     __syncwarp();
     // T_{l-1} was read only by the previous kernel, which has completed: zero this CTA's slice
@@ -141,9 +157,11 @@ __global__ void __launch_bounds__(FT, 1)
         const int kk = up ? kb - kg : kb;
 #pragma unroll
         for (int k = 0; k < 4; ++k) mma_bf16_ss(d, ad + 2 * k, bd + 128 * k, idesc, (kk | k) != 0);
+        if (LARGE && kb == kg - 1) mma_commit(gdone);
       }
       mma_commit(bdone);
       mbar_wait(xfull, 0);
+      if constexpr (LARGE) mbar_wait(wfull2, 0);
       tc_fence_after();
       for (int t = 0; t < nT; ++t)
         for (int h = 0; h < 2; ++h) {
@@ -169,9 +187,9 @@ __global__ void __launch_bounds__(FT, 1)
     constexpr int ITEMS = 64 * QPR;              // per k-block
     constexpr int PER = ITEMS >= FEPI ? ITEMS / FEPI : 1;
     {
-      float4 v[4][PER];
+      float4 v[KMAX][PER];
 #pragma unroll
-      for (int kb = 0; kb < 4; ++kb)
+      for (int kb = 0; kb < KMAX; ++kb)
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
           const int e = et + u * FEPI;
@@ -181,7 +199,7 @@ __global__ void __launch_bounds__(FT, 1)
         }
       if (et == 0) TRACE(12);
 #pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
+      for (int kb = 0; kb < KMAX; ++kb) {
         if (kb >= kbB) break;
         const uint32_t dst = smem_u32(sT) + kb * SM::T_BLK;
 #pragma unroll
@@ -291,17 +309,18 @@ __global__ void __launch_bounds__(FT, 1)
 #undef TRACE
 }
 
-template <int BN, bool GATED>
+template <int BN, bool GATED, int KMAX>
 int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi, const FusedArgs& a,
                  int grid, cudaStream_t st) {
   // plain boundaries (decode stacks: 40-64 CTAs) reserve the full layout, one CTA per SM; the gated
   // MLP boundary (inter/128 = 200 CTAs at Qwen3 shapes) takes only what its ranks need, so two
   // CTAs share an SM and the grid runs in one wave
-  const size_t smem = GATED ? FSmem::bytes((a.kB + 63) / 64, (a.nA + 127) / 128) : FSmem::bytes(4, 2);
+  const size_t smem = KMAX > 4 ? FSmem::bytes_large((a.kB + 63) / 64)
+                     : GATED ? FSmem::bytes((a.kB + 63) / 64, (a.nA + 127) / 128) : FSmem::bytes(4, 2);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dec_fused_kernel<BN, GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)FSmem::bytes(4, 2));
+    cudaError_t e = cudaFuncSetAttribute(dec_fused_kernel<BN, GATED, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(KMAX > 4 ? FSmem::bytes_large(KMAX) : FSmem::bytes(4, 2)));
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
@@ -315,7 +334,7 @@ int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap&
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dec_fused_kernel<BN, GATED>, wo, t, wi, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dec_fused_kernel<BN, GATED, KMAX>, wo, t, wi, a);
   count_launch();
   return (int)e;
 }
@@ -324,15 +343,22 @@ int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap&
 
 int launch_dec_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi, const FusedArgs& a,
                      int grid, cudaStream_t st) {
-  if (a.kB > 256 || a.nA > 256 || a.rows % 128) return (int)cudaErrorInvalidValue;
-  if (a.kg) {
-    if (a.tokens <= 16) return launch_fused<16, true>(wo, t, wi, a, grid, st);
-    if (a.tokens <= 32) return launch_fused<32, true>(wo, t, wi, a, grid, st);
-    return launch_fused<64, true>(wo, t, wi, a, grid, st);
+  if (a.nA > 256 || a.rows % 128) return (int)cudaErrorInvalidValue;
+  if (a.kB > 256) {
+    // large gated boundary: B_in (2 * nT blocks) must fit in the gate's A blocks
+    if (!a.kg || a.kB > 512 || a.kg < 2 * ((a.nA + 127) / 128)) return (int)cudaErrorInvalidValue;
+    if (a.tokens <= 16) return launch_fused<16, true, 8>(wo, t, wi, a, grid, st);
+    if (a.tokens <= 32) return launch_fused<32, true, 8>(wo, t, wi, a, grid, st);
+    return launch_fused<64, true, 8>(wo, t, wi, a, grid, st);
   }
-  if (a.tokens <= 16) return launch_fused<16, false>(wo, t, wi, a, grid, st);
-  if (a.tokens <= 32) return launch_fused<32, false>(wo, t, wi, a, grid, st);
-  return launch_fused<64, false>(wo, t, wi, a, grid, st);
+  if (a.kg) {
+    if (a.tokens <= 16) return launch_fused<16, true, 4>(wo, t, wi, a, grid, st);
+    if (a.tokens <= 32) return launch_fused<32, true, 4>(wo, t, wi, a, grid, st);
+    return launch_fused<64, true, 4>(wo, t, wi, a, grid, st);
+  }
+  if (a.tokens <= 16) return launch_fused<16, false, 4>(wo, t, wi, a, grid, st);
+  if (a.tokens <= 32) return launch_fused<32, false, 4>(wo, t, wi, a, grid, st);
+  return launch_fused<64, false, 4>(wo, t, wi, a, grid, st);
 }
 
 }  // namespace tnl

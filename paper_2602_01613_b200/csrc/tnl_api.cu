@@ -1125,7 +1125,7 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
 // ---------------------------------------------------------------------------
 static constexpr int64_t kSwapMaxM = 64;  // tokens: swap-AB (weights on the M side) below this
 
-constexpr size_t kDecHeadBytes = sizeof(float) * 64 * 256;  // decode accumulator (r_pad <= 256)
+constexpr size_t kDecHeadBytes = sizeof(float) * 64 * 512;  // decode accumulator (r_pad <= 256; 512 for a stacked gate/up cut)
 // one decode slot = accumulator + counter + the GEMV variant's T scratch (M <= 8, r_pad <= 256).
 // Every workspace layout reserves kDecSlots slots at fixed offsets, so a decode call may run on
 // slot 1 (a forked stream) concurrently with one on slot 0 (MLP gate || up) and no layout ever
@@ -1939,9 +1939,12 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
   CUDA_TRY(cudaStreamCreateWithFlags(&B->side, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&B->ev_fork, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&B->ev_join, cudaEventDisableTiming));
+  // gate + up cut <= 256: everything resident; <= 512: down's B_in reuses the gate's A blocks
+  // (needs the gate's cut to cover down's input blocks)
   B->gated = !(flags & 1) && cut(gate) && cut(up) && cut(down) && gate->decode_max_m && up->decode_max_m &&
-              down->decode_max_m && B->rg + B->ru <= 256 && down->r_pad <= 256 && B->inter % 128 == 0 &&
-              B->hidden % 128 == 0;
+             down->decode_max_m && down->r_pad <= 256 && B->inter % 128 == 0 && B->hidden % 128 == 0 &&
+             (B->rg + B->ru <= 256 ||
+              (B->rg + B->ru <= 512 && B->rg / 64 >= 2 * ((down->r_pad + 127) / 128)));
   if (B->gated) {
     const int64_t rgu = B->rg + B->ru;
     const size_t bytes = 2 * rgu * B->inter;

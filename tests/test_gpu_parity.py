@@ -470,6 +470,24 @@ def test_mlp_decode_gated_cfg3(m):
         assert rel(ref, y) <= 2 * BF16_TOL
 
 
+@pytest.mark.parametrize("m", [1, 64])
+def test_mlp_decode_gated_large_rank(m):
+    """Decode MLP with gate + up cut 512 (Tucker-2 R256, the cfg4 edge layers): the large gated
+    boundary (down's B_in loaded into the gate's A blocks once the gate MMAs completed) vs the oracle."""
+    from paper_2602_01613_b200.mlp import TNMLP
+
+    Ls = [O.synthetic_layer("tucker", sh, 1, (256, 256), seed=51_200 + i) for i, sh in
+          enumerate([(25600, 5120), (25600, 5120), (5120, 25600)])]
+    pairs = [to_layer(L, round_bf16=True) for L in Ls]
+    mlp = TNMLP(*[p[0] for p in pairs])
+    x = O.round_bf16(O.synthetic_x(m, 5120, seed=51_209))
+    xt = torch.tensor(x, dtype=torch.bfloat16, device=DEV)
+    ys = [mlp(xt).float().cpu().numpy() for _ in range(3)]
+    ref = _mlp_ref(*[p[1] for p in pairs], x)
+    for y in ys:
+        assert rel(ref, y) <= 2 * BF16_TOL
+
+
 def test_qwen_stack_fused_mlp_matches_unfused():
     """cfg4 driver: the stack with fused TNMLP blocks (TT r64 / TR4 layers) equals the unfused stack."""
     from paper_2602_01613_b200.qwen_stack import QwenTNStack
