@@ -2,9 +2,21 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace tnl {
+
+// One-time per-(kernel, device) setup such as cudaFuncSetAttribute: the attribute is per-device
+// state, so a process that drives several GPUs must set it once on each of them.
+struct AttrOnce {
+  std::atomic<unsigned long long> mask{0};
+  bool needed(int* dev) {
+    if (cudaGetDevice(dev) != cudaSuccess) *dev = 0;
+    return !((mask.load(std::memory_order_acquire) >> (*dev & 63)) & 1ull);
+  }
+  void done(int dev) { mask.fetch_or(1ull << (dev & 63), std::memory_order_release); }
+};
 
 // Per-thread count of libtnl kernel launches (tnl_launch_count).
 void count_launch(int64_t n = 1);

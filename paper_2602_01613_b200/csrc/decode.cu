@@ -268,12 +268,13 @@ template <int BN, int STAGES, bool ACT_F32>
 int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& y, const DecArgs& a,
                int splits, cudaStream_t st) {
   constexpr size_t smem = DecSmem<BN, STAGES, ACT_F32>::bytes;
-  static bool attr = false;
-  if (!attr) {
+  static AttrOnce attr;
+  int attr_dev = 0;
+  if (attr.needed(&attr_dev)) {
     cudaError_t e = cudaFuncSetAttribute(dec_kernel<BN, STAGES, ACT_F32>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr.done(attr_dev);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.M_rows + BM - 1) / BM, 1, splits);

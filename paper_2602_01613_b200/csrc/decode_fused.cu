@@ -317,12 +317,13 @@ int launch_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap&
   // CTAs share an SM and the grid runs in one wave
   const size_t smem = KMAX > 4 ? FSmem::bytes_large((a.kB + 63) / 64)
                      : GATED ? FSmem::bytes((a.kB + 63) / 64, (a.nA + 127) / 128) : FSmem::bytes(4, 2);
-  static bool attr = false;
-  if (!attr) {
+  static AttrOnce attr;
+  int attr_dev = 0;
+  if (attr.needed(&attr_dev)) {
     cudaError_t e = cudaFuncSetAttribute(dec_fused_kernel<BN, GATED, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(KMAX > 4 ? FSmem::bytes_large(KMAX) : FSmem::bytes(4, 2)));
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr.done(attr_dev);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);

@@ -216,11 +216,12 @@ bool dual_silu_ok(const DualArgs& a) {
 int launch_dual_silu(const CUtensorMap& t, const CUtensorMap& g, const CUtensorMap& u, const CUtensorMap& h,
                      const DualArgs& a, cudaStream_t st) {
   if (!dual_silu_ok(a)) return (int)cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  static AttrOnce attr;
+  int attr_dev = 0;
+  if (attr.needed(&attr_dev)) {
     cudaError_t e = cudaFuncSetAttribute(dual_silu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D_SMEM);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr.done(attr_dev);
   }
   const int tiles_m = ((a.M + DBM - 1) / DBM + 1) / 2 * 2, tiles_n = (a.N + DBN - 1) / DBN;
   // output-tile slices per token tile: waves nearly full (one CTA per SM), ~2 tiles of fixed

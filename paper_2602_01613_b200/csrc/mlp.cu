@@ -841,13 +841,14 @@ int launch_mlp_mid(const CUtensorMap& t, const CUtensorMap& ag, const CUtensorMa
   if (a.rg % 64 || a.ru % 64 || a.rd % 64 || a.rg > 128 || a.ru > 128 || a.rd > 256 || a.inter % CH ||
       L.total > 227 * 1024)
     return (int)cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  static AttrOnce attr;
+  int attr_dev = 0;
+  if (attr.needed(&attr_dev)) {
     cudaError_t e = cudaFuncSetAttribute(mlp_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mlp_mid_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr.done(attr_dev);
   }
   const MlpTsLayout Lt = mlp_ts_layout(a);
   static const int ts_env = getenv("TNL_MLP_SS") ? 0 : 1;
@@ -884,11 +885,12 @@ int launch_mlp_mid_pair(const CUtensorMap& t, const CUtensorMap& ag, const CUten
                         const MlpArgs& a, int slices, cudaStream_t st) {
   if (!mlp_pair_ok(a)) return (int)cudaErrorInvalidValue;
   const MlpPairLayout L = mlp_pair_layout(a);
-  static bool attr = false;
-  if (!attr) {
+  static AttrOnce attr;
+  int attr_dev = 0;
+  if (attr.needed(&attr_dev)) {
     cudaError_t e = cudaFuncSetAttribute(mlp_mid_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr.done(attr_dev);
   }
   const int tiles = (a.M + 127) / 128;
   cudaLaunchConfig_t cfg = {};

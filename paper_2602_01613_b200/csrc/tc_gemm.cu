@@ -186,12 +186,13 @@ template <int BN, int STAGES>
 int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const TcGemmArgs& args, int splits,
                 bool pdl, cudaStream_t stream) {
   constexpr size_t smem = smem_bytes<BN, STAGES>();
-  static bool attr_set = false;  // benign race: idempotent attribute set
-  if (!attr_set) {
+  static AttrOnce attr_set;  // benign race: idempotent attribute set
+  int attr_dev = 0;
+  if (attr_set.needed(&attr_dev)) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    attr_set = true;
+    attr_set.done(attr_dev);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((args.M + BM - 1) / BM, (args.N + BN - 1) / BN, splits);

@@ -231,12 +231,13 @@ template <int BN, int STAGES, bool SCALE>
 int launch_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcGemmArgs& args,
                 int splits, cudaStream_t st) {
   constexpr size_t smem = PairSmem<BN, STAGES>::bytes;
-  static bool attr = false;
-  if (!attr) {
+  static AttrOnce attr;
+  int attr_dev = 0;
+  if (attr.needed(&attr_dev)) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<BN, STAGES, SCALE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr.done(attr_dev);
   }
   const int tiles_m2 = (args.M + 2 * PBM - 1) / (2 * PBM), tiles_n = (args.N + BN - 1) / BN;
   const int tiles = tiles_m2 * tiles_n * splits;

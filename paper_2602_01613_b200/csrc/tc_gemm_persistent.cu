@@ -229,12 +229,13 @@ template <int BN, int STAGES, bool SCALE>
 int launch_p(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcGemmArgs& args,
              int splits, int max_ctas, bool pdl, cudaStream_t st) {
   constexpr size_t smem = PSmem<BN, STAGES>::bytes;
-  static bool attr = false;
-  if (!attr) {
+  static AttrOnce attr;
+  int attr_dev = 0;
+  if (attr.needed(&attr_dev)) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_persistent_kernel<BN, STAGES, SCALE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr.done(attr_dev);
   }
   const int tiles_m = (args.M + BM - 1) / BM, tiles_n = (args.N + BN - 1) / BN;
   const int tiles = tiles_m * tiles_n * splits;
