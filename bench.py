@@ -446,6 +446,33 @@ def main():
         blk.close()
         del xs, yp
 
+    # secondary (cfg5, N > 1 only): prefill of the cfg3 gate projection sharded over the ranks —
+    # output-mode sharded (each rank owns 25600/N rows of the leading output mode, one NCCL
+    # all-gather over NVLink assembles y) and token-sharded (no collective); max over ranks
+    sharded = None
+    if world > 1 and not args.no_prefill:
+        try:
+            from paper_2602_01613_b200.sharded import OutputShardedLayer, TokenShardedLayer
+
+            fam, ms_, rm, rk = S.CFG3_GATE
+            lay = S.make_layer(fam, ms_, rm, rk, seed=30_064)
+            Mp = 8192
+            xs = torch.randn(Mp, 5120, device="cuda").to(torch.bfloat16)
+            osl = OutputShardedLayer(lay, dtype=torch.bfloat16, device=torch.device("cuda", local))
+            tsl = TokenShardedLayer(lay, dtype=torch.bfloat16, device=torch.device("cuda", local))
+            yfull = torch.empty(Mp, 25600, device="cuda", dtype=torch.bfloat16)
+            ms_o = time_graph(lambda: osl.forward(xs, out=yfull), 10, 3, torch, dist)
+            ms_t = time_graph(lambda: tsl.forward(xs), 10, 3, torch, dist)
+            sharded = {"layer": f"TT r64 {ms_}", "M": Mp, "world": world,
+                       "output_sharded": {"ms": ms_o, "tokens_per_s": Mp / (ms_o / 1e3),
+                                          "allgather_bytes_per_rank": 2 * Mp * 25600 // world,
+                                          "how": "row-restricted plan per rank + all_gather_into_tensor (NCCL) + "
+                                                 "[G][M][rows/G] -> (M, rows) placement; max over ranks"},
+                       "token_sharded": {"ms": ms_t, "tokens_per_s": Mp / (ms_t / 1e3),
+                                         "how": "M/N tokens per rank, full weights, no collective; max over ranks"}}
+        except Exception as exc:  # report, never fail the headline run
+            sharded = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # secondary: cfg1 (BASELINE configs[0]) TT (64,64|64,64) r32, M=16 — fp32 generic chain (the
     # reference-precision path, CUDA-core bound) and bf16 plans; 8 distinct layers (> L2? no: 2 MB)
     cfg1 = None
@@ -540,6 +567,7 @@ def main():
         "replay_stats": rep_stats,
         "prefill_cfg3": prefill,
         "cfg1_m16": cfg1,
+        "sharded_prefill_cfg5": sharded,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
