@@ -73,11 +73,19 @@ class OutputShardedLayer:
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         m = x.shape[0]
         per = self.row_range[1] - self.row_range[0]
-        y_local = self.local_forward(x)  # (M, rows/G)
-        flat = torch.empty((self.world * m, per), dtype=y_local.dtype, device=y_local.device)
-        dist.all_gather_into_tensor(flat, y_local.contiguous(), group=self.group)
+        # this rank's rows are computed straight into its slot of the gather buffer, and the
+        # all-gather runs in place (input = output slot `rank`): no staging copy
+        flat = torch.empty((self.world * m, per), dtype=self.dtype, device=x.device)
         gathered = flat.view(self.world, m, per)
-        y = out if out is not None else torch.empty((m, self.rows), dtype=y_local.dtype, device=y_local.device)
+        try:
+            self.local_forward(x, out=gathered[self.rank])
+        except TypeError:  # injected compute without an `out` argument (CPU tests)
+            y_local = self.local_forward(x)
+            flat = torch.empty((self.world * m, per), dtype=y_local.dtype, device=y_local.device)
+            gathered = flat.view(self.world, m, per)
+            gathered[self.rank].copy_(y_local)
+        dist.all_gather_into_tensor(flat, gathered[self.rank], group=self.group)
+        y = out if out is not None else torch.empty((m, self.rows), dtype=flat.dtype, device=flat.device)
         # [G][M][rows/G] -> (M, rows): rank g's slice lands in columns [g*per, (g+1)*per)
         y.view(m, self.world, per).copy_(gathered.permute(1, 0, 2))
         return y

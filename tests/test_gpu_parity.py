@@ -686,3 +686,30 @@ def test_prefill_pair_gemm(spec, m):
     check_bf16(L, m, seed=54_100 + m)
     if fam == "tucker":
         check_bf16(L, m, seed=54_200 + m, flags=tnl.PLAN_CHAIN)
+
+
+def test_output_sharded_layer_single_rank_nccl():
+    """OutputShardedLayer through a real NCCL group (world 1 on this box): the rank's rows are computed
+    into its slot of the gather buffer and gathered in place; equals the plain forward."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2602_01613_b200.sharded import OutputShardedLayer
+
+    L = O.synthetic_layer("tt", (160, 160, 64, 80), 2, (64, 64, 64), seed=53_000)
+    layer, _ = to_layer(L, round_bf16=True)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        osl = OutputShardedLayer(layer, dtype=torch.bfloat16, device=torch.device(DEV, 0))
+        x = torch.randn(300, 5120, device=DEV).to(torch.bfloat16)
+        y = osl(x)
+        ref = layer.plan(torch.bfloat16).forward(x)
+        torch.cuda.synchronize()
+        # split-K fp32 atomics in the first step: equal up to summation order
+        assert rel(ref.float().cpu().numpy(), y.float().cpu().numpy()) <= 1e-3
+    finally:
+        dist.destroy_process_group()
