@@ -70,6 +70,12 @@ int launch_tc_gemm_persistent(const CUtensorMap& a, const CUtensorMap& b, const 
                               const TcGemmArgs& args, int bn, int splits, int max_ctas, bool pdl,
                               cudaStream_t st);
 
+// Split-K over a 2-CTA cluster (tc_gemm_splitk2.cu): out (M x N bf16, N <= 64, N % 8 == 0) =
+// A (M x K) . B (N x K)^T; CTA 1 ships its K-half partial to CTA 0 over DSMEM (no fp32 buffer, no
+// memset, no conversion pass). a: box {64, 128}; b: box {64, 64}.
+int launch_tc_gemm_splitk2(const CUtensorMap& a, const CUtensorMap& b, __nv_bfloat16* out, int64_t ldo, int M, int N,
+                           int K, cudaStream_t st);
+
 // CTA-pair variant (tc_gemm_pair.cu): 256 x bn tiles over 2x1 clusters, bn in {128, 256};
 // `b` must be a map with box {64, bn / 2} (each CTA loads half of the B tile).
 int launch_tc_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcGemmArgs& args,

@@ -1389,6 +1389,11 @@ static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void*
   return TNL_OK;
 }
 
+static bool no_splitk2() {  // A/B switch (TNL_SPLITK2=0: fp32 split-K + conversion instead)
+  static const bool v = getenv("TNL_SPLITK2") && atoi(getenv("TNL_SPLITK2")) == 0;
+  return v;
+}
+
 static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y, int64_t ldy,
                              void* ws, size_t ws_bytes, cudaStream_t st, const tnl_fwd_opts* o = nullptr) {
   const bool fold = o && (o->accumulate || o->ss_in);
@@ -1447,6 +1452,14 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
       // no fp32 partials, no memset, no conversion pass (cfg4 q, Tucker-2 R256 at M=8192: 72.6 -> 65.2 us)
       s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, 1, st, (int)(k1 / 2), o, nullptr);
       if (s) return s;
+    } else if (splits == 2 && k1 <= 64 && !(o && o->ss_in) && !no_splitk2()) {
+      // two K halves over a CTA pair, partial exchanged through DSMEM: bf16 T straight out
+      CUtensorMap ta, tb;
+      int err;
+      if ((err = get_tmap(P, &ta, x, P->cols, M, ldx, 128)) || (err = get_tmap(P, &tb, win, P->cols, k1, P->cols, 64)))
+        return fail(TNL_ERR_CUDA, "tensor map (split-K pair step) failed: %d", err);
+      if ((err = launch_tc_gemm_splitk2(ta, tb, t0, k1, (int)M, (int)k1, (int)P->cols, st)))
+        return fail(TNL_ERR_CUDA, "split-K pair launch: %s", cudaGetErrorString((cudaError_t)err));
     } else if (splits > 1) {
       s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, tf, k1, true, splits, st);
       if (s) return s;

@@ -713,3 +713,19 @@ def test_output_sharded_layer_single_rank_nccl():
         assert rel(ref.float().cpu().numpy(), y.float().cpu().numpy()) <= 1e-3
     finally:
         dist.destroy_process_group()
+
+
+def test_prefill_splitk2_pair_deterministic():
+    """Narrow first step (cut <= 64) with >= 50 token tiles: split-K over a CTA pair, the partial
+    exchanged through DSMEM (no fp32 buffer / atomics) — oracle parity and bitwise repeatability."""
+    L = O.synthetic_layer("tt", (32, 32, 64, 80), 2, (64, 64, 64), seed=54_000)
+    layer, Lr = to_layer(L, round_bf16=True)
+    m = 50 * 128  # 50 token tiles -> split-K 2
+    x = O.round_bf16(O.synthetic_x(m, 5120, seed=54_009))
+    xt = torch.tensor(x, dtype=torch.bfloat16, device=DEV)
+    y1 = layer.forward(xt)
+    y2 = layer.forward(xt)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    ref = O.forward_torch_orient(Lr, x[:512])
+    assert rel(ref, y1[:512].float().cpu().numpy()) <= BF16_TOL
