@@ -470,7 +470,7 @@ def test_mlp_decode_gated_cfg3(m):
         assert rel(ref, y) <= 2 * BF16_TOL
 
 
-@pytest.mark.parametrize("m", [1, 64])
+@pytest.mark.parametrize("m", [1, 37, 64])
 def test_mlp_decode_gated_large_rank(m):
     """Decode MLP with gate + up cut 512 (Tucker-2 R256, the cfg4 edge layers): the large gated
     boundary (down's B_in loaded into the gate's A blocks once the gate MMAs completed) vs the oracle."""
@@ -720,7 +720,7 @@ def test_prefill_splitk2_pair_deterministic():
     exchanged through DSMEM (no fp32 buffer / atomics) — oracle parity and bitwise repeatability."""
     L = O.synthetic_layer("tt", (32, 32, 64, 80), 2, (64, 64, 64), seed=54_000)
     layer, Lr = to_layer(L, round_bf16=True)
-    m = 50 * 128  # 50 token tiles -> split-K 2
+    m = 50 * 128 + 37  # 51 token tiles (ragged last tile) -> split-K 2
     x = O.round_bf16(O.synthetic_x(m, 5120, seed=54_009))
     xt = torch.tensor(x, dtype=torch.bfloat16, device=DEV)
     y1 = layer.forward(xt)
@@ -729,3 +729,5 @@ def test_prefill_splitk2_pair_deterministic():
     assert torch.equal(y1, y2)
     ref = O.forward_torch_orient(Lr, x[:512])
     assert rel(ref, y1[:512].float().cpu().numpy()) <= BF16_TOL
+    tail = O.forward_torch_orient(Lr, x[-200:])  # rows of the ragged last tile
+    assert rel(tail, y1[-200:].float().cpu().numpy()) <= BF16_TOL
