@@ -1447,9 +1447,10 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     const int64_t kb1 = (P->cols + 63) / 64;
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb1 / 8));
     static const bool no_nsplit = getenv("TNL_STEP1_NSPLIT") && atoi(getenv("TNL_STEP1_NSPLIT")) == 0;  // A/B
-    if (!no_nsplit && splits > 1 && k1 >= 128 && k1 % 128 == 0 && ((M + 127) / 128) * 2 >= 96) {
+    if (!no_nsplit && splits > 1 && k1 >= 128 && k1 % 128 == 0 && ((M + 127) / 128) * 2 >= 96 && P->cols <= 12288) {
       // split the cut dimension instead of K: two half-width tiles per token tile, full K each ->
-      // no fp32 partials, no memset, no conversion pass (cfg4 q, Tucker-2 R256 at M=8192: 72.6 -> 65.2 us)
+      // no fp32 partials, no memset, no conversion pass (Tucker-2 R256 at M=8192: q 73.5 -> 66.2 us,
+      // o 73.8 -> 70.1 us). A long K (down, 25600) keeps the CTA-pair split-K: 84.6 vs 103 us.
       s = tc_step_p(P, x, ldx, win, P->cols, M, k1, P->cols, t0, k1, false, 1, st, (int)(k1 / 2), o, nullptr);
       if (s) return s;
     } else if (splits == 2 && k1 <= 64 && !(o && o->ss_in) && !no_splitk2()) {
