@@ -48,7 +48,7 @@ def peaks():
 # ---------------------------------------------------------------------------
 
 
-def cpu_reference_sample(m: int, steps: int, variants=None, chain: bool = False):
+def cpu_reference_sample(m: int, steps: int, variants=None, chain: bool = False, budget_s: float = 0.0):
     """Time the reference algorithm on host cores; one cfg2 layer per step, cycling variants.
 
     The reference's only forward is ``layer_to_matrix(L) @ x`` (tn_decompositions.py:364-365,
@@ -72,7 +72,11 @@ def cpu_reference_sample(m: int, steps: int, variants=None, chain: bool = False)
     x = S.make_x(m, 5120, seed=29_999).astype(np.float64).T.copy()  # (cols, M) reference orientation
     times = []
     names = []
+    t_start = time.perf_counter()
     for i in range(steps):
+        # bounded sample: once every variant has been timed, stop at the time budget
+        if budget_s > 0 and i >= len(layers) and time.perf_counter() - t_start > budget_s:
+            break
         name, L = layers[i % len(layers)]
         t0 = time.perf_counter()
         y = O.apply_chain(L, x) if chain else O.apply_reference(L, x)
@@ -103,7 +107,10 @@ def run_reference(args):
     steps = max(args.steps, 1)
     cpu_reference_sample(args.m, 1)  # warm-up (bounded: one layer)
     n = max(steps, 7)
-    times, names = cpu_reference_sample(args.m, n)
+    # each step is one layer of the reference algorithm; the sample stops after ~90 s of host
+    # work (at least one layer of every variant) so the reference arm ends within a few minutes
+    times, names = cpu_reference_sample(args.m, n, budget_s=90.0)
+    n = len(times)
     per = {}
     for nm, t in zip(names, times):
         per.setdefault(nm, []).append(t)
