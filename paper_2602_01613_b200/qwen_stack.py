@@ -118,6 +118,16 @@ class QwenTNStack:
             self._side = [torch.cuda.Stream(self.device) for _ in range(2)]
         return self._ws_side
 
+    def _group_ctx(self, m: int):
+        """Private workspaces (zero-filled: decode accumulators) and k/v side streams for one
+        concurrently running token group (decode microbatches)."""
+        need = max(max(p.workspace_bytes(m) for _, _, p in self.projections()),
+                   max(blk["mlp"].workspace_bytes(m) for blk in self.layers))
+        need_side = max(max(blk[n][2].workspace_bytes(m) for n in ("k", "v")) for blk in self.layers)
+        z = lambda n: torch.zeros(max(n, 256), dtype=torch.uint8, device=self.device)  # noqa: E731
+        return {"ws": z(need), "ws_side": [z(need_side), z(need_side)],
+                "side": [torch.cuda.Stream(self.device) for _ in range(2)]}
+
     def _buffers(self, m: int):
         mk = lambda n: torch.empty((m, n), dtype=self.dtype, device=self.device)  # noqa: E731
         return {"h": mk(HIDDEN), "q": mk(QDIM), "k": mk(KVDIM), "v": mk(KVDIM), "o": mk(HIDDEN), "d": mk(HIDDEN),
@@ -161,18 +171,24 @@ class QwenTNStack:
                                            ws.numel(), ctypes.byref(o_both), st))  # x += mlp(norm(x))
         return x
 
-    def forward(self, x: torch.Tensor, bufs=None) -> torch.Tensor:
-        """One pass of all layers; x (M x 5120) is updated in place (residual stream)."""
+    def forward(self, x: torch.Tensor, bufs=None, ctx=None) -> torch.Tensor:
+        """One pass of all layers; x (M x 5120) is updated in place (residual stream). `ctx`
+        (from _group_ctx) gives a token group its own workspaces and side streams."""
         m = x.shape[0]
-        ws = self.workspace(m)
+        ws = ctx["ws"] if ctx else self.workspace(m)
         b = bufs or self._buffers(m)
         if self.fold_prefill and m > 64:
             if "ss" not in b:
                 b["ss"] = torch.zeros((2, m), dtype=torch.float32, device=self.device)
             return self._forward_prefill_folded(x, b, ws)
         fork = self.concurrent_kv and m <= 64
+        side = self._side
         if fork:
-            ws_side = self._side_workspace(m)
+            if ctx:
+                ws_side, side = ctx["ws_side"], ctx["side"]
+            else:
+                ws_side = self._side_workspace(m)
+                side = self._side
             cur = torch.cuda.current_stream(self.device)
         for li, blk in enumerate(self.layers):
             # x += previous MLP output; h = rms(x)   (fused residual add + RMSNorm, one pass)
@@ -182,8 +198,8 @@ class QwenTNStack:
                 # shorter than the q -> o chain, so neither is on the critical path; joined before h is
                 # overwritten
                 for j, name in enumerate(("k", "v")):
-                    self._side[j].wait_stream(cur)
-                    with torch.cuda.stream(self._side[j]):
+                    side[j].wait_stream(cur)
+                    with torch.cuda.stream(side[j]):
                         blk[name][2].forward(b["h"], out=b[name], ws=ws_side[j])
             else:
                 blk["k"][2].forward(b["h"], out=b["k"], ws=ws)
@@ -199,25 +215,53 @@ class QwenTNStack:
                 blk["q"][2].forward(b["h"], out=b["q"], ws=ws)
                 blk["o"][2].forward(b["q"], out=b["o"], ws=ws)  # attention core: pass-through
             if fork:
-                for sd in self._side:
+                for sd in side:
                     cur.wait_stream(sd)
             self.add_rmsnorm(x, b["o"], b["h"])
             blk["mlp"].forward(b["h"], out=b["d"], ws=ws)
         x.add_(b["d"])
         return x
 
-    def capture(self, m: int):
+    def capture(self, m: int, microbatches: int = 1):
+        """Record one pass for M = m tokens into a CUDA graph. Decode (m <= 64) may split the
+        tokens into `microbatches` groups that run the whole stack concurrently on forked streams,
+        each with its own workspaces (tokens are independent through the stack: the attention core
+        is a pass-through)."""
         self.x = torch.zeros((m, HIDDEN), dtype=self.dtype, device=self.device)
-        self.bufs = self._buffers(m)
-        self.workspace(m)
+        k = max(1, min(microbatches, m)) if m <= 64 else 1
+        bounds = [(i * m // k, (i + 1) * m // k) for i in range(k)]
+        if k == 1:
+            self.bufs = self._buffers(m)
+            self.workspace(m)
+            groups = [(0, m, self.bufs, None)]
+        else:
+            groups = [(lo, hi, self._buffers(hi - lo), self._group_ctx(hi - lo)) for lo, hi in bounds]
+            self.bufs = groups[0][2]
+        gstreams = [torch.cuda.Stream(self.device) for _ in groups]
         s = torch.cuda.Stream(self.device)
+
+        def one_pass():
+            fork = torch.cuda.Event()
+            fork.record(s)
+            joins = []
+            for (lo, hi, bufs, ctx), gs in zip(groups, gstreams):
+                gs.wait_event(fork)
+                with torch.cuda.stream(gs):
+                    self.forward(self.x[lo:hi], bufs, ctx)
+                    e = torch.cuda.Event()
+                    e.record(gs)
+                    joins.append(e)
+            for e in joins:
+                s.wait_event(e)
+
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
-            self.forward(self.x, self.bufs)
+            one_pass()
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            self.forward(self.x, self.bufs)
+            one_pass()
         self.graph = g
+        self.microbatches = k
         return g

@@ -731,3 +731,22 @@ def test_prefill_splitk2_pair_deterministic():
     assert rel(ref, y1[:512].float().cpu().numpy()) <= BF16_TOL
     tail = O.forward_torch_orient(Lr, x[-200:])  # rows of the ragged last tile
     assert rel(tail, y1[-200:].float().cpu().numpy()) <= BF16_TOL
+
+
+def test_qwen_stack_decode_microbatches():
+    """cfg4 decode graph with two concurrent token groups (own workspaces / side streams) equals
+    the single-group graph."""
+    from paper_2602_01613_b200.qwen_stack import QwenTNStack
+
+    st = QwenTNStack(6)
+    torch.manual_seed(4)
+    x0 = torch.randn(64, 5120, device=DEV).to(torch.bfloat16)
+    outs = []
+    for mb in (1, 2):
+        g = st.capture(64, microbatches=mb)
+        st.x.copy_(x0)
+        g.replay()
+        torch.cuda.synchronize()
+        outs.append(st.x.float().cpu().numpy())
+    assert np.isfinite(outs[1]).all()
+    assert rel(outs[0], outs[1]) <= 1e-2

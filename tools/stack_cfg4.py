@@ -21,6 +21,7 @@ ap.add_argument("--unfused-mlp", action="store_true")
 ap.add_argument("--serial-kv", action="store_true", help="k/v on the main stream (no fork)")
 ap.add_argument("--no-fuse-qo", action="store_true", help="decode: q and o as two tnl_forward calls")
 ap.add_argument("--no-fold", action="store_true", help="prefill: separate residual-add + RMSNorm passes")
+ap.add_argument("--microbatches", type=int, default=2, help="decode: concurrent token groups (M <= 64)")
 a = ap.parse_args()
 HBM, TC = 6554.6e9, 1635e12
 
@@ -35,7 +36,7 @@ F = st.chain_flops_per_token()
 print(json.dumps({"layers": a.layers, "projections": 7 * a.layers, "params": P, "chain_flops_per_token": F,
                   "build_s": build_s, "fused_mlp_blocks": st.fused_mlp_count()}), flush=True)
 for m in [int(t) for t in a.ms.split(",")]:
-    g = st.capture(m)
+    g = st.capture(m, microbatches=a.microbatches)
     st.x.normal_()
     for _ in range(2):
         g.replay()
