@@ -2254,6 +2254,9 @@ static tnl_status mlp_forward_impl(const tnl_mlp* Bc, const void* x, int64_t m, 
   float* td32 = reinterpret_cast<float*>(w + off[2]);
   __nv_bfloat16* td = reinterpret_cast<__nv_bfloat16*>(w + off[3]);
   tnl_status s;
+  // 0. zero T_d's fp32 accumulator first, so no memset node sits between the T_gu GEMM and the
+  //    middle kernel (they stay PDL-chained: the middle kernel's prologue overlaps the GEMM's tail)
+  if (cudaMemsetAsync(td32, 0, sizeof(float) * m * B->rd, st) != cudaSuccess) return fail(TNL_ERR_CUDA, "memset");
   // 1. T_gu = x . [B_g; B_u]^T   (rows scaled by 1/rms(x) when the block's RMSNorm is folded)
   if ((s = mlp_tgu(B, x, m, ldx, tgu32, tgu, st, fold ? &in_o : nullptr))) return s;
   // 2. T_d = (silu(T_g A_g^T) * (T_u A_u^T)) B_d^T, h on chip
@@ -2294,7 +2297,6 @@ static tnl_status mlp_forward_impl(const tnl_mlp* Bc, const void* x, int64_t m, 
   a.td = td32;
   a.ld_td = B->rd;
   a.trace = B->g->trace;
-  if (cudaMemsetAsync(td32, 0, sizeof(float) * m * B->rd, st) != cudaSuccess) return fail(TNL_ERR_CUDA, "memset");
   if ((err = pair ? launch_mlp_mid_pair(tt, tag, tau, tbd, a, slices, st) : launch_mlp_mid(tt, tag, tau, tbd, a, slices, st)))
     return fail(TNL_ERR_CUDA, "MLP middle kernel launch: %s", cudaGetErrorString((cudaError_t)err));
   to_bf16(td32, td, m * B->rd, st);
