@@ -91,6 +91,9 @@ __global__ void f32_to_bf16_2d(const float* __restrict__ src, int64_t lds, __nv_
 }
 // contiguous fp32 -> bf16, 8 elements per thread (n % 8 == 0, 16-byte aligned buffers)
 __global__ void f32_to_bf16_v8(const float4* __restrict__ src, uint4* __restrict__ dst, int64_t n8) {
+  // PDL: wait for the producer of src (split-K reductions), release the consumer of dst early
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
     const float4 a = src[2 * e], b = src[2 * e + 1];
     __nv_bfloat162 o[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
@@ -127,6 +130,8 @@ static int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 
 // layer input: the cut activations are linear in x, so normalising them == normalising x)
 __global__ void f32_to_bf16_rowscale(const float4* __restrict__ src, uint4* __restrict__ dst, int64_t n8, int64_t cols8,
                                      const float* __restrict__ ss, float inv_n, float eps) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
     const float sc = rsqrtf(ss[e / cols8] * inv_n + eps);
     const float4 a = src[2 * e], b = src[2 * e + 1];
@@ -138,17 +143,17 @@ __global__ void f32_to_bf16_rowscale(const float4* __restrict__ src, uint4* __re
 static void to_bf16_scaled(const float* src, __nv_bfloat16* dst, int64_t rows, int64_t cols, const tnl_fwd_opts* o,
                            cudaStream_t st) {
   const int64_t n8 = rows * cols / 8;
-  f32_to_bf16_rowscale<<<grid_for(n8), 256, 0, st>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<uint4*>(dst),
-                                                      n8, cols / 8, o->ss_in, 1.f / (float)o->rms_n, o->rms_eps);
-  count_launch();
+  launch_pdl(f32_to_bf16_rowscale, dim3(grid_for(n8)), dim3(256), 0, st, reinterpret_cast<const float4*>(src),
+             reinterpret_cast<uint4*>(dst), n8, cols / 8, o->ss_in, 1.f / (float)o->rms_n, o->rms_eps);
 }
 static void to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st) {
   if (n % 8 == 0 && !(reinterpret_cast<uintptr_t>(src) & 15) && !(reinterpret_cast<uintptr_t>(dst) & 15))
-    f32_to_bf16_v8<<<grid_for(n / 8), 256, 0, st>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<uint4*>(dst),
-                                                      n / 8);
-  else
+    launch_pdl(f32_to_bf16_v8, dim3(grid_for(n / 8)), dim3(256), 0, st, reinterpret_cast<const float4*>(src),
+               reinterpret_cast<uint4*>(dst), n / 8);
+  else {
     f32_to_bf16_2d<<<grid_for(n), 256, 0, st>>>(src, n, dst, n, 1, n);
-  count_launch();
+    count_launch();
+  }
 }
 // ss[row] = sum_j x[row][j]^2 (one CTA per row; the folded RMSNorm's statistics)
 __global__ void __launch_bounds__(256) row_sumsq_bf16(const __nv_bfloat16* __restrict__ x, int64_t ldx, int64_t n,
