@@ -330,7 +330,7 @@ def main():
 
     # end-to-end through the public API: pinned host x -> H2D -> L layers -> D2H y, one graph
     e2e_stack = TNStack(layers, torch.bfloat16, flags=args.flags)
-    e2e_stack.capture(M, host_io=True, microbatches=args.microbatches)
+    e2e_stack.capture(M, host_io=True, microbatches=args.microbatches, zero_copy=True)
     e2e_stack.x_host.copy_(x0.cpu())
     ms_e2e = time_graph(e2e_stack.replay, args.steps, args.warmup, torch, dist)
     torch.cuda.synchronize()
@@ -563,7 +563,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": world * M * L / (ms_e2e / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": e2e_stack.h2d_bytes, "d2h_bytes_per_step": e2e_stack.d2h_bytes,
-                "ms_per_step": ms_e2e, "api": "TNStack CUDA graph: per token group, pinned host x -> tnl_copy_async (SM-driven H2D) -> the 70-layer chain -> tnl_copy_async D2H to pinned host y"},
+                "ms_per_step": ms_e2e, "api": "TNStack CUDA graph: per token group, tnl_stack_forward_host — the first kernel reads the pinned host x over the bus, the 70-layer chain runs, the last kernel writes the pinned host y (zero-copy H2D/D2H)"},
         "gpu_launches": launches_per_step * args.steps,
         "launches_per_step": launches_per_step,
         "clocks": clocks,

@@ -206,6 +206,13 @@ TNL_API tnl_status tnl_chain_destroy(tnl_chain* chain);
  * >= 16*256*8 int64 ([cta][layer][event]); NULL disables. */
 TNL_API tnl_status tnl_chain_set_trace(tnl_chain* chain, void* device_buffer);
 
+/* tnl_stack_forward with zero-copy host I/O: x (m x ldx) and y (m x ldy) are PINNED host buffers;
+ * the first kernel reads its x slices straight from host memory and the last one writes y straight
+ * to it (no copy-engine transfers, no staging kernels). Fused decode stacks only (M <= 64). */
+TNL_API tnl_status tnl_stack_forward_host(const tnl_plan* const* plans, int32_t n, const void* x_host, int64_t m,
+                                          int64_t ldx, void* y_host, int64_t ldy, void* workspace,
+                                          size_t workspace_bytes, void* stream);
+
 /* Qwen3 MLP block of three TN layers: y = down(silu(gate(x)) * up(x)).
  * For merged-cut bf16 plans (gate/up cut <= 128, down cut <= 256) and M > 64 the
  * intermediate h (M x inter) never reaches HBM: one kernel streams chunks of the

@@ -40,6 +40,7 @@ EXPORTED = (
     "tnl_jacobi_sweeps",
     "tnl_add_rmsnorm",
     "tnl_copy_async",
+    "tnl_stack_forward_host",
     "tnl_forward_ex",
     "tnl_mlp_forward_ex",
     "tnl_rms_stats",
@@ -157,6 +158,9 @@ def load():
         lib.tnl_add_rmsnorm.restype = ctypes.c_int
         lib.tnl_copy_async.argtypes = [P, P, ctypes.c_size_t, P]
         lib.tnl_copy_async.restype = ctypes.c_int
+        lib.tnl_stack_forward_host.argtypes = [ctypes.POINTER(P), ctypes.c_int32, P, i64, i64, P, i64, P,
+                                               ctypes.c_size_t, P]
+        lib.tnl_stack_forward_host.restype = ctypes.c_int
         OP = ctypes.POINTER(FwdOpts)
         lib.tnl_forward_ex.argtypes = [P, P, i64, i64, P, i64, P, ctypes.c_size_t, OP, P]
         lib.tnl_forward_ex.restype = ctypes.c_int

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     tma_prefetch_desc(&tmX);
     if (ACT_F32) tma_prefetch_desc(&tmY);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], ACT_F32 ? 2 : 1);
+      mbar_init(&full[s], (ACT_F32 || a.x_host) ? 2 : 1);
       mbar_init(&empty[s], 1);
       mbar_init(&stg[s], 1);
     }
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
   if (warp == 0) {
     if (elect_one()) {
       const int npre = min(nkb, STAGES);
-      const uint32_t tx = A_STAGE + (ACT_F32 ? 0u : B_STAGE);
+      const uint32_t tx = A_STAGE + ((ACT_F32 || a.x_host) ? 0u : B_STAGE);
       for (int i = 0; i < npre; ++i) {  // weights do not depend on the previous kernel
         mbar_arrive_expect_tx(&full[i], tx);
         tma_load_2d_hint(sA + i * A_STAGE, &tmW, &full[i], (kb0 + i) * BK, tile_m * BM,
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       TRACE(2);
       pdl_wait();
       TRACE(3);
-      if (!ACT_F32)  // (phase B: the epilogue warps read the fp32 accumulator themselves)
+      if (!ACT_F32 && !a.x_host)  // (phase B / host x: the epilogue warps fill the operand stages)
         for (int i = 0; i < npre; ++i) tma_load_2d(sB + i * B_STAGE, &tmX, &full[i], (kb0 + i) * BK, 0);
       for (int i = npre; i < nkb; ++i) {  // (phase A only: ACT_F32 keeps nkb <= STAGES)
         const int s = i % STAGES;
@@ -153,6 +153,45 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
   } else {
     const int et = threadIdx.x - 64;  // 0..255
     pdl_wait();
+    if constexpr (!ACT_F32) {
+      if (a.x_host) {
+        // zero-copy H2D: this CTA's K slice of x, [BN tokens][64 k] per stage (SW128 K-major), read
+        // from pinned host memory with every 16-byte request in flight at once (nkb <= STAGES)
+        constexpr int ITEMS = BN * 8;  // (token, 16-byte chunk) per stage
+        constexpr int PER = (ITEMS + DEC_EPI - 1) / DEC_EPI;
+        uint4 v[4][PER];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int e = et + u * DEC_EPI;
+            const int tok = e >> 3, ch = e & 7;
+            v[i][u] = make_uint4(0u, 0u, 0u, 0u);
+            if (i < nkb && e < ITEMS && tok < a.tokens) {
+              const uint4* src = reinterpret_cast<const uint4*>(a.x_host + (int64_t)tok * a.ldx_host + (kb0 + i) * BK) + ch;
+              asm volatile("ld.global.cv.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v[i][u].x), "=r"(v[i][u].y), "=r"(v[i][u].z), "=r"(v[i][u].w)
+                           : "l"(src));
+            }
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i >= nkb) break;
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int e = et + u * DEC_EPI;
+            if (e < ITEMS) {
+              const int tok = e >> 3, ch = e & 7;
+              sts128(smem_u32(sB + i * B_STAGE) + sw128_off(tok, ch), v[i][u]);
+            }
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar(1, DEC_EPI);
+        if (et == 0)
+          for (int i = 0; i < nkb; ++i) mbar_arrive(&full[i]);
+      }
+    }
     if (et == 0) TRACE(6);
     if constexpr (ACT_F32) {
       // fp32 accumulator [64 kappa][BN tokens] per k-block -> bf16 MN-major SW128 operand
@@ -242,7 +281,17 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
     if constexpr (ACT_F32) {
       fence_proxy_async_smem();
       named_bar(1, DEC_EPI);
-      if (et == 0) {
+      if (a.y_host) {
+        // zero-copy D2H: the staged y tile [BN tokens][128 rows] straight to pinned host memory
+        for (int e = et; e < a.tokens * (BM / 8); e += DEC_EPI) {
+          const int tok = e / (BM / 8), ch = e % (BM / 8);
+          const int row0 = tile_m * BM + ch * 8;
+          if (row0 < a.M_rows)
+            *reinterpret_cast<uint4*>(a.y_host + (int64_t)tok * a.ldy_host + row0) =
+                lds128(smem_u32(sY) + (tok * BM + ch * 8) * 2);
+        }
+        __threadfence_system();
+      } else if (et == 0) {
         tma_store_2d(&tmY, sY, tile_m * BM, 0);
         tma_store_commit();
       }

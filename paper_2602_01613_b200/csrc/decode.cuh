@@ -45,6 +45,13 @@ struct DecArgs {
   int64_t zero_prev_elems;
   // optional timeline (tnl_plan_set_trace): [cta][16] %globaltimer stamps
   unsigned long long* trace;
+  // zero-copy host I/O (decode stacks, tnl_stack_forward_host): phase A reads its x slice straight
+  // from pinned host memory [tokens][ldx_host] (the epilogue warps fill the operand stages);
+  // phase B writes y straight to pinned host memory [tokens][ldy_host]
+  const __nv_bfloat16* x_host;
+  int64_t ldx_host;
+  __nv_bfloat16* y_host;
+  int64_t ldy_host;
 };
 
 // phase A: weights (TMA map `w`, rows=M_rows, K) x activations (TMA map `x`, bf16 tokens x K)

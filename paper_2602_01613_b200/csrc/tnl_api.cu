@@ -1704,8 +1704,29 @@ tnl_status tnl_stack_workspace_size(const tnl_plan* const* plans, int32_t n, int
   return TNL_OK;
 }
 
+static tnl_status stack_forward_impl(const tnl_plan* const* plans, int32_t n, const void* x, int64_t m, int64_t ldx,
+                                     void* y, int64_t ldy, void* ws, size_t ws_bytes, void* stream, bool host_io);
+
 tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void* x, int64_t m,
                              int64_t ldx, void* y, int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+  return stack_forward_impl(plans, n, x, m, ldx, y, ldy, ws, ws_bytes, stream, false);
+}
+
+tnl_status tnl_stack_forward_host(const tnl_plan* const* plans, int32_t n, const void* x_host, int64_t m, int64_t ldx,
+                                  void* y_host, int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+  for (const void* p : {x_host, static_cast<const void*>(y_host)}) {
+    cudaPointerAttributes at;
+    if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type == cudaMemoryTypeUnregistered ||
+        at.type == cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      return fail(TNL_ERR_ARG, "stack_forward_host: x and y must be pinned host buffers");
+    }
+  }
+  return stack_forward_impl(plans, n, x_host, m, ldx, y_host, ldy, ws, ws_bytes, stream, true);
+}
+
+static tnl_status stack_forward_impl(const tnl_plan* const* plans, int32_t n, const void* x, int64_t m, int64_t ldx,
+                                     void* y, int64_t ldy, void* ws, size_t ws_bytes, void* stream, bool host_io) {
   if (!plans || n < 1 || !x || !y) return fail(TNL_ERR_ARG, "null argument");
   for (int i = 0; i < n; ++i)
     if (!plans[i]) return fail(TNL_ERR_ARG, "null plan %d", i);
@@ -1720,6 +1741,7 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
   tnl_plan* const* Pv = const_cast<tnl_plan* const*>(plans);
   if (!stack_fusable(plans, n, m) || (reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8 ||
       (reinterpret_cast<uintptr_t>(x) & 15) || ldx % 8) {
+    if (host_io) return fail(TNL_ERR_UNSUPPORTED, "stack_forward_host: needs the fused decode stack (M <= 64)");
     // generic chain: per-layer forwards through two activation buffers in the workspace
     size_t layer_ws = 0;
     int64_t width = 0;
@@ -1759,8 +1781,9 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     tnl_plan* P = Pv[0];
     CUtensorMap tw, tx;
     if ((err = get_tmap(P, &tw, P->bin, P->cols, P->r_pad, P->cols, 128)) ||
-        (err = get_tmap(P, &tx, x, P->cols, m, ldx, bn)))
+        (err = host_io ? 0 : get_tmap(P, &tx, x, P->cols, m, ldx, bn)))
       return fail(TNL_ERR_CUDA, "tensor map (stack phase A) failed: %d", err);
+    if (host_io) tx = tw;  // unused: the kernel reads x from host memory
     DecArgs a;
     memset(&a, 0, sizeof a);
     a.M_rows = (int32_t)P->r_pad;
@@ -1774,6 +1797,10 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     a.ldo_j = 1;
     a.out_f32_atomic = 1;
     a.trace = P->trace;
+    if (host_io) {
+      a.x_host = static_cast<const __nv_bfloat16*>(x);
+      a.ldx_host = ldx;
+    }
     if ((err = launch_dec_a(tw, tx, a, splits, st)))
       return fail(TNL_ERR_CUDA, "stack phase A launch: %s", cudaGetErrorString((cudaError_t)err));
   }
@@ -1809,8 +1836,9 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
     CUtensorMap tw2, tt, ty;
     if ((err = get_tmap(P, &tw2, P->aout, P->r_pad, rows_local, P->r_pad, 128)) ||
         (err = get_tmap2(P, &tt, tacc[l % 3], true, 64, P->r_pad, 64, bn, 64, 0)) ||
-        (err = get_tmap2(P, &ty, y, false, rows_local, m, ldy, 128, bn, 0)))
+        (err = host_io ? 0 : get_tmap2(P, &ty, y, false, rows_local, m, ldy, 128, bn, 0)))
       return fail(TNL_ERR_CUDA, "tensor map (stack phase B) failed: %d", err);
+    if (host_io) ty = tw2;  // unused: the kernel writes y to host memory
     DecArgs b;
     memset(&b, 0, sizeof b);
     b.M_rows = (int32_t)rows_local;
@@ -1829,6 +1857,10 @@ tnl_status tnl_stack_forward(const tnl_plan* const* plans, int32_t n, const void
       b.zero_prev_elems = 64 * Pv[l - 1]->r_pad;
     }
     b.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
+    if (host_io) {
+      b.y_host = static_cast<__nv_bfloat16*>(y);
+      b.ldy_host = ldy;
+    }
     if ((err = launch_dec_b(tw2, tt, ty, b, st)))
       return fail(TNL_ERR_CUDA, "stack phase B launch: %s", cudaGetErrorString((cudaError_t)err));
   }

@@ -100,8 +100,23 @@ class TNStack:
                                             ws.numel(), ctypes.c_void_p(stream)))
         return out
 
-    def capture(self, m: int, host_io: bool = True, warmup: int = 1, microbatches: int = 1):
-        """Record one pass for M = m tokens into a CUDA graph (static buffers)."""
+    def forward_host(self, x_host, y_host, slot: int = 0):
+        """Zero-copy decode step (tnl_stack_forward_host): pinned host x -> the first kernel reads
+        it over the bus, the last kernel writes y straight to pinned host y."""
+        m = x_host.shape[0]
+        ws = self.workspace(m, slot)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        N.check(self._lib.tnl_stack_forward_host(self._handles, len(self.plans), ctypes.c_void_p(x_host.data_ptr()), m,
+                                                 x_host.stride(0) if m > 1 else self.cols,
+                                                 ctypes.c_void_p(y_host.data_ptr()),
+                                                 y_host.stride(0) if m > 1 else self.rows,
+                                                 ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(stream)))
+        return y_host
+
+    def capture(self, m: int, host_io: bool = True, warmup: int = 1, microbatches: int = 1, zero_copy: bool = False):
+        """Record one pass for M = m tokens into a CUDA graph (static buffers). host_io: the pass
+        starts from pinned host x and ends in pinned host y — through SM-driven copies, or with
+        zero_copy=True (decode stacks) read/written directly by the first/last kernel."""
         self.m = m
         k = max(1, min(microbatches, m))
         bounds = [(i * m // k, (i + 1) * m // k) for i in range(k)]
@@ -131,11 +146,14 @@ class TNStack:
                 s = side[j]
                 s.wait_event(fork)
                 with torch.cuda.stream(s):
-                    if host_io:
-                        copy(self.x_dev[lo:hi], self.x_host[lo:hi])
-                    self.forward(self.x_dev[lo:hi], out=self.y_dev[lo:hi], slot=j)
-                    if host_io:
-                        copy(self.y_host[lo:hi], self.y_dev[lo:hi])
+                    if host_io and zero_copy:
+                        self.forward_host(self.x_host[lo:hi], self.y_host[lo:hi], slot=j)
+                    else:
+                        if host_io:
+                            copy(self.x_dev[lo:hi], self.x_host[lo:hi])
+                        self.forward(self.x_dev[lo:hi], out=self.y_dev[lo:hi], slot=j)
+                        if host_io:
+                            copy(self.y_host[lo:hi], self.y_dev[lo:hi])
                     e = torch.cuda.Event()
                     e.record(s)
                     joins.append(e)

@@ -289,16 +289,18 @@ def test_stack_graph_replay_matches_eager():
     assert float(d) < 1e-2
 
 
+@pytest.mark.parametrize("zero_copy", [False, True])
 @pytest.mark.parametrize("mb", [1, 2, 3])
-def test_stack_graph_host_io_microbatches(mb):
-    """Host I/O through tnl_copy_async per token group (graph) == the eager device pass."""
+def test_stack_graph_host_io_microbatches(mb, zero_copy):
+    """Host I/O per token group (graph) == the eager device pass: through tnl_copy_async, or zero-copy
+    (tnl_stack_forward_host: the first kernel reads pinned x, the last writes pinned y)."""
     from paper_2602_01613_b200.stack import TNStack
 
     Ls = [O.synthetic_layer("tucker", (1024, 1024), 1, (64, 64), seed=46_100 + i) for i in range(3)]
     st = TNStack([to_layer(L, round_bf16=True)[0] for L in Ls], torch.bfloat16)
     x = torch.randn(37, 1024, device=DEV).to(torch.bfloat16)
     ye = st.forward(x).clone()
-    st.capture(37, host_io=True, microbatches=mb)
+    st.capture(37, host_io=True, microbatches=mb, zero_copy=zero_copy)
     st.x_host.copy_(x.cpu())
     st.y_host.zero_()
     st.replay()

@@ -66,6 +66,12 @@ for mb in (1, 2):
     s0 = TNStack(layers, torch.bfloat16)
     s0.capture(M, host_io=False, microbatches=mb)
     print(f"mb={mb} device-resident: {timeit(s0.replay):.1f} us/step")
-    s1 = TNStack(layers, torch.bfloat16)
-    s1.capture(M, host_io=True, microbatches=mb)
-    print(f"mb={mb} e2e: {timeit(s1.replay):.1f} us/step")
+    for zc in (False, True):
+        s1 = TNStack(layers, torch.bfloat16)
+        s1.capture(M, host_io=True, microbatches=mb, zero_copy=zc)
+        s1.x_host.copy_(torch.randn(M, 5120).to(torch.bfloat16))
+        s1.replay(); torch.cuda.synchronize()
+        y0 = s1.y_host.clone()
+        s0.x_dev.copy_(s1.x_host.cuda()); s0.replay(); torch.cuda.synchronize()
+        err = float((y0.float() - s0.y_dev.cpu().float()).norm() / s0.y_dev.cpu().float().norm())
+        print(f"mb={mb} e2e zero_copy={zc}: {timeit(s1.replay):.1f} us/step (rel diff vs device pass {err:.2e})")
