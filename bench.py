@@ -330,7 +330,8 @@ def main():
 
     # end-to-end through the public API: pinned host x -> H2D -> L layers -> D2H y, one graph
     e2e_stack = TNStack(layers, torch.bfloat16, flags=args.flags)
-    e2e_stack.capture(M, host_io=True, microbatches=args.microbatches, zero_copy=True)
+    zero_copy = os.environ.get("TNL_E2E_ZERO_COPY", "1") != "0"  # A/B switch: SM-driven copies instead
+    e2e_stack.capture(M, host_io=True, microbatches=args.microbatches, zero_copy=zero_copy)
     e2e_stack.x_host.copy_(x0.cpu())
     ms_e2e = time_graph(e2e_stack.replay, args.steps, args.warmup, torch, dist)
     torch.cuda.synchronize()
