@@ -752,3 +752,25 @@ def test_qwen_stack_decode_microbatches():
         outs.append(st.x.float().cpu().numpy())
     assert np.isfinite(outs[1]).all()
     assert rel(outs[0], outs[1]) <= 1e-2
+
+
+def test_stack_forward_host_rejects_pageable_and_prefill():
+    """tnl_stack_forward_host: pageable host buffers and prefill-sized M are refused (no fallback)."""
+    from paper_2602_01613_b200.stack import TNStack
+
+    L = O.synthetic_layer("tucker", (1024, 1024), 1, (64, 64), seed=55_000)
+    st = TNStack([to_layer(L, round_bf16=True)[0]] * 2, torch.bfloat16)
+    xp = torch.zeros(8, 1024, dtype=torch.bfloat16)  # pageable
+    yp = torch.zeros(8, 1024, dtype=torch.bfloat16)
+    with pytest.raises(Exception):
+        st.forward_host(xp, yp)
+    xh = torch.zeros(100, 1024, dtype=torch.bfloat16).pin_memory()
+    yh = torch.zeros(100, 1024, dtype=torch.bfloat16).pin_memory()
+    with pytest.raises(Exception):
+        st.forward_host(xh, yh)  # M = 100 > 64: not a fused decode stack
+    xs, ys = xh[:8], yh[:8]
+    xs.copy_(torch.randn(8, 1024).to(torch.bfloat16))
+    st.forward_host(xs, ys)
+    torch.cuda.synchronize()
+    ref = st.forward(xs.cuda()).cpu()
+    assert rel(ref.float().numpy(), ys.float().numpy()) <= 1e-2
