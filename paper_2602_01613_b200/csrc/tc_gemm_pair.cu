@@ -24,6 +24,9 @@ namespace {
 constexpr int PBM = 128, PBK = 64;
 constexpr uint32_t P_A_STAGE = PBM * PBK * 2;
 constexpr uint32_t P_C_CHUNK = PBM * 64 * 2;
+#ifndef P_NC
+#define P_NC 3  // 3 staging buffers: gate r64 prefill 94.4 -> 92.9 us vs 2
+#endif
 
 __device__ __forceinline__ void pbar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -32,7 +35,8 @@ __device__ __forceinline__ void pbar(uint32_t id, uint32_t n) {
 template <int BN, int STAGES>
 struct PairSmem {
   static constexpr uint32_t B_STAGE = (BN / 2) * PBK * 2;  // this CTA's half of the B tile
-  static constexpr size_t bytes = 1024 + (size_t)STAGES * (P_A_STAGE + B_STAGE) + 2 * P_C_CHUNK + 256;
+  static constexpr int NC = P_NC;  // output staging buffers (TMA stores in flight per CTA)
+  static constexpr size_t bytes = 1024 + (size_t)STAGES * (P_A_STAGE + B_STAGE) + NC * P_C_CHUNK + 256;
 };
 
 template <int BN, int STAGES, bool SCALE>
@@ -48,7 +52,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * P_A_STAGE;
   uint8_t* sC = sB + STAGES * B_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sC + 2 * P_C_CHUNK);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + P_NC * P_C_CHUNK);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2] leader: 4 epilogue warps x 2 CTAs
@@ -151,8 +155,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       if (args.out_mode == TC_OUT_BF16) {
         const float rscale = SCALE ? row_rms_scale(args, row) : 1.f;
         for (int c0 = 0; c0 < BN; c0 += 64) {
-          uint8_t* stage = sC + (chunk_ct & 1) * P_C_CHUNK;
-          if (et == 0) tma_store_wait_read_le1();
+          uint8_t* stage = sC + (chunk_ct % P_NC) * P_C_CHUNK;
+          if (et == 0) tma_store_wait_read_le<P_NC - 1>();
           pbar(1, 128);
 #pragma unroll
           for (int c = 0; c < 64; c += 16) {
