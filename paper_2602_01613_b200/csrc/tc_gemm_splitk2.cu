@@ -23,7 +23,10 @@ namespace tnl {
 
 namespace {
 
-constexpr int BM = 128, BK = 64, BN = 64, STAGES = 7;
+#ifndef TNL_SK2_STAGES
+#define TNL_SK2_STAGES 7
+#endif
+constexpr int BM = 128, BK = 64, BN = 64, STAGES = TNL_SK2_STAGES;
 constexpr uint32_t A_STAGE = BM * BK * 2, B_STAGE = BN * BK * 2;
 constexpr uint32_t RBUF = BM * BN * 4;  // CTA 1's fp32 partial, [row][BN]
 constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_STAGE + B_STAGE) + RBUF + 256;
