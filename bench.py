@@ -446,10 +446,10 @@ def main():
         P3 = sum(tnl.param_count(l_) for l_ in (g_, u_, d_))
         b_bytes = 2 * (P3 + Mp * (5120 + 5120))
         b_flops = Mp * sum(l_.chain_flops_per_token() for l_ in (g_, u_, d_))
-        t_roof = max(b_bytes / (hbm * 1e9), b_flops / (tc * 1e12))
+        t_roof_mlp = max(b_bytes / (hbm * 1e9), b_flops / (tc * 1e12))
         prefill["mlp_block"] = {"what": "Qwen3-32B MLP block y = down(silu(gate(x)) * up(x)), TT r64, one tnl_mlp_forward",
                                 "M": Mp, "ms": ms_b, "tokens_per_s": Mp / (ms_b / 1e3), "fused": bool(blk.fused),
-                                "t_roofline_ms": 1e3 * t_roof, "frac_roofline": t_roof / (ms_b / 1e3),
+                                "t_roofline_ms": 1e3 * t_roof_mlp, "frac_roofline": t_roof_mlp / (ms_b / 1e3),
                                 "chain_TFLOPs": b_flops / (ms_b / 1e3) / 1e12}
         blk.close()
         del xs, yp

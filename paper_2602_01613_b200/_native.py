@@ -23,7 +23,8 @@ PLAN_AUTO, PLAN_CUT, PLAN_CHAIN, PLAN_GENERIC, PLAN_NO_DECODE, PLAN_GEMV = 0, 1,
 PLAN_NAMES = {PLAN_CUT: "cut", PLAN_CHAIN: "chain", PLAN_GENERIC: "generic", 0: "none"}
 MAX_MODES = 6
 
-# Every symbol include/tnl.h declares (checked by tests/test_abi.py).
+# Every symbol include/tnl.h declares: the drop-in boundary of the reference layer
+# (checked by tests/test_abi.py).
 EXPORTED = (
     "tnl_abi_version",
     "tnl_last_error",
@@ -35,26 +36,25 @@ EXPORTED = (
     "tnl_forward",
     "tnl_forward_host",
     "tnl_reconstruct",
-    "tnl_launch_count",
-    "tnl_plan_set_trace",
     "tnl_jacobi_sweeps",
-    "tnl_add_rmsnorm",
-    "tnl_copy_async",
-    "tnl_stack_forward_host",
-    "tnl_forward_ex",
-    "tnl_mlp_forward_ex",
+)
+# include/tnl_stack.h: decoder-stack extensions (no reference counterpart; the Qwen3 stack driver).
+EXPORTED_STACK = (
     "tnl_rms_stats",
-    "tnl_chain_create",
-    "tnl_chain_forward",
-    "tnl_chain_destroy",
-    "tnl_chain_set_trace",
+    "tnl_forward_ex",
     "tnl_stack_workspace_size",
     "tnl_stack_forward",
+    "tnl_stack_forward_host",
     "tnl_mlp_create",
     "tnl_mlp_destroy",
     "tnl_mlp_is_fused",
     "tnl_mlp_workspace_size",
     "tnl_mlp_forward",
+    "tnl_mlp_forward_ex",
+    "tnl_add_rmsnorm",
+    "tnl_copy_async",
+    "tnl_launch_count",
+    "tnl_plan_set_trace",
 )
 
 
@@ -168,14 +168,6 @@ def load():
         lib.tnl_mlp_forward_ex.restype = ctypes.c_int
         lib.tnl_rms_stats.argtypes = [P, i64, i64, i64, P, P]
         lib.tnl_rms_stats.restype = ctypes.c_int
-        lib.tnl_chain_create.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(P)]
-        lib.tnl_chain_create.restype = ctypes.c_int
-        lib.tnl_chain_forward.argtypes = [P, P, i64, i64, P, i64, P]
-        lib.tnl_chain_forward.restype = ctypes.c_int
-        lib.tnl_chain_destroy.argtypes = [P]
-        lib.tnl_chain_destroy.restype = ctypes.c_int
-        lib.tnl_chain_set_trace.argtypes = [P, P]
-        lib.tnl_chain_set_trace.restype = ctypes.c_int
         lib.tnl_launch_count.argtypes = [ctypes.c_int32]
         lib.tnl_launch_count.restype = i64
         for name in ("tnl_plan_create", "tnl_plan_create_rows", "tnl_plan_destroy", "tnl_plan_query",

@@ -49,7 +49,7 @@ def sources() -> list[str]:
 
 def headers() -> list[str]:
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    return hs + [os.path.join(ROOT, "include", "tnl.h")]
+    return hs + [os.path.join(ROOT, "include", h) for h in ("tnl.h", "tnl_stack.h")]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

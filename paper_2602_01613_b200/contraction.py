@@ -12,7 +12,8 @@ reference code) plus the two tensor helpers the reference forward path is built 
   {cores or core+factors or W, x (cols modes × batch)}, minimising
   Σ 2·Π(all mode sizes involved in a step) (`SPEC.md:465-473`), ties broken by the
   lexicographic step encoding; never worse than the left-to-right order (`SPEC.md:486-494`);
-* ``execute_plan(plan, layer, x)`` — runs a plan step by step (numpy float64), counting the
+* (the float64 step-by-step executor of a plan, ``execute_plan``, is test infrastructure and lives
+  in ``oracle/plan_exec.py``; this package never computes a layer on the CPU) — it counts the
   multiply-adds and the largest intermediate, for the SPEC's instrumentation invariants;
 * ``flop_report(layers, batch) -> FlopReport`` (`SPEC.md:496-500`);
 * ``micro_benchmark(layer, x, reps, warmup)`` (`SPEC.md:502-507`) — median / IQR of the GPU
@@ -218,47 +219,6 @@ def left_to_right_plan(layer, batch: int) -> ContractionPlan:
     """The baseline: operands contracted in their listed order (cores / factors, then x)."""
     net = layer_network(layer, batch)
     return _plan_from_order(net, list(range(len(net.operands))))
-
-
-def _arrays(layer):
-    if layer.family == "dense":
-        return [np.asarray(layer.matrix, dtype=np.float64)]
-    if layer.family == "tucker":
-        return [np.asarray(layer.core, dtype=np.float64)] + [np.asarray(f, dtype=np.float64) for f in layer.factors]
-    return [np.asarray(c, dtype=np.float64) for c in layer.cores]
-
-
-def execute_plan(plan: ContractionPlan, layer, x) -> tuple[np.ndarray, dict]:
-    """Apply a plan to x (cols, batch) in float64; returns (y (rows, batch), instrumentation)."""
-    net = plan.network
-    x = np.asarray(x, dtype=np.float64)
-    rm = layer.row_mode_count
-    ms = tuple(layer.mode_shape)
-    if layer.family == "dense":
-        xin = x
-    else:
-        xin = x.reshape(ms[rm:] + (x.shape[1],))
-    tensors = {i: a for i, a in enumerate(_arrays(layer) + [xin])}
-    labels = {i: m for i, m in enumerate(net.operands)}
-    letters = {}
-    for l in net.sizes:
-        letters[l] = chr(ord("a") + len(letters)) if len(letters) < 26 else chr(ord("A") + len(letters) - 26)
-    macs, largest = 0, 0
-    nxt = len(net.operands)
-    for (a, b), (ma, mb, res) in zip(plan.steps, plan.step_modes):
-        spec = "".join(letters[l] for l in ma) + "," + "".join(letters[l] for l in mb) + "->" + \
-            "".join(letters[l] for l in res)
-        tensors[nxt] = np.einsum(spec, tensors.pop(a), tensors.pop(b), optimize=False)
-        labels[nxt] = res
-        macs += math.prod(net.sizes[l] for l in set(ma) | set(mb))
-        largest = max(largest, tensors[nxt].size)
-        nxt += 1
-    (last,) = tensors.keys()
-    y = tensors[last]
-    order = [labels[last].index(l) for l in net.out]
-    y = np.transpose(y, order)
-    rows = math.prod(ms[:rm]) if layer.family != "dense" else layer.matrix_shape[0]
-    return y.reshape(rows, x.shape[1]), {"multiply_adds": macs, "flops": 2 * macs, "largest_intermediate": largest}
 
 
 # --- reports ---------------------------------------------------------------------------------

@@ -155,6 +155,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       if (args.out_mode == TC_OUT_BF16) {
         const float rscale = SCALE ? row_rms_scale(args, row) : 1.f;
         for (int c0 = 0; c0 < BN; c0 += 64) {
+          // Dead chunk (ragged N, or a CTA whose half tile lies past M): skip it entirely so the
+          // staging ring advances only on committed stores (wait_read_le<P_NC-1> guards reuse).
+          if (tn * BN + c0 >= args.N || tm * PBM >= args.M) {
+            if (c0 + 64 >= BN) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane_id() == 0) mbar_arrive_remote(mapa_shared(&tempty[acc], 0));
+            }
+            continue;
+          }
           uint8_t* stage = sC + (chunk_ct % P_NC) * P_C_CHUNK;
           if (et == 0) tma_store_wait_read_le<P_NC - 1>();
           pbar(1, 128);
@@ -189,13 +199,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           pbar(1, 128);
           if (et == 0) {
             const int col = tn * BN + c0;
-            if (col < args.N && tm * PBM < args.M) {
-              if (args.reduce_add)
-                tma_reduce_add_2d(&tmC, stage, col, tm * PBM);
-              else
-                tma_store_2d(&tmC, stage, col, tm * PBM);
-              tma_store_commit();
-            }
+            if (args.reduce_add)
+              tma_reduce_add_2d(&tmC, stage, col, tm * PBM);
+            else
+              tma_store_2d(&tmC, stage, col, tm * PBM);
+            tma_store_commit();
           }
           ++chunk_ct;
         }

@@ -149,6 +149,16 @@ __global__ void __launch_bounds__(192, 1)
       if (args.out_mode == TC_OUT_BF16) {
         const float rscale = SCALE ? row_rms_scale(args, row) : 1.f;
         for (int c0 = 0; c0 < BN; c0 += 64) {
+          // Dead chunk (ragged N): no TMEM read, no smem write, no store; the staging ring only
+          // advances on committed stores so wait_read_le1 always guards the buffer being reused.
+          if (tn * BN + c0 >= args.N) {
+            if (c0 + 64 >= BN) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+            }
+            continue;
+          }
           uint8_t* stage = sC + (chunk_ct & 1) * C_CHUNK;
           // the TMA store that used this staging buffer two chunks ago must have read it
           if (et == 0) tma_store_wait_read_le1();
@@ -184,13 +194,11 @@ __global__ void __launch_bounds__(192, 1)
           named_bar_sync(1, 128);
           if (et == 0) {
             const int col = tn * BN + c0;
-            if (col < args.N) {
-              if (args.reduce_add)
-                tma_reduce_add_2d(&tmC, stage, col, tm * BM);
-              else
-                tma_store_2d(&tmC, stage, col, tm * BM);
-              tma_store_commit();
-            }
+            if (args.reduce_add)
+              tma_reduce_add_2d(&tmC, stage, col, tm * BM);
+            else
+              tma_store_2d(&tmC, stage, col, tm * BM);
+            tma_store_commit();
           }
           ++chunk_ct;
         }

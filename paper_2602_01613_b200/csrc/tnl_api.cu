@@ -32,10 +32,10 @@
 #include <vector>
 
 #include "../../include/tnl.h"
+#include "../../include/tnl_stack.h"
 #include "chain.cuh"
 #include "common.cuh"
 #include "decode.cuh"
-#include "decode_cluster.cuh"
 #include "generic.cuh"
 #include "mlp.cuh"
 #include "tc_gemm.cuh"
@@ -1739,6 +1739,19 @@ static tnl_status stack_forward_impl(const tnl_plan* const* plans, int32_t n, co
   if (ws_bytes < need) return fail(TNL_ERR_ARG, "stack workspace %zu < required %zu bytes", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   tnl_plan* const* Pv = const_cast<tnl_plan* const*>(plans);
+  if (host_io) {
+    // The zero-copy loads read whole 64-column k-blocks of x (4 per CTA, register buffered) and
+    // the stores write 8-row uint4 chunks of y: reject shapes those kernels would over-read or
+    // over-write instead of bounds-checking the hot loop.
+    const tnl_plan* P0 = plans[0];
+    const tnl_plan* PL = plans[n - 1];
+    const int64_t rows_l = PL->row_end - PL->row_begin;
+    if (P0->cols % 64 || rows_l % 8 || ldx < P0->cols || ldy < rows_l)
+      return fail(TNL_ERR_UNSUPPORTED,
+                  "stack_forward_host: needs cols %% 64 == 0 (got %lld), rows %% 8 == 0 (got %lld), ldx >= cols, "
+                  "ldy >= rows",
+                  (long long)P0->cols, (long long)rows_l);
+  }
   if (!stack_fusable(plans, n, m) || (reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8 ||
       (reinterpret_cast<uintptr_t>(x) & 15) || ldx % 8) {
     if (host_io) return fail(TNL_ERR_UNSUPPORTED, "stack_forward_host: needs the fused decode stack (M <= 64)");
@@ -2017,139 +2030,6 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
   return TNL_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Cluster-resident decode chain (decode_cluster.cu)
-// ---------------------------------------------------------------------------
-struct tnl_chain {
-  int32_t n = 0, rpc = 0, device = 0;
-  int64_t dim = 0, per_cta = 0;
-  uint8_t* arena = nullptr;  // [16][per_cta] pre-swizzled weight blocks
-  uint8_t* rq = nullptr;     // [n] r_pad / 64
-  long long* trace = nullptr;  // debug timeline (tnl_chain_set_trace)
-};
-
-tnl_status tnl_chain_set_trace(tnl_chain* C, void* device_buffer) {
-  if (!C) return fail(TNL_ERR_ARG, "null argument");
-  C->trace = static_cast<long long*>(device_buffer);
-  return TNL_OK;
-}
-
-tnl_status tnl_chain_create(const tnl_plan* const* plans, int32_t n, int32_t flags, tnl_chain** out) {
-  (void)flags;
-  if (!plans || !out) return fail(TNL_ERR_ARG, "null argument");
-  *out = nullptr;
-  if (n < 1 || n > 256) return fail(TNL_ERR_UNSUPPORTED, "chain: 1..256 layers (got %d)", n);
-  const int64_t D = plans[0] ? plans[0]->cols : 0;
-  for (int i = 0; i < n; ++i) {
-    const tnl_plan* P = plans[i];
-    if (!P) return fail(TNL_ERR_ARG, "null plan %d", i);
-    if (P->compute_dtype != TNL_BF16 || !P->bin || !P->aout || !P->decode_max_m)
-      return fail(TNL_ERR_UNSUPPORTED, "chain: layer %d has no bf16 merged-cut panels", i);
-    if (P->rows != D || P->cols != D || P->row_begin != 0 || P->row_end != P->rows)
-      return fail(TNL_ERR_UNSUPPORTED, "chain: layer %d is not %lld x %lld (square, unsharded)", i, (long long)D,
-                  (long long)D);
-    if (P->r_pad % 64 || P->r_pad > 256)
-      return fail(TNL_ERR_UNSUPPORTED, "chain: layer %d cut %lld (padded %lld) not a multiple of 64 <= 256", i,
-                  (long long)P->r_cut, (long long)P->r_pad);
-  }
-  if (D % (64 * tnl::CHAIN_CS) || D / tnl::CHAIN_CS > 384)
-    return fail(TNL_ERR_UNSUPPORTED, "chain: width %lld must be a multiple of %d and <= %d", (long long)D,
-                64 * tnl::CHAIN_CS, 384 * tnl::CHAIN_CS);
-  const int rpc = (int)(D / tnl::CHAIN_CS);
-  if (tnl::chain_max_active_clusters(rpc, 32) < 1)
-    return fail(TNL_ERR_UNSUPPORTED, "chain: a %d-CTA cluster of the chain kernel cannot be scheduled here",
-                tnl::CHAIN_CS);
-  // block list in the kernel's consumption order (per CTA): A(0) B(0) A(1) B(1) ...
-  std::vector<tnl::CChainBlock> blocks;
-  const int kbx = rpc / 64, ntb = (rpc + 127) / 128;
-  int64_t per_cta = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int c = 0; c < tnl::CHAIN_CS; ++c) {
-      int64_t off = (int64_t)c * per_cta;
-      for (int l = 0; l < n; ++l) {
-        const tnl_plan* P = plans[l];
-        const int rp = (int)P->r_pad;
-        for (int u = 0; u < (rp + 127) / 128; ++u) {
-          const int rows = std::min(128, rp - u * 128);
-          for (int kb = 0; kb < kbx; ++kb) {
-            if (pass) blocks.push_back({P->bin, P->cols, u * 128, c * rpc + kb * 64, rows, 0, off});
-            off += rows * 128;
-          }
-        }
-        for (int t = 0; t < ntb; ++t) {
-          const int rows = std::min(128, rpc - t * 128);
-          for (int kb = 0; kb < rp / 64; ++kb) {
-            if (pass) blocks.push_back({P->aout, P->r_pad, c * rpc + t * 128, kb * 64, rows, 0, off});
-            off += rows * 128;
-          }
-        }
-      }
-      if (!pass && c == 0) per_cta = off;
-    }
-  }
-  int dev = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
-  std::unique_ptr<tnl_chain> C(new tnl_chain);
-  C->n = n;
-  C->rpc = rpc;
-  C->dim = D;
-  C->device = dev;
-  C->per_cta = per_cta;
-  tnl::CChainBlock* bdev = nullptr;
-  CUDA_TRY(cudaMalloc(&C->arena, (size_t)per_cta * tnl::CHAIN_CS));
-  CUDA_TRY(cudaMalloc(&C->rq, 256));
-  CUDA_TRY(cudaMalloc(&bdev, sizeof(tnl::CChainBlock) * blocks.size()));
-  std::vector<uint8_t> rq(n);
-  for (int l = 0; l < n; ++l) rq[l] = (uint8_t)(plans[l]->r_pad / 64);
-  CUDA_TRY(cudaMemcpy(C->rq, rq.data(), n, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(bdev, blocks.data(), sizeof(tnl::CChainBlock) * blocks.size(), cudaMemcpyHostToDevice));
-  int err = tnl::launch_chain_repack(bdev, (int64_t)blocks.size(), C->arena, 0);
-  cudaError_t se = cudaDeviceSynchronize();
-  cudaFree(bdev);
-  if (err || se != cudaSuccess) {
-    cudaFree(C->arena);
-    cudaFree(C->rq);
-    return fail(TNL_ERR_CUDA, "chain arena repack: %s", cudaGetErrorString(err ? (cudaError_t)err : se));
-  }
-  *out = C.release();
-  return TNL_OK;
-}
-
-tnl_status tnl_chain_forward(const tnl_chain* C, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
-                             void* stream) {
-  if (!C || !x || !y) return fail(TNL_ERR_ARG, "null argument");
-  if (m < 1 || m > 32) return fail(TNL_ERR_UNSUPPORTED, "chain: 1 <= M <= 32 tokens per call (got %lld)", (long long)m);
-  if (ldx < C->dim || ldy < C->dim) return fail(TNL_ERR_SHAPE, "chain: row pitches must be >= %lld", (long long)C->dim);
-  tnl::CChainArgs a;
-  memset(&a, 0, sizeof a);
-  a.arena = C->arena;
-  a.per_cta_bytes = C->per_cta;
-  a.rq = C->rq;
-  a.n = C->n;
-  a.rpc = C->rpc;
-  a.tokens = (int32_t)m;
-  a.x = static_cast<const __nv_bfloat16*>(x);
-  a.ldx = ldx;
-  a.y = static_cast<__nv_bfloat16*>(y);
-  a.ldy = ldy;
-  a.trace = C->trace;
-  static const int dbg = [] {
-    const char* e = getenv("TNL_CHAIN_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  a.debug = dbg;
-  const int err = tnl::launch_chain(a, static_cast<cudaStream_t>(stream));
-  if (err) return fail(TNL_ERR_CUDA, "chain launch: %s", cudaGetErrorString((cudaError_t)err));
-  return TNL_OK;
-}
-
-tnl_status tnl_chain_destroy(tnl_chain* C) {
-  if (!C) return TNL_OK;
-  cudaFree(C->arena);
-  cudaFree(C->rq);
-  delete C;
-  return TNL_OK;
-}
 
 tnl_status tnl_mlp_destroy(tnl_mlp* B) {
   if (!B) return TNL_OK;

@@ -30,37 +30,8 @@ JACOBI_TOL = 1e-12  # tensor_core.py:32
 JACOBI_MAX_SWEEPS = 60  # tensor_core.py:33
 
 
-# --- truncation policies (tensor_core.py:137-164) ---------------------------------------
-
-
-@dataclass(frozen=True)
-class FixedRank:
-    rank: int
-
-    def __post_init__(self):
-        if int(self.rank) < 1:
-            raise RankError(f"fixed rank must be >= 1, got {self.rank}")
-        object.__setattr__(self, "rank", int(self.rank))
-
-
-@dataclass(frozen=True)
-class RelativeError:
-    epsilon: float
-
-    def __post_init__(self):
-        if not 0.0 < float(self.epsilon) <= 1.0:
-            raise RankError(f"relative-error threshold must be in (0, 1], got {self.epsilon}")
-        object.__setattr__(self, "epsilon", float(self.epsilon))
-
-
-@dataclass(frozen=True)
-class ParamBudget:
-    budget: int
-
-    def __post_init__(self):
-        if int(self.budget) < 1:
-            raise RankError(f"parameter budget must be >= 1, got {self.budget}")
-        object.__setattr__(self, "budget", int(self.budget))
+# truncation policies (tensor_core.py:136-166) are shared with the rank planner
+from .modes import FixedRank, ParamBudget, RelativeError  # noqa: E402
 
 
 @dataclass(frozen=True)

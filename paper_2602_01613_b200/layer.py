@@ -49,13 +49,39 @@ def _shape(a) -> tuple[int, ...]:
     return tuple(int(s) for s in a.shape)
 
 
+def _array_token(a) -> tuple:
+    """Cheap identity of one payload array: object id, data pointer, shape, dtype and (torch) the
+    in-place version counter — changes whenever the array is replaced or a torch tensor is
+    written in place."""
+    if torch is not None and isinstance(a, torch.Tensor):
+        return (id(a), a.data_ptr(), tuple(a.shape), str(a.dtype), a._version)
+    arr = np.asarray(a)
+    return (id(a), arr.__array_interface__["data"][0], arr.shape, arr.dtype.str)
+
+
+def _array_digest(a) -> int:
+    """Content checksum (crc32 of the bytes) of one payload array — detects in-place writes to
+    numpy arrays, which carry no version counter."""
+    import zlib
+
+    if torch is not None and isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    arr = np.ascontiguousarray(np.asarray(a))
+    return zlib.crc32(memoryview(arr).cast("B"))
+
+
 @dataclass(eq=False)
 class CompressedLayer:
     """Tagged union over Dense / Tucker / TT / TR storage (tn_decompositions.py:66-126).
 
-    Arrays are stored by reference, as in the reference. Device plans are
-    built lazily per (dtype, device, flags) and cached; ``invalidate()`` drops
-    them after the arrays or ``row_mode_count`` are mutated.
+    Arrays are stored by reference, as in the reference, and the reference re-reads them on
+    every ``reconstruct`` (:346-361). Device plans are packed snapshots, so they are cached under
+    a key that includes every payload array's identity (object, data pointer, shape, dtype, and a
+    torch tensor's in-place version): replacing a core, swapping the factor list or writing a
+    torch core in place re-plans on the next call. numpy arrays have no version counter, so the
+    reference-API functions (``reconstruct``, ``layer_to_matrix``, ``apply_compressed``) also
+    compare a crc32 of the payload bytes; ``forward(x, check_cores=True)`` does the same on the
+    hot path. ``invalidate()`` drops every cached plan explicitly.
     """
 
     family: str
@@ -142,6 +168,26 @@ class CompressedLayer:
         for p in self._plans.values():
             p.close()
         self._plans.clear()
+        self._digest = None
+
+    def _payload(self) -> list:
+        if self.family == "tucker":
+            return [self.core] + list(self.factors)
+        if self.family in ("tt", "tr"):
+            return list(self.cores)
+        return [self.matrix]
+
+    def _identity(self) -> tuple:
+        return (self.family, self.mode_shape, self.row_mode_count,
+                tuple(_array_token(a) for a in self._payload()))
+
+    def check_cores(self) -> None:
+        """Re-plan if any payload array changed content since the plans were built (crc32)."""
+        dg = tuple(_array_digest(a) for a in self._payload())
+        prev = getattr(self, "_digest", None)
+        if self._plans and (prev is None or dg != prev):  # plans of unknown / different content
+            self.invalidate()
+        self._digest = dg
 
     # --- device plans -------------------------------------------------------
     def plan(self, dtype=None, device=None, flags: int = N.PLAN_AUTO, max_m: int = 0,
@@ -154,17 +200,27 @@ class CompressedLayer:
         if device is None:
             raise DeviceError("no CUDA device: the TN layer has no CPU fallback")
         device = torch.device(device)
-        key = (dtype, device.index, flags, max_m, row_range, self.row_mode_count, self.mode_shape)
+        ident = self._identity()
+        if getattr(self, "_ident", None) != ident:  # a core was replaced / written (torch) in place
+            if self._plans:
+                self.validate()
+                for p in self._plans.values():
+                    p.close()
+                self._plans.clear()
+            self._ident = ident
+        key = (dtype, device.index, flags, max_m, row_range)
         p = self._plans.get(key)
         if p is None:
             p = NativePlan(self, dtype, device, flags, max_m, row_range)
             self._plans[key] = p
         return p
 
-    def forward(self, x, out=None, flags: int = N.PLAN_AUTO):
+    def forward(self, x, out=None, flags: int = N.PLAN_AUTO, check_cores: bool = False):
         """y (M, rows) = x (M, cols) @ W^T on the GPU (x: CUDA bf16 or fp32 tensor)."""
         if torch is None or not isinstance(x, torch.Tensor) or not x.is_cuda:
             raise DeviceError("forward needs a CUDA tensor (no CPU fallback)")
+        if check_cores:
+            self.check_cores()
         return self.plan(x.dtype, x.device, flags).forward(x, out=out)
 
     __call__ = forward
@@ -268,6 +324,8 @@ class NativePlan:
         ldx = x.stride(0) if m > 1 else cols
         if out is None:
             out = torch.empty((m, self.rows_local), dtype=self.dtype, device=x.device)
+        else:
+            check_out(out, m, self.rows_local, self.dtype, x.device)
         if ws is None or ws.numel() < self.workspace_bytes(m):
             ws = self.workspace(m)
         if stream is None:
@@ -298,6 +356,21 @@ class NativePlan:
         return w
 
 
+def check_out(out, m: int, rows: int, dtype, device) -> None:
+    """A caller-supplied output must be exactly what the kernels write: (m, rows), the plan's
+    compute dtype, on the input's device, unit stride along rows, row pitch >= rows."""
+    if not isinstance(out, torch.Tensor):
+        raise ShapeError("out must be a torch tensor")
+    if tuple(out.shape) != (m, rows):
+        raise ShapeError(f"out has shape {tuple(out.shape)}, expected {(m, rows)}")
+    if out.dtype != dtype:
+        raise ShapeError(f"out dtype {out.dtype} != compute dtype {dtype}")
+    if out.device != torch.device(device):
+        raise ShapeError(f"out is on {out.device}, x on {device}")
+    if m > 0 and (out.stride(1) != 1 or (m > 1 and out.stride(0) < rows)):
+        raise ShapeError(f"out strides {tuple(out.stride())} are not row-major with unit column stride")
+
+
 # --- module functions (reference API) ------------------------------------------
 
 
@@ -318,6 +391,7 @@ def reconstruct(layer: CompressedLayer, dtype=None, device=None):
     layer itself; pass ``torch.bfloat16`` to reconstruct the bf16-rounded cores.
     """
     layer.validate()
+    layer.check_cores()  # the reference re-reads the arrays on every call (:346-361)
     dtype = dtype or torch.float32
     p = layer.plan(dtype=dtype, device=device, flags=N.PLAN_GENERIC)
     return p.reconstruct(torch.float32).reshape(layer.mode_shape)
@@ -333,7 +407,7 @@ def apply_compressed(layer: CompressedLayer, x, flags: int = N.PLAN_AUTO):
     rows, cols = layer.matrix_shape
     if x.dim() != 2 or x.shape[0] != cols:
         raise ShapeError(f"x inner dimension {tuple(x.shape)} does not match {cols} columns")
-    return layer.forward(x.t().contiguous(), flags=flags).t()
+    return layer.forward(x.t().contiguous(), flags=flags, check_cores=True).t()
 
 
 def param_count(layer: CompressedLayer) -> int:

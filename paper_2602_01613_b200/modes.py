@@ -6,7 +6,9 @@ cut bonds and stored-scalar counts agree exactly:
   param_count_formula                   tn_decompositions.py:381-401
   maximal_ranks                         tn_decompositions.py:404-418
   tr_feasible / ranks_feasible          tn_decompositions.py:259-286,425-442
-  select_ranks (FixedRank/ParamBudget)  tn_decompositions.py:445-510
+  RankSpec                              tn_decompositions.py:129-143
+  select_ranks -> RankSpec              tn_decompositions.py:445-510
+  FixedRank/RelativeError/ParamBudget   tensor_core.py:136-166 (truncation policies)
 and adds the FLOP currency of the SPEC: 2 x product of all
 involved mode sizes per pairwise step, canonical chain order.
 """
@@ -115,37 +117,85 @@ def ranks_feasible(family: str, shape, ranks) -> bool:
         return False
 
 
+# --- truncation policies (tensor_core.py:136-166) ------------------------------
+
+
 @dataclass(frozen=True)
 class FixedRank:
     rank: int
+
+    def __post_init__(self):
+        if int(self.rank) < 1:
+            raise RankError(f"fixed rank must be >= 1, got {self.rank}")
+        object.__setattr__(self, "rank", int(self.rank))
+
+
+@dataclass(frozen=True)
+class RelativeError:
+    epsilon: float
+
+    def __post_init__(self):
+        if not 0.0 < float(self.epsilon) <= 1.0:
+            raise RankError(f"relative-error threshold must be in (0, 1], got {self.epsilon}")
+        object.__setattr__(self, "epsilon", float(self.epsilon))
 
 
 @dataclass(frozen=True)
 class ParamBudget:
     budget: int
 
+    def __post_init__(self):
+        if int(self.budget) < 1:
+            raise RankError(f"parameter budget must be >= 1, got {self.budget}")
+        object.__setattr__(self, "budget", int(self.budget))
 
-def select_ranks(mode_shape, family: str, target) -> tuple[int, ...] | None:
-    """Ranks for a FixedRank or ParamBudget target (greedy, as the reference)."""
+
+@dataclass(frozen=True)
+class RankSpec:
+    """Concrete ranks for a family, or a relative-error threshold to resolve them during
+    decomposition (tn_decompositions.py:129-143: same fields, same RankError checks)."""
+
+    family: str
+    ranks: tuple | None = None
+    rel_error: float | None = None
+
+    def __post_init__(self):
+        if self.family not in FAMILIES and self.family != DENSE:
+            raise RankError(f"unknown family {self.family!r}")
+        if self.ranks is not None:
+            object.__setattr__(self, "ranks", tuple(int(r) for r in self.ranks))
+            if any(r < 1 for r in self.ranks):
+                raise RankError(f"ranks must be >= 1, got {self.ranks}")
+
+
+def select_ranks(mode_shape, family: str, target) -> RankSpec:
+    """Rank selection toward a truncation target (tn_decompositions.py:445-510).
+
+    ParamBudget: budgets at or above the dense size give the maximal (exact) ranks, else the
+    largest feasible uniform rank grown greedily position by position; FixedRank: the rank
+    clipped to the caps, lowered at the first largest position until feasible; RelativeError:
+    deferred to the decomposition (``RankSpec(rel_error=epsilon)``)."""
     shape = tuple(int(s) for s in mode_shape)
     if family == DENSE:
-        return None
+        return RankSpec(family=DENSE)
     if family not in FAMILIES:
         raise RankError(f"unknown family {family!r}")
     d = len(shape)
     npos = {"tucker": d, "tt": d - 1, "tr": d}[family]
+    if isinstance(target, RelativeError):
+        return RankSpec(family=family, ranks=None, rel_error=target.epsilon)
     caps = maximal_ranks(family, shape)
     if isinstance(target, FixedRank):
         ranks = [min(target.rank, c) for c in caps]
         while not ranks_feasible(family, shape, tuple(ranks)):
             i = max(range(len(ranks)), key=lambda t: (ranks[t], -t))
             ranks[i] = max(1, ranks[i] - 1)
-        return tuple(ranks)
+        return RankSpec(family=family, ranks=tuple(ranks))
     if not isinstance(target, ParamBudget):
         raise TypeError(f"unsupported target {target!r}")
     budget = target.budget
     if budget >= math.prod(shape):
-        return caps
+        return RankSpec(family=family, ranks=caps)
     floor_cost = param_count_formula(family, shape, (1,) * npos)
     if floor_cost > budget:
         raise InfeasibleBudgetError(
@@ -171,7 +221,7 @@ def select_ranks(mode_shape, family: str, target) -> tuple[int, ...] | None:
             trial[i] += 1
             if fits(tuple(trial)):
                 ranks, grew = trial, True
-    return tuple(ranks)
+    return RankSpec(family=family, ranks=tuple(ranks))
 
 
 # --- FLOP currency, canonical chain order ---

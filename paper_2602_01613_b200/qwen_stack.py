@@ -62,13 +62,17 @@ SHAPES = {"q": (QDIM, HIDDEN), "k": (KVDIM, HIDDEN), "v": (KVDIM, HIDDEN), "o": 
 
 class QwenTNStack:
     def __init__(self, n_layers: int = 64, dtype=torch.bfloat16, device=None, seed: int = 40_000,
-                 fused_mlp: bool = True):
+                 fused_mlp: bool = True, mlp_kinds=None):
+        """mlp_kinds: optional per-layer MLP family override (e.g. ["tt64", "tr4", "tucker4"]) so
+        short stacks can exercise every cfg4 layer variant; default: the sensitivity-mix layout."""
         self.n_layers = n_layers
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.layers = []
         for l in range(n_layers):
             kinds = layer_kinds(l, n_layers)
+            if mlp_kinds is not None:
+                kinds.update(gate=mlp_kinds[l], up=mlp_kinds[l], down=mlp_kinds[l])
             blk = {}
             for j, name in enumerate(("q", "k", "v", "o", "gate", "up", "down")):
                 rows, cols = SHAPES[name]

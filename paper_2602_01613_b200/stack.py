@@ -24,12 +24,12 @@ import torch
 
 from . import _native as N
 from .errors import ShapeError
-from .layer import CompressedLayer
+from .layer import CompressedLayer, check_out
 
 
 class TNStack:
     def __init__(self, layers: list[CompressedLayer], dtype=torch.bfloat16, device=None,
-                 flags: int = N.PLAN_AUTO, cluster: bool = False):
+                 flags: int = N.PLAN_AUTO):
         if not layers:
             raise ShapeError("empty stack")
         self.layers = layers
@@ -46,24 +46,6 @@ class TNStack:
         self.graph = None
         self._lib = N.load()
         self._handles = (ctypes.c_void_p * len(self.plans))(*[p.handle.value for p in self.plans])
-        # opt-in cluster-resident decode (tnl_chain_*: one 16-CTA cluster walks the whole chain,
-        # DSMEM reductions, bitwise-deterministic) when every layer qualifies (square bf16
-        # merged-cut layers); decode calls with M <= 32 then run as ONE kernel. Measured slower
-        # than the per-boundary kernels on the cfg2 bank (16 SMs cannot stream the weights fast
-        # enough), so it is not the default.
-        self.chain = None
-        if cluster and dtype == torch.bfloat16 and len(self.plans) >= 1:
-            h = ctypes.c_void_p()
-            if self._lib.tnl_chain_create(self._handles, len(self.plans), 0, ctypes.byref(h)) == 0:
-                self.chain = h
-
-    def __del__(self):
-        if getattr(self, "chain", None) is not None:
-            try:
-                self._lib.tnl_chain_destroy(self.chain)
-            except Exception:
-                pass
-            self.chain = None
 
     def workspace_bytes(self, m: int) -> int:
         n = ctypes.c_size_t()
@@ -85,15 +67,15 @@ class TNStack:
         m = x.shape[0]
         if x.stride(1) != 1 or (m > 1 and x.stride(0) < self.cols):
             x = x.contiguous()
+        if x.dim() != 2 or x.shape[1] != self.cols or x.dtype != self.dtype:
+            raise ShapeError(f"x {tuple(x.shape)} {x.dtype} does not match the stack's {self.cols} {self.dtype} inputs")
         if out is None:
             out = torch.empty((m, self.rows), dtype=self.dtype, device=self.device)
+        else:
+            check_out(out, m, self.rows, self.dtype, x.device)
         stream = torch.cuda.current_stream(self.device).cuda_stream
         ldx = x.stride(0) if m > 1 else self.cols
         ldy = out.stride(0) if m > 1 else self.rows
-        if self.chain is not None and m <= 32:
-            N.check(self._lib.tnl_chain_forward(self.chain, ctypes.c_void_p(x.data_ptr()), m, ldx,
-                                                ctypes.c_void_p(out.data_ptr()), ldy, ctypes.c_void_p(stream)))
-            return out
         ws = self.workspace(m, slot)
         N.check(self._lib.tnl_stack_forward(self._handles, len(self.plans), ctypes.c_void_p(x.data_ptr()), m, ldx,
                                             ctypes.c_void_p(out.data_ptr()), ldy, ctypes.c_void_p(ws.data_ptr()),

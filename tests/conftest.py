@@ -30,3 +30,22 @@ def golden():
     return index, arrays
 
 
+
+
+# The unmodified reference package: installed into baseline/_ref (git-ignored, travels to the GPU
+# box with the snapshot) or, in the build container, importable from /root/reference.
+REF_PATHS = [os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"]
+
+
+@pytest.fixture(scope="session")
+def minima():
+    for p in REF_PATHS:
+        if os.path.isdir(os.path.join(p, "minima")):
+            if p not in sys.path:
+                sys.path.append(p)
+            import minima as m
+            import minima.tensor_core  # noqa: F401
+            import minima.tn_decompositions  # noqa: F401
+
+            return m
+    pytest.skip("reference package (minima) not installed: baseline/_ref or /root/reference")

@@ -12,22 +12,27 @@ from paper_2602_01613_b200 import _native as N
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def header_symbols():
-    text = open(os.path.join(ROOT, "include", "tnl.h")).read()
+def header_symbols(name="tnl.h"):
+    text = open(os.path.join(ROOT, "include", name)).read()
     return sorted(set(re.findall(r"TNL_API\s+[\w\s\*]+?\b(tnl_\w+)\s*\(", text)))
+
+
+def all_symbols():
+    return sorted(set(header_symbols("tnl.h")) | set(header_symbols("tnl_stack.h")))
 
 
 def test_header_and_binding_agree():
     syms = header_symbols()
-    assert len(syms) >= 11
+    assert len(syms) == 11  # the reference boundary: plan lifecycle, forward, reconstruct, Jacobi
     assert sorted(N.EXPORTED) == syms
+    assert sorted(N.EXPORTED_STACK) == header_symbols("tnl_stack.h")
 
 
 def test_library_exports_every_symbol():
     assert os.path.exists(N.lib_path()), "build libtnl.so first (python -m paper_2602_01613_b200.build)"
     out = subprocess.run(["nm", "-D", "--defined-only", N.lib_path()], capture_output=True, text=True).stdout
     exported = set(re.findall(r"\bT (tnl_\w+)", out))
-    missing = set(header_symbols()) - exported
+    missing = set(all_symbols()) - exported
     assert not missing, missing
 
 
@@ -35,7 +40,7 @@ def test_library_loads_and_reports_abi():
     lib = N.load()
     assert lib.tnl_abi_version() == 1
     assert isinstance(lib.tnl_last_error(), bytes)
-    for s in header_symbols():
+    for s in all_symbols():
         assert hasattr(lib, s)
 
 

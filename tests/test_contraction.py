@@ -7,6 +7,7 @@ import math
 import numpy as np
 import pytest
 
+from oracle import plan_exec as PE
 from oracle import tn_oracle as O
 from paper_2602_01613_b200 import CompressedLayer
 from paper_2602_01613_b200 import contraction as C
@@ -79,7 +80,7 @@ def test_execute_plan_matches_reference_and_counts(fam, ms, rm, ranks):
     x = O.synthetic_x(5, cols, seed=4).T  # reference orientation (cols, M)
     ref = O.apply_reference(Lo, x)
     for plan in (C.plan_contraction(lay, 5), C.left_to_right_plan(lay, 5)):
-        y, inst = C.execute_plan(plan, lay, x)
+        y, inst = PE.execute_plan(plan, lay, x)
         assert C.relative_error(ref, y) <= 1e-10
         assert inst["flops"] == plan.predicted_flops  # SPEC.md:511 instrumentation invariant
         assert inst["largest_intermediate"] == plan.largest_intermediate

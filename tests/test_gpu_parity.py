@@ -337,36 +337,6 @@ def test_copy_async_roundtrip(nbytes):
                                    ctypes.c_void_p(s)))
 
 
-@pytest.mark.parametrize("m", [1, 5, 16, 17, 32])
-def test_cluster_chain_matches_oracle_and_is_deterministic(m):
-    """tnl_chain_forward (one 16-CTA cluster, DSMEM reductions) vs the oracle applied layer by layer
-    on the same bf16 values, vs the per-boundary stack path, and bitwise-repeatable."""
-    from paper_2602_01613_b200.stack import TNStack
-
-    specs = [("tucker", (5120, 5120), 1, (256, 256)), ("tr", (64, 80, 64, 80), 2, (8, 8, 8, 8)),
-             ("tucker", (5120, 5120), 1, (128, 128)), ("tr", (5120, 5120), 1, (16, 16)),
-             ("tucker", (5120, 5120), 1, (64, 64))]
-    Ls = [O.synthetic_layer(f, ms, rm, rk, seed=49_000 + i) for i, (f, ms, rm, rk) in enumerate(specs)]
-    pairs = [to_layer(L, round_bf16=True) for L in Ls]
-    st = TNStack([p[0] for p in pairs], torch.bfloat16, cluster=True)
-    assert st.chain is not None
-    ref_st = TNStack([p[0] for p in pairs], torch.bfloat16)
-    x = O.round_bf16(O.synthetic_x(m, 5120, seed=49_999))
-    xt = torch.tensor(x, dtype=torch.bfloat16, device=DEV)
-    y = st.forward(xt)
-    again = [st.forward(xt) for _ in range(5)]
-    yb = ref_st.forward(xt)
-    torch.cuda.synchronize()
-    ref = x
-    for _, Lr in pairs:
-        ref = O.round_bf16(O.forward_torch_orient(Lr, ref))
-    got = y.float().cpu().numpy()
-    assert np.isfinite(got).all() and np.linalg.norm(got) > 0
-    assert rel(ref, got) <= 3 * BF16_TOL
-    assert rel(ref, yb.float().cpu().numpy()) <= 3 * BF16_TOL
-    assert all(torch.equal(a, y) for a in again)
-
-
 def test_chain_plan_selected_for_two_mode_inputs():
     L = O.synthetic_layer("tr", (64, 80, 64, 80), 2, (16, 16, 16, 16), seed=47_000)
     layer, _ = to_layer(L, round_bf16=True)

@@ -65,8 +65,9 @@ def test_modes_match_reference_goldens(golden):
 
 def test_select_ranks_reference_cases():
     # pkg/tests/test_tn_decompositions.py:209-212, 223-238
-    assert modes.select_ranks((8, 8, 8, 8), "tt", modes.ParamBudget(320)) == (4, 4, 4)
-    r = modes.select_ranks((8, 8, 8, 8), "tucker", modes.ParamBudget(383))
+    spec = modes.select_ranks((8, 8, 8, 8), "tt", modes.ParamBudget(320))
+    assert isinstance(spec, modes.RankSpec) and spec.family == "tt" and spec.ranks == (4, 4, 4)
+    r = modes.select_ranks((8, 8, 8, 8), "tucker", modes.ParamBudget(383)).ranks
     assert modes.param_count_formula("tucker", (8, 8, 8, 8), r) <= 383
     for i in range(4):
         t = list(r)
@@ -75,10 +76,18 @@ def test_select_ranks_reference_cases():
     with pytest.raises(tnl.InfeasibleBudgetError):
         modes.select_ranks((8, 8, 8, 8), "tt", modes.ParamBudget(10))
     for fam in ("tucker", "tt", "tr"):
-        assert modes.select_ranks((4, 4, 4), fam, modes.ParamBudget(64)) == modes.maximal_ranks(fam, (4, 4, 4))
+        assert modes.select_ranks((4, 4, 4), fam, modes.ParamBudget(64)).ranks == modes.maximal_ranks(fam, (4, 4, 4))
     # TR closure capped at 1 (tn_decompositions.py:416-417)
-    assert modes.select_ranks((6, 8, 5, 8), "tr", modes.ParamBudget(600))[0] == 1
-    assert modes.select_ranks((4, 4, 4), "tt", modes.FixedRank(16)) == (4, 4)
+    assert modes.select_ranks((6, 8, 5, 8), "tr", modes.ParamBudget(600)).ranks[0] == 1
+    assert modes.select_ranks((4, 4, 4), "tt", modes.FixedRank(16)).ranks == (4, 4)
+    # RelativeError defers to the decomposition (tn_decompositions.py:462-463); dense has no ranks
+    spec = modes.select_ranks((8, 8, 8, 8), "tr", modes.RelativeError(0.1))
+    assert spec == modes.RankSpec(family="tr", ranks=None, rel_error=0.1)
+    assert modes.select_ranks((4, 4), "dense", modes.FixedRank(2)) == modes.RankSpec("dense")
+    with pytest.raises(tnl.RankError, match="unknown family"):
+        modes.RankSpec("mpo")
+    with pytest.raises(tnl.RankError, match="ranks must be >= 1"):
+        modes.RankSpec("tt", ranks=(0, 2))
 
 
 def test_flop_accounting_matches_oracle():
