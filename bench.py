@@ -93,32 +93,98 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-def run_reference(args):
-    """Reference arm: the reference's CPU algorithm on host cores, rank 0 only.
+def import_reference():
+    """The UNMODIFIED reference package (minima) installed into baseline/_ref (git-ignored, travels
+    to the GPU box); None when it is not installed."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "minima")):
+        return None
+    if path not in sys.path:
+        sys.path.append(path)
+    try:
+        from minima import tn_decompositions as T
 
-    A step is one cfg2 layer (variants cycled); at least one layer of each of the 7
-    variants is measured even when K < 7, and value = M / (mean over variants of the
-    per-variant mean time), so the figure does not depend on which variants K covers.
+        return T
+    except Exception:
+        return None
+
+
+def reference_sample(m: int, steps: int, budget_s: float):
+    """Time the reference's own forward, ``layer_to_matrix(L) @ x`` (tn_decompositions.py:364-365,
+    sensitivity.py:156), with the UNMODIFIED minima package on the cfg2 layers, float64, all host
+    threads; one layer per step cycling the 7 variants. A TR reconstruct materialises r0^2 * 26 M
+    doubles (54 GB at r0 = 16): a variant whose transient does not fit in 60 % of the available host
+    memory runs the oracle port instead (reported per variant)."""
+    import numpy as np
+
+    from paper_2602_01613_b200 import synthetic as S
+
+    T = import_reference()
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    layers = []
+    for v, (name, fam, ms, rm, ranks) in enumerate(S.CFG2_VARIANTS):
+        L = S.make_layer(fam, ms, rm, ranks, seed=20_000 + 100 * v)
+        kw = dict(family=fam, mode_shape=ms, row_mode_count=rm)
+        if fam == "tucker":
+            kw.update(core=L.core.astype(np.float64), factors=[u.astype(np.float64) for u in L.factors])
+        else:
+            kw.update(cores=[c.astype(np.float64) for c in L.cores])
+        transient = 8 * (ranks[0] ** 2 if fam == "tr" else 1) * math.prod(ms)
+        if T is not None and transient < 0.6 * avail:
+            layers.append((name, "reference", T.CompressedLayer(**kw), T.layer_to_matrix))
+        else:
+            from oracle import tn_oracle as O
+
+            layers.append((name, "port", O.OracleLayer(**kw), O.layer_to_matrix))
+    x = S.make_x(m, 5120, seed=29_999).astype(np.float64).T.copy()  # (cols, M) reference orientation
+    times, names, kinds = [], [], {}
+    t_start = time.perf_counter()
+    for i in range(steps):
+        if budget_s > 0 and i >= len(layers) and time.perf_counter() - t_start > budget_s:
+            break
+        name, kind, L, to_matrix = layers[i % len(layers)]
+        t0 = time.perf_counter()
+        y = to_matrix(L) @ x
+        times.append(time.perf_counter() - t0)
+        names.append(name)
+        kinds[name] = kind
+        assert y.shape == (5120, m)
+        del y
+    return times, names, kinds
+
+
+def run_reference(args):
+    """Reference arm: the reference's own CPU forward on host cores, rank 0 only.
+
+    A step is one cfg2 layer through the unmodified minima package (variants cycled); at least
+    one layer of each of the 7 variants is measured even when K < 7, and value = M / (mean over
+    variants of the per-variant mean time), so the figure does not depend on which variants K
+    covers.
     """
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     nthreads = cpu_cores()
     steps = max(args.steps, 1)
-    cpu_reference_sample(args.m, 1)  # warm-up (bounded: one layer)
     n = max(steps, 7)
-    # each step is one layer of the reference algorithm; the sample stops after ~90 s of host
-    # work (at least one layer of every variant) so the reference arm ends within a few minutes
-    times, names = cpu_reference_sample(args.m, n, budget_s=90.0)
+    # each step is one layer; the sample stops after ~120 s of host work (at least one layer of
+    # every variant) so the reference arm ends within a few minutes
+    times, names, kinds = reference_sample(args.m, n, budget_s=120.0)
     n = len(times)
     per = {}
     for nm, t in zip(names, times):
         per.setdefault(nm, []).append(t)
     mean_layer_s = sum(sum(v) / len(v) for v in per.values()) / len(per)
     value = args.m / mean_layer_s
+    kind = "reference" if all(k == "reference" for k in kinds.values()) else "port"
     sample = (f"{n} layers (one per step, cycling the {len(per)} cfg2 5120x5120 variants), M={args.m}, "
-              "float64 layer_to_matrix(L) @ x (oracle port of the reference algorithm); "
-              "value = M / mean per-variant layer time")
+              "float64 layer_to_matrix(L) @ x through the unmodified reference package (minima, "
+              "installed in baseline/_ref); value = M / mean per-variant layer time")
     line = {
         "metric": METRIC,
         "impl": "reference",
@@ -134,8 +200,9 @@ def run_reference(args):
         "dtype": "f64",
         "data": "synthetic",
         "config": workload_config(args),
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": nthreads, "kind": "port", "sample": sample,
-                         "per_variant_s": {k: sum(v) / len(v) for k, v in per.items()}},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": nthreads, "kind": kind, "sample": sample,
+                         "per_variant_s": {k: sum(v) / len(v) for k, v in per.items()},
+                         "per_variant_impl": kinds},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -257,6 +324,117 @@ def time_graph(replay, steps, warmup, torch, dist=None):
     return ms / steps
 
 
+# ---------------------------------------------------------------------------
+# cfg4: the 64-layer Qwen3-32B-shaped mixed-TN stack (secondary lines) vs a measured dense stack
+# ---------------------------------------------------------------------------
+
+
+class DenseQwenStack:
+    """The same decoder step as QwenTNStack with UNCOMPRESSED bf16 weights and cuBLAS matmuls
+    (torch.matmul), pre-norm RMSNorm and SiLU*mul as torch ops, attention core a pass-through:
+        h = rms(x); q, k, v = h Wq^T, h Wk^T, h Wv^T; x += q Wo^T
+        h = rms(x); x += (silu(h Wg^T) * (h Wu^T)) Wd^T
+    64 layers x (8192x5120 + 2x1024x5120 + 5120x8192 + 2x25600x5120 + 5120x25600) = 31.2 G params
+    (62.4 GB bf16, resident in HBM). Random-init weights, N(0, 1/cols)."""
+
+    def __init__(self, n_layers, torch):
+        from paper_2602_01613_b200 import qwen_stack as Q
+
+        self.torch = torch
+        self.w = []
+        for _ in range(n_layers):
+            blk = {}
+            for name, (rows, cols) in Q.SHAPES.items():
+                blk[name] = torch.empty(rows, cols, dtype=torch.bfloat16, device="cuda").normal_(0, cols ** -0.5)
+            self.w.append(blk)
+        self.params = sum(w.numel() for blk in self.w for w in blk.values())
+
+    def forward(self, x):
+        torch = self.torch
+        F = torch.nn.functional
+
+        def rms(t):
+            tf = t.float()
+            return (tf * torch.rsqrt(tf.pow(2).mean(-1, keepdim=True) + 1e-6)).to(torch.bfloat16)
+
+        for blk in self.w:
+            h = rms(x)
+            q = torch.matmul(h, blk["q"].t())
+            torch.matmul(h, blk["k"].t())
+            torch.matmul(h, blk["v"].t())
+            x = x + torch.matmul(q, blk["o"].t())
+            h = rms(x)
+            x = x + torch.matmul(F.silu(torch.matmul(h, blk["gate"].t())) * torch.matmul(h, blk["up"].t()),
+                                 blk["down"].t())
+        return x
+
+
+def capture_graph(fn, torch):
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn()
+    return g
+
+
+def bench_cfg4(hbm, tc, torch, n_layers=64, ms=(1, 64, 8192), dense=True, reps=(5, 5, 2)):
+    """BASELINE cfg4: the full 64-layer mixed-TN stack (sensitivity-mix layout) —
+    decode M=1 and M=64 (CUDA graph, two token groups on forked streams) and prefill M=8192
+    (folded residual/RMSNorm) — each against the same decoder with uncompressed weights on cuBLAS,
+    measured in the same process. Roofline per pass: bytes = sum over the 448 projections of
+    2*(P + M*(rows+cols)), flops = M * sum of chain flops; the RMSNorm/residual traffic of the
+    decoder is not counted (it is the same for both stacks)."""
+    from paper_2602_01613_b200.qwen_stack import HIDDEN, QwenTNStack
+
+    t0 = time.perf_counter()
+    st = QwenTNStack(n_layers)
+    build = dict(st.build_s, total=time.perf_counter() - t0)
+    P = st.param_count()
+    F = st.chain_flops_per_token()
+    rc = sum(r + c for _, lay, _ in st.projections() for r, c in [lay.matrix_shape])
+    out = {"layers": n_layers, "projections": 7 * n_layers, "params": P, "chain_flops_per_token": F,
+           "build_s": build, "fused_mlp_blocks": st.fused_mlp_count(), "lines": {}}
+    for m, k in zip(ms, reps):
+        g = st.capture(m, microbatches=2)
+        st.x.normal_()
+        ms_tn = time_graph(g.replay, k, 2, torch, None)
+        finite = bool(torch.isfinite(st.x).all())
+        byts = 2 * (P + m * rc)
+        t_roof = max(byts / (hbm * 1e9), m * F / (tc * 1e12))
+        bound = "hbm" if byts / (hbm * 1e9) >= m * F / (tc * 1e12) else "tensor"
+        out["lines"][f"M={m}"] = {
+            "phase": "decode" if m <= 64 else "prefill", "ms_per_pass": ms_tn, "tokens_per_s": m / (ms_tn / 1e3),
+            "roofline": {"bound": bound, "t_roofline_ms": 1e3 * t_roof, "frac": 1e3 * t_roof / ms_tn,
+                         "alg_bytes": byts, "alg_flops": m * F, "achieved_GBps": byts / (ms_tn / 1e3) / 1e9,
+                         "achieved_chain_TFLOPs": m * F / (ms_tn / 1e3) / 1e12},
+            "finite": finite}
+        del g
+        torch.cuda.empty_cache()
+    del st
+    torch.cuda.empty_cache()
+    if dense:
+        D = DenseQwenStack(n_layers, torch)
+        out["dense_params"] = D.params
+        for m, k in zip(ms, reps):
+            x = torch.randn(m, HIDDEN, device="cuda").to(torch.bfloat16)
+            g = capture_graph(lambda: D.forward(x), torch)
+            ms_d = time_graph(g.replay, k, 1, torch, None)
+            ln = out["lines"][f"M={m}"]
+            ln["dense_cublas"] = {"ms_per_pass": ms_d, "tokens_per_s": m / (ms_d / 1e3),
+                                  "weight_GB": 2 * D.params / 1e9}
+            ln["speedup_vs_dense"] = ms_d / ln["ms_per_pass"]
+            del g
+            torch.cuda.empty_cache()
+        del D
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -268,6 +446,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense cuBLAS comparison")
     ap.add_argument("--no-prefill", action="store_true", help="skip the secondary cfg3 prefill measurement")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the secondary cfg4 64-layer stack measurement")
+    ap.add_argument("--cfg4-layers", type=int, default=64)
     ap.add_argument("--flags", type=int, default=0, help="TNL_PLAN_* preference for every layer")
     ap.add_argument("--microbatches", type=int, default=2,
                     help="concurrent token groups (streams) the M tokens are split into inside the graph")
@@ -447,10 +627,17 @@ def main():
         b_bytes = 2 * (P3 + Mp * (5120 + 5120))
         b_flops = Mp * sum(l_.chain_flops_per_token() for l_ in (g_, u_, d_))
         t_roof_mlp = max(b_bytes / (hbm * 1e9), b_flops / (tc * 1e12))
+        # what the kernels execute (merged cut: 2*r_cut*(rows+cols) per token and projection)
+        x_flops = Mp * sum(l_.plan(torch.bfloat16).info["cut_flops_per_token"] for l_ in (g_, u_, d_))
         prefill["mlp_block"] = {"what": "Qwen3-32B MLP block y = down(silu(gate(x)) * up(x)), TT r64, one tnl_mlp_forward",
                                 "M": Mp, "ms": ms_b, "tokens_per_s": Mp / (ms_b / 1e3), "fused": bool(blk.fused),
                                 "t_roofline_ms": 1e3 * t_roof_mlp, "frac_roofline": t_roof_mlp / (ms_b / 1e3),
-                                "chain_TFLOPs": b_flops / (ms_b / 1e3) / 1e12}
+                                "chain_TFLOPs": b_flops / (ms_b / 1e3) / 1e12,
+                                "executed_flops": x_flops, "executed_TFLOPs": x_flops / (ms_b / 1e3) / 1e12,
+                                "frac_tensor_executed": x_flops / (tc * 1e12) / (ms_b / 1e3),
+                                "note": "frac_roofline divides the chain-flop/byte roofline time by the block time; "
+                                        "frac_tensor_executed is the flops the kernels execute (merged cut) over "
+                                        "the tensor-core peak"}
         blk.close()
         del xs, yp
 
@@ -519,6 +706,14 @@ def main():
                                                                                    if name == "fp32" else "bf16 tensor / HBM"),
                           "plan": pls[0].info["plan_small_name"]}
 
+    stack_cfg4 = None
+    if world == 1 and not args.no_cfg4:
+        try:
+            stack_cfg4 = bench_cfg4(hbm, tc, torch, n_layers=args.cfg4_layers, dense=not args.no_dense)
+        except Exception as exc:  # report, never fail the headline run
+            stack_cfg4 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         times, names = cpu_reference_sample(M, 7)
@@ -576,6 +771,7 @@ def main():
         "prefill_cfg3": prefill,
         "cfg1_m16": cfg1,
         "sharded_prefill_cfg5": sharded,
+        "stack_cfg4": stack_cfg4,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

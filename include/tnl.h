@@ -177,6 +177,26 @@ TNL_API tnl_status tnl_jacobi_sweeps(double* work, double* rot, int64_t batch, i
 
 
 
+/* The same sweeps for ONE large problem (e.g. a 5120 x 640 unfolding) in a parallel order: the
+ * Brent-Luk round-robin ordering rotates n/2 disjoint pairs per step, one warp per pair across a
+ * persistent cooperative grid, one grid barrier per step. Same skip rules and rotation formulas;
+ * the pair ORDER differs from the reference's cyclic order (tensor_core.py:203-212), so results
+ * agree with it up to rounding (spectra to <= 1e-10 relative) and the sweep count may differ.
+ * Opt-in: the batched cyclic kernel above stays the parity path. `sweeps` (device int32, may be
+ * NULL) receives the sweep count. */
+TNL_API tnl_status tnl_jacobi_sweeps_parallel(double* work, double* rot, int64_t n, int64_t m, int64_t nv, double tol,
+                                              int32_t max_sweeps, int32_t* sweeps, void* stream);
+
+/* The post-processing of _jacobi_svd (tensor_core.py:214-235) on the device, batched, one CTA per
+ * problem: values = row norms of the swept `work` (batch x n x m) in stable descending order,
+ * left (batch x m x n) = work[order]^T / values, completed for exactly-zero values by the greedy
+ * canonical pick of _complete_basis (:185-200), right (batch x n x n) = rot[order]^T, and the sign
+ * convention (largest-|.| entry of each left vector positive, right flipped with it). Requires
+ * m >= n (the reference transposes wide inputs first; swap left/right for them). `scratch`:
+ * device buffer of batch * (2n + 2m) doubles. All pointers device memory, row-major. */
+TNL_API tnl_status tnl_svd_finish(const double* work, const double* rot, int64_t batch, int64_t n, int64_t m,
+                                  double* left, double* values, double* right, double* scratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

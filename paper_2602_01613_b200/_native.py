@@ -37,6 +37,8 @@ EXPORTED = (
     "tnl_forward_host",
     "tnl_reconstruct",
     "tnl_jacobi_sweeps",
+    "tnl_jacobi_sweeps_parallel",
+    "tnl_svd_finish",
 )
 # include/tnl_stack.h: decoder-stack extensions (no reference counterpart; the Qwen3 stack driver).
 EXPORTED_STACK = (
@@ -154,6 +156,10 @@ def load():
         lib.tnl_plan_set_trace.restype = ctypes.c_int
         lib.tnl_jacobi_sweeps.argtypes = [P, P, i64, i64, i64, i64, ctypes.c_double, ctypes.c_int32, P, P]
         lib.tnl_jacobi_sweeps.restype = ctypes.c_int
+        lib.tnl_jacobi_sweeps_parallel.argtypes = [P, P, i64, i64, i64, ctypes.c_double, ctypes.c_int32, P, P]
+        lib.tnl_jacobi_sweeps_parallel.restype = ctypes.c_int
+        lib.tnl_svd_finish.argtypes = [P, P, i64, i64, i64, P, P, P, P, P]
+        lib.tnl_svd_finish.restype = ctypes.c_int
         lib.tnl_add_rmsnorm.argtypes = [P, i64, P, i64, P, i64, i64, i64, ctypes.c_float, P]
         lib.tnl_add_rmsnorm.restype = ctypes.c_int
         lib.tnl_copy_async.argtypes = [P, P, ctypes.c_size_t, P]

@@ -53,5 +53,9 @@ int launch_copy16(void* dst, const void* src, size_t bytes, int sms, cudaStream_
 // jacobi.cu: batched one-sided Jacobi sweeps (tnl_jacobi_sweeps)
 int launch_jacobi_sweeps(double* work, double* rot, int64_t batch, int n, int m, int nv, double tol, int max_sweeps,
                          int32_t* sweeps, cudaStream_t st);
+int launch_jacobi_parallel(double* work, double* rot, int n, int m, int nv, double tol, int max_sweeps,
+                           int32_t* sweeps, unsigned int* sync, int sms, cudaStream_t st);
+int launch_svd_finish(const double* work, const double* rot, int64_t batch, int n, int m, double* left, double* values,
+                      double* right, double* scratch, cudaStream_t st);
 
 }  // namespace tnl

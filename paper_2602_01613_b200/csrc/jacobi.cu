@@ -17,6 +17,7 @@
 // grants its own numpy twin ("bit-for-bit up to summation order inside dot products").
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -208,6 +209,292 @@ int launch_jacobi_sweeps(double* work, double* rot, int64_t batch, int n, int m,
   JAC_REG(8, 8)
 #undef JAC_REG
   jacobi_sweeps_kernel<<<(unsigned)grid, 32 * JW, 0, st>>>(work, rot, batch, n, m, nv, tol, max_sweeps, sweeps);
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Parallel-ordering sweeps for one LARGE problem (opt-in; the single
+// unfoldings of a Qwen-shaped decomposition take hours in the reference's cyclic order).
+//
+// Brent-Luk round-robin ("circle") ordering: a sweep is n' - 1 steps (n' = n rounded up to even),
+// each step rotates n'/2 DISJOINT pairs, so all pairs of a step run concurrently — one warp per
+// pair, pairs spread over a persistent cooperative grid, one grid barrier per step. Every pair is
+// visited once per sweep, with the reference's skip rules and rotation formulas (the (p, q) roles
+// follow p < q, as in the cyclic order); the pair ORDER differs from the reference's cyclic
+// order, so results agree up to rounding (spectrum parity <= 1e-10, singular vectors up to the
+// sign convention applied afterwards) and the sweep count may differ. A sweep with no rotation
+// ends the loop, as in the reference.
+// ---------------------------------------------------------------------------------------------
+
+namespace {
+
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = *(volatile unsigned int*)gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*(volatile unsigned int*)gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// partner layout of the circle method: position 0 fixed, positions 1..n'-1 rotate by one per step
+__device__ __forceinline__ int rr_member(int pos, int step, int np) {
+  return pos == 0 ? 0 : 1 + ((pos - 1 + step) % (np - 1));
+}
+
+__global__ void __launch_bounds__(256) jacobi_parallel_kernel(double* __restrict__ W, double* __restrict__ R, int n,
+                                                              int m, int nv, double tol, int max_sweeps,
+                                                              int32_t* sweeps_out, unsigned int* sync) {
+  unsigned int* bar_count = sync;
+  unsigned int* bar_gen = sync + 1;
+  unsigned int* rot_sweep = sync + 2;  // 1 + index of the last sweep that rotated (monotonic)
+  const int np = n + (n & 1);
+  const int pairs = np / 2;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  int sweeps = 0;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int step = 0; step < np - 1; ++step) {
+      for (int k = gwarp; k < pairs; k += nwarps) {
+        int p = rr_member(k, step, np), q = rr_member(np - 1 - k, step, np);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        if (q >= n) continue;  // the dummy column of an odd n
+        double* wp_row = W + (int64_t)p * m;
+        double* wq_row = W + (int64_t)q * m;
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          const double wp = wp_row[i], wq = wq_row[i];
+          app = __dadd_rn(app, __dmul_rn(wp, wp));
+          aqq = __dadd_rn(aqq, __dmul_rn(wq, wq));
+          apq = __dadd_rn(apq, __dmul_rn(wp, wq));
+        }
+        app = warp_sum(app);
+        aqq = warp_sum(aqq);
+        apq = warp_sum(apq);
+        if (app == 0.0 || aqq == 0.0) continue;
+        if (fabs(apq) <= __dmul_rn(tol, sqrt(__dmul_rn(app, aqq)))) continue;
+        const double zeta = __ddiv_rn(__dsub_rn(aqq, app), __dmul_rn(2.0, apq));
+        const double t = __ddiv_rn(copysign(1.0, zeta), __dadd_rn(fabs(zeta), sqrt(__dadd_rn(1.0, __dmul_rn(zeta, zeta)))));
+        const double c = __ddiv_rn(1.0, sqrt(__dadd_rn(1.0, __dmul_rn(t, t))));
+        const double s = __dmul_rn(c, t);
+        for (int i = lane; i < m; i += 32) {
+          const double wp = wp_row[i], wq = wq_row[i];
+          wp_row[i] = __dsub_rn(__dmul_rn(c, wp), __dmul_rn(s, wq));
+          wq_row[i] = __dadd_rn(__dmul_rn(s, wp), __dmul_rn(c, wq));
+        }
+        double* rp_row = R + (int64_t)p * nv;
+        double* rq_row = R + (int64_t)q * nv;
+        for (int i = lane; i < nv; i += 32) {
+          const double vp = rp_row[i], vq = rq_row[i];
+          rp_row[i] = __dsub_rn(__dmul_rn(c, vp), __dmul_rn(s, vq));
+          rq_row[i] = __dadd_rn(__dmul_rn(s, vp), __dmul_rn(c, vq));
+        }
+        if (lane == 0) atomicMax(rot_sweep, (unsigned int)sweep + 1u);
+      }
+      grid_barrier(bar_count, bar_gen, gridDim.x);
+    }
+    ++sweeps;
+    if (*(volatile unsigned int*)rot_sweep < (unsigned int)sweep + 1u) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && sweeps_out) *sweeps_out = sweeps;
+}
+
+// ---------------------------------------------------------------------------------------------
+// SVD post-processing of _jacobi_svd (tensor_core.py:214-235) on the device, one CTA per problem:
+// column norms of the swept work rows, stable descending order, normalised left vectors,
+// right = rot[order]^T, greedy canonical completion of the left basis for exactly-zero values
+// (_complete_basis, tensor_core.py:185-200: residual I - B B^T, largest column norm, lowest index on
+// ties, orthogonalise, normalise), and the sign convention (largest-|.| entry of each left vector
+// positive, right flipped with it). Outputs per problem: left (m x n), values (n), right (n x n),
+// row-major. Summation order inside the norms / dot products differs from numpy's.
+// ---------------------------------------------------------------------------------------------
+
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = __dadd_rn(s, red[i]);
+  return s;
+}
+
+// argmax of v over [0, n) (first index on ties); returns the index (all threads)
+__device__ int block_argmax(double v, int idx, double* redv, int* redi) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    redv[w] = v;
+    redi[w] = idx;
+  }
+  __syncthreads();
+  double bv = redv[0];
+  int bi = redi[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+    if (redv[i] > bv || (redv[i] == bv && redi[i] < bi)) {
+      bv = redv[i];
+      bi = redi[i];
+    }
+  return bi;
+}
+
+__global__ void __launch_bounds__(256) svd_finish_kernel(const double* __restrict__ work, const double* __restrict__ rot,
+                                                         int n, int m, double* __restrict__ left, double* __restrict__ values,
+                                                         double* __restrict__ right, double* __restrict__ scratch) {
+  __shared__ double redv[8];
+  __shared__ int redi[8];
+  const int64_t b = blockIdx.x;
+  const double* Wb = work + b * (int64_t)n * m;
+  const double* Rb = rot + b * (int64_t)n * n;
+  double* Lb = left + b * (int64_t)m * n;
+  double* Vb = values + b * (int64_t)n;
+  double* RTb = right + b * (int64_t)n * n;
+  double* norms = scratch + b * (int64_t)(2 * n + 2 * m);  // [n] norms, [n] order (as double), [m] v, [m] c-norms^2
+  double* orderd = norms + n;
+  double* vbuf = orderd + n;
+  // 1. row norms of work
+  for (int j = 0; j < n; ++j) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) acc = __dadd_rn(acc, __dmul_rn(Wb[(int64_t)j * m + i], Wb[(int64_t)j * m + i]));
+    acc = block_sum(acc, redv);
+    if (threadIdx.x == 0) norms[j] = sqrt(acc);
+  }
+  __syncthreads();
+  // 2. stable descending order: rank_j = #{i : norm_i > norm_j} + #{i < j : norm_i == norm_j}
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double nj = norms[j];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) rank += (norms[i] > nj) || (norms[i] == nj && i < j);
+    orderd[rank] = (double)j;
+  }
+  __syncthreads();
+  // 3. values, left = work[order] / values (positive values), right = rot[order]^T
+  int positive = 0;
+  for (int k = 0; k < n; ++k) positive += norms[(int)orderd[k]] > 0.0;
+  for (int k = 0; k < n; ++k) {
+    const int j = (int)orderd[k];
+    const double v = norms[j];
+    if (threadIdx.x == 0) Vb[k] = v;
+    for (int i = threadIdx.x; i < m; i += blockDim.x)
+      Lb[(int64_t)i * n + k] = k < positive ? __ddiv_rn(Wb[(int64_t)j * m + i], v) : 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) RTb[(int64_t)i * n + k] = Rb[(int64_t)j * n + i];
+  }
+  __syncthreads();
+  // 4. _complete_basis for the exactly-zero tail
+  for (int j = positive; j < n; ++j) {
+    // column norms of resid = I - B B^T, B = left[:, :j]
+    double best = -1.0;
+    int besti = 0;
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      double s2 = 0.0;
+      for (int r = 0; r < m; ++r) {
+        double bb = 0.0;
+        for (int k = 0; k < j; ++k) bb = __dadd_rn(bb, __dmul_rn(Lb[(int64_t)r * n + k], Lb[(int64_t)c * n + k]));
+        const double e = __dsub_rn(r == c ? 1.0 : 0.0, bb);
+        s2 = __dadd_rn(s2, __dmul_rn(e, e));
+      }
+      const double nc = sqrt(s2);
+      if (nc > best) {
+        best = nc;
+        besti = c;
+      }
+    }
+    const int pick = block_argmax(best, besti, redv, redi);
+    // v = resid[:, pick]; v -= B (B^T v); u_j = v / |v|
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+      double bb = 0.0;
+      for (int k = 0; k < j; ++k) bb = __dadd_rn(bb, __dmul_rn(Lb[(int64_t)r * n + k], Lb[(int64_t)pick * n + k]));
+      vbuf[r] = __dsub_rn(r == pick ? 1.0 : 0.0, bb);
+    }
+    __syncthreads();
+    for (int k = 0; k < j; ++k) {  // coefficients B^T v, then v -= B coef
+      double acc = 0.0;
+      for (int r = threadIdx.x; r < m; r += blockDim.x) acc = __dadd_rn(acc, __dmul_rn(Lb[(int64_t)r * n + k], vbuf[r]));
+      acc = block_sum(acc, redv);
+      if (threadIdx.x == 0) orderd[k] = acc;  // order no longer needed: reuse as coefficient buffer
+      __syncthreads();
+    }
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < j; ++k) acc = __dadd_rn(acc, __dmul_rn(Lb[(int64_t)r * n + k], orderd[k]));
+      vbuf[r] = __dsub_rn(vbuf[r], acc);
+    }
+    __syncthreads();
+    double nn = 0.0;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) nn = __dadd_rn(nn, __dmul_rn(vbuf[r], vbuf[r]));
+    nn = sqrt(block_sum(nn, redv));
+    for (int r = threadIdx.x; r < m; r += blockDim.x) Lb[(int64_t)r * n + j] = __ddiv_rn(vbuf[r], nn);
+    __syncthreads();
+  }
+  // 5. sign convention
+  for (int j = 0; j < n; ++j) {
+    double best = -1.0;
+    int besti = 0;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+      const double a = fabs(Lb[(int64_t)r * n + j]);
+      if (a > best) {
+        best = a;
+        besti = r;
+      }
+    }
+    const int piv = block_argmax(best, besti, redv, redi);
+    const bool flip = Lb[(int64_t)piv * n + j] < 0.0;
+    __syncthreads();
+    if (flip) {
+      for (int r = threadIdx.x; r < m; r += blockDim.x) Lb[(int64_t)r * n + j] = -Lb[(int64_t)r * n + j];
+      for (int r = threadIdx.x; r < n; r += blockDim.x) RTb[(int64_t)r * n + j] = -RTb[(int64_t)r * n + j];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int launch_jacobi_parallel(double* work, double* rot, int n, int m, int nv, double tol, int max_sweeps,
+                           int32_t* sweeps, unsigned int* sync, int sms, cudaStream_t st) {
+  // one warp per pair of a step, four warps per CTA, spread over as many SMs as there are pairs
+  const int pairs = (n + 1) / 2;
+  constexpr int kThreads = 128;
+  int blocks = std::min(sms, std::max(1, (pairs + 3) / 4));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_parallel_kernel, kThreads, 0);
+  blocks = std::min(blocks, std::max(1, per_sm) * sms);  // co-residency for the grid barrier
+  if (cudaMemsetAsync(sync, 0, 4 * sizeof(unsigned int), st) != cudaSuccess) return (int)cudaGetLastError();
+  void* args[] = {&work, &rot, &n, &m, &nv, &tol, &max_sweeps, &sweeps, &sync};
+  cudaError_t e =
+      cudaLaunchCooperativeKernel((const void*)jacobi_parallel_kernel, dim3(blocks), dim3(kThreads), args, 0, st);
+  count_launch();
+  return (int)e;
+}
+
+int launch_svd_finish(const double* work, const double* rot, int64_t batch, int n, int m, double* left, double* values,
+                      double* right, double* scratch, cudaStream_t st) {
+  if (batch <= 0) return 0;
+  svd_finish_kernel<<<(unsigned)batch, 256, 0, st>>>(work, rot, n, m, left, values, right, scratch);
   count_launch();
   return (int)cudaGetLastError();
 }

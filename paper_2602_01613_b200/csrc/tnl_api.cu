@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -70,6 +71,51 @@ static tnl_status fail(tnl_status st, const char* fmt, ...) {
                   __FILE__, __LINE__);                                                  \
   } while (0)
 
+// Plan-build stage timer (TNL_BUILD_PROFILE=1: one line per plan on stderr; measurement aid).
+struct BuildTimer {
+  bool on = getenv("TNL_BUILD_PROFILE") && atoi(getenv("TNL_BUILD_PROFILE")) != 0;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  char buf[512];
+  int len = 0;
+  void mark(const char* what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    auto n = std::chrono::steady_clock::now();
+    len += snprintf(buf + len, sizeof buf - len, " %s=%.2fms", what,
+                    std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
+// Device allocations of plans, MLP blocks and their build temporaries come from the device's
+// stream-ordered memory pool with an unlimited release threshold: building the 448 projections of
+// the cfg4 stack allocates and frees ~900 panel temporaries, which cudaMalloc / cudaFree turned into
+// driver calls with implicit device synchronisation (seconds in total); from the pool they are
+// sub-allocations of memory the process already holds.
+static cudaError_t dev_alloc(void** p, size_t bytes) {
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    configured = dev;
+  }
+  cudaError_t e = cudaMallocAsync(p, bytes, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  return e;
+}
+static void dev_free(void* p) {
+  if (p) cudaFreeAsync(p, 0);
+}
+template <typename T>
+static cudaError_t dev_alloc(T** p, size_t bytes) {
+  return dev_alloc(reinterpret_cast<void**>(p), bytes);
+}
+
 static inline int64_t prod(const int64_t* a, int lo, int hi) {
   int64_t p = 1;
   for (int i = lo; i < hi; ++i) p *= a[i];
@@ -108,6 +154,16 @@ __global__ void identity_f32(float* dst, int64_t rows, int64_t cols, int64_t off
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = e / cols, c = e % cols;
     dst[e] = (c == r + offset) ? 1.f : 0.f;
+  }
+}
+// out[a][b][c][d] (contiguous) = X[a*sxa + c*sxc] * Y[b*syb + d*syd] — the Kronecker-structured
+// panel of a two-mode Tucker side with no core in between (plan-time panel builder)
+__global__ void kron2_f32(float* out, const float* X, int64_t sxa, int64_t sxc, const float* Y, int64_t syb,
+                          int64_t syd, int64_t Da, int64_t Db, int64_t Dc, int64_t Dd) {
+  const int64_t n = Da * Db * Dc * Dd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t dd = e % Dd, cc = (e / Dd) % Dc, bb = (e / (Dd * Dc)) % Db, aa = e / (Dd * Dc * Db);
+    out[e] = X[aa * sxa + cc * sxc] * Y[bb * syb + dd * syd];
   }
 }
 __global__ void copy_2d_any(const void* src, int s_dt, int64_t s_r, int64_t s_c, void* dst, int d_dt,
@@ -764,9 +820,141 @@ static int64_t chain_flops(const tnl_plan* P) {
 // Device-side panel construction (fp32 generic steps on identity inputs)
 // ---------------------------------------------------------------------------
 static tnl_status alloc_arena(tnl_plan* P, size_t bytes) {
-  CUDA_TRY(cudaMalloc(&P->arena, bytes));
+  CUDA_TRY(dev_alloc(&P->arena, bytes));
   P->arena_bytes = bytes;
   CUDA_TRY(cudaMemset(P->arena, 0, bytes));
+  return TNL_OK;
+}
+
+// Direct two-mode panel construction (see build_panel_f32); TNL_ERR_UNSUPPORTED when the side is
+// not two modes (or the row range is not aligned to the second output mode).
+static tnl_status build_panel_2mode(tnl_plan* P, int seg, float* out, cudaStream_t st) {
+  const int d = P->d, rm = P->rm;
+  const int64_t* ms = P->ms;
+  const int64_t* r = P->rk;
+  const int64_t K = P->r_cut;
+  const bool ttr = P->family == TNL_FAMILY_TT || P->family == TNL_FAMILY_TR;
+  const bool tucker = P->family == TNL_FAMILY_TUCKER;
+  if (!(ttr || tucker)) return TNL_ERR_UNSUPPORTED;
+  if (seg == SEG_INPUT && d - rm == 2) {
+    const int64_t na = ms[rm], nb = ms[d - 1];
+    if (ttr) {
+      // B_in[alpha*B + b][ja*nb + jb] = sum_c C[b][ja][c] D[c][jb][alpha]; C natural (B, na, c),
+      // D permuted [alpha][jb][c]
+      const int64_t B = r[rm], c = r[d - 1], r0 = r[d];
+      GStep g = mk(r0, 1, B * na, c, nb);
+      g.A = P->gcore[rm];
+      g.sai = c;
+      g.sap = 1;
+      g.B = P->gcore[d - 1];
+      g.sb1 = nb * c;
+      g.sbp = 1;
+      g.sbj = c;
+      g.C = out;
+      g.sc1 = B * P->cols;
+      g.sci = nb;
+      g.scj = 1;
+      if (launch_generic_step(g, st)) return fail(TNL_ERR_CUDA, "panel (two-mode input) launch failed");
+    } else if (P->tucker_cut_in) {
+      // B_in[(ra, rb)][(ja, jb)] = Ua[ja][ra] * Ub[jb][rb]
+      const int64_t Ra = r[rm], Rb = r[d - 1];
+      const int64_t n = Ra * Rb * na * nb;
+      kron2_f32<<<grid_for(n), 256, 0, st>>>(out, P->gcore[1 + rm], 1, Ra, P->gcore[1 + d - 1], 1, Rb, Ra, Rb, na, nb);
+    } else {
+      // B_in[kappa][(ja, jb)] = sum_{ra, rb} G[kappa][ra][rb] Ua[ja][ra] Ub[jb][rb]  (kappa = out ranks)
+      const int64_t Ra = r[rm], Rb = r[d - 1];
+      float* w = nullptr;
+      CUDA_TRY(dev_alloc(&w, sizeof(float) * K * Ra * nb));
+      GStep g1 = mk(1, 1, K * Ra, Rb, nb);  // W[(kappa, ra)][jb] = sum_rb G[(kappa, ra)][rb] Ub[jb][rb]
+      g1.A = P->gcore[0];
+      g1.sai = Rb;
+      g1.sap = 1;
+      g1.B = P->gcore[1 + d - 1];
+      g1.sbp = 1;
+      g1.sbj = Rb;
+      g1.C = w;
+      g1.sci = nb;
+      g1.scj = 1;
+      GStep g2 = mk(K, 1, na, Ra, nb);  // B_in[kappa][ja][jb] = sum_ra Ua[ja][ra] W[kappa][ra][jb]
+      g2.A = P->gcore[1 + rm];
+      g2.sai = Ra;
+      g2.sap = 1;
+      g2.B = w;
+      g2.sb1 = Ra * nb;
+      g2.sbp = nb;
+      g2.sbj = 1;
+      g2.C = out;
+      g2.sc1 = P->cols;
+      g2.sci = nb;
+      g2.scj = 1;
+      const bool bad = launch_generic_step(g1, st) || launch_generic_step(g2, st);
+      cudaStreamSynchronize(st);
+      dev_free(w);
+      if (bad) return fail(TNL_ERR_CUDA, "panel (two-mode Tucker input) launch failed");
+    }
+  } else if (seg == SEG_OUTPUT && rm == 2 && P->row_begin % ms[1] == 0 && P->row_end % ms[1] == 0) {
+    const int64_t n1 = ms[1];
+    const int64_t i0b = P->row_begin / n1, n0l = (P->row_end - P->row_begin) / n1;
+    if (ttr) {
+      // A_out[(i0, i1)][alpha*B + b] = sum_a A0[i0][(alpha, a)] B1[a][i1][b]; A0 permuted [i0][(alpha, a)]
+      const int64_t r0 = r[0], a = r[1], B = r[2];
+      GStep g = mk(r0, n1, n0l, a, B);
+      g.A = P->gcore[0] + i0b * r0 * a;
+      g.sa1 = a;
+      g.sai = r0 * a;
+      g.sap = 1;
+      g.B = P->gcore[1];
+      g.sb2 = B;
+      g.sbp = n1 * B;
+      g.sbj = 1;
+      g.C = out;
+      g.sc1 = B;
+      g.sc2 = K;
+      g.sci = n1 * K;
+      g.scj = 1;
+      if (launch_generic_step(g, st)) return fail(TNL_ERR_CUDA, "panel (two-mode output) launch failed");
+    } else if (!P->tucker_cut_in) {
+      // A_out[(i0, i1)][(r0, r1)] = U0[i0][r0] * U1[i1][r1]
+      const int64_t R0 = r[0], R1 = r[1];
+      const int64_t n = n0l * n1 * R0 * R1;
+      kron2_f32<<<grid_for(n), 256, 0, st>>>(out, P->gcore[1] + i0b * R0, R0, 1, P->gcore[2], R1, 1, n0l, n1, R0, R1);
+    } else {
+      // A_out[i0][i1][kappa] = sum_r0 U0[i0][r0] sum_r1 U1[i1][r1] G[r0][r1][kappa]
+      const int64_t R0 = r[0], R1 = r[1];
+      float* w = nullptr;
+      CUDA_TRY(dev_alloc(&w, sizeof(float) * R0 * n1 * K));
+      GStep g1 = mk(R0, 1, n1, R1, K);  // W[r0][i1][kappa]
+      g1.A = P->gcore[2];
+      g1.sai = R1;
+      g1.sap = 1;
+      g1.B = P->gcore[0];
+      g1.sb1 = R1 * K;
+      g1.sbp = K;
+      g1.sbj = 1;
+      g1.C = w;
+      g1.sc1 = n1 * K;
+      g1.sci = K;
+      g1.scj = 1;
+      GStep g2 = mk(1, 1, n0l, R0, n1 * K);  // A_out[i0][(i1, kappa)]
+      g2.A = P->gcore[1] + i0b * R0;
+      g2.sai = R0;
+      g2.sap = 1;
+      g2.B = w;
+      g2.sbp = n1 * K;
+      g2.sbj = 1;
+      g2.C = out;
+      g2.sci = n1 * K;
+      g2.scj = 1;
+      const bool bad = launch_generic_step(g1, st) || launch_generic_step(g2, st);
+      cudaStreamSynchronize(st);
+      dev_free(w);
+      if (bad) return fail(TNL_ERR_CUDA, "panel (two-mode Tucker output) launch failed");
+    }
+  } else {
+    return TNL_ERR_UNSUPPORTED;
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
   return TNL_OK;
 }
 
@@ -820,15 +1008,23 @@ static tnl_status build_panel_f32(tnl_plan* P, int seg, float* out, cudaStream_t
     CUDA_TRY(cudaGetLastError());
     return TNL_OK;
   }
+  // Two-mode sides (every BASELINE shape with d = 4, rm = 2): the panel is one contraction of the
+  // side's two cores (TT/TR: one batched step per closure index; Tucker: a Kronecker product of
+  // the two factors, or two factor steps applied to the core), built directly instead of by
+  // running the chain on identity columns (cfg4 down projections: 25600 identity columns).
+  {
+    tnl_status ds = build_panel_2mode(P, seg, out, st);
+    if (ds != TNL_ERR_UNSUPPORTED) return ds;
+  }
   const int64_t n_in = (seg == SEG_INPUT) ? P->cols : K;       // identity size
   const int64_t chunk = std::min<int64_t>(n_in, 512);
   float *eye = nullptr, *ws0 = nullptr, *ws1 = nullptr, *tmp = nullptr;
   const int64_t ms_tok = std::max<int64_t>(max_state_per_token(P), 1);
   const int64_t out_feats = (seg == SEG_INPUT) ? K : P->rows;
-  CUDA_TRY(cudaMalloc(&eye, sizeof(float) * chunk * n_in));
-  CUDA_TRY(cudaMalloc(&ws0, sizeof(float) * chunk * ms_tok));
-  CUDA_TRY(cudaMalloc(&ws1, sizeof(float) * chunk * ms_tok));
-  CUDA_TRY(cudaMalloc(&tmp, sizeof(float) * chunk * out_feats));
+  CUDA_TRY(dev_alloc(&eye, sizeof(float) * chunk * n_in));
+  CUDA_TRY(dev_alloc(&ws0, sizeof(float) * chunk * ms_tok));
+  CUDA_TRY(dev_alloc(&ws1, sizeof(float) * chunk * ms_tok));
+  CUDA_TRY(dev_alloc(&tmp, sizeof(float) * chunk * out_feats));
   tnl_status st_ret = TNL_OK;
   for (int64_t c0 = 0; c0 < n_in && st_ret == TNL_OK; c0 += chunk) {
     const int64_t m = std::min(chunk, n_in - c0);
@@ -852,10 +1048,10 @@ static tnl_status build_panel_f32(tnl_plan* P, int seg, float* out, cudaStream_t
     }
   }
   cudaStreamSynchronize(st);
-  cudaFree(eye);
-  cudaFree(ws0);
-  cudaFree(ws1);
-  cudaFree(tmp);
+  dev_free(eye);
+  dev_free(ws0);
+  dev_free(ws1);
+  dev_free(tmp);
   if (st_ret == TNL_OK) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TNL_ERR_CUDA, "panel build: %s", cudaGetErrorString(e));
@@ -875,6 +1071,7 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   if (compute_dtype != TNL_F32 && compute_dtype != TNL_BF16)
     return fail(TNL_ERR_ARG, "compute dtype must be TNL_F32 or TNL_BF16");
   std::unique_ptr<tnl_plan> P(new tnl_plan());
+  BuildTimer bt;
   P->family = L->family;
   P->d = L->ndim;
   P->rm = L->row_mode_count;
@@ -945,6 +1142,7 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     P->r_cut = r0 * r[rm];
   }
   P->param_count = pc;
+  bt.mark("host_load");
   P->chain_flops = chain_flops(P.get());
   P->cut_flops = 2 * P->r_cut * (P->rows + P->cols);
   P->max_state = max_state_per_token(P.get());
@@ -1038,12 +1236,14 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   }
   tnl_status as = alloc_arena(P.get(), bytes);
   if (as != TNL_OK) return as;
+  bt.mark("arena");
   char* base = static_cast<char*>(P->arena);
   for (size_t i = 0; i < host.size(); ++i) {
     float* dptr = reinterpret_cast<float*>(base + off[i]);
     CUDA_TRY(cudaMemcpy(dptr, host[i].data(), host[i].size() * 4, cudaMemcpyHostToDevice));
     P->gcore.push_back(dptr);
   }
+  bt.mark("upload");
   cudaStream_t st = 0;
   if (large == TNL_PLAN_CUT && dense) {
     P->wdense = reinterpret_cast<__nv_bfloat16*>(base + off_w);
@@ -1055,8 +1255,8 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     P->bin = reinterpret_cast<__nv_bfloat16*>(base + off_bin);
     P->aout = reinterpret_cast<__nv_bfloat16*>(base + off_aout);
     float *fb = nullptr, *fa = nullptr;
-    CUDA_TRY(cudaMalloc(&fb, sizeof(float) * P->r_cut * P->cols));
-    CUDA_TRY(cudaMalloc(&fa, sizeof(float) * rows_local * P->r_cut));
+    CUDA_TRY(dev_alloc(&fb, sizeof(float) * P->r_cut * P->cols));
+    CUDA_TRY(dev_alloc(&fa, sizeof(float) * rows_local * P->r_cut));
     tnl_status s1 = build_panel_f32(P.get(), SEG_INPUT, fb, st);
     tnl_status s2 = s1 == TNL_OK ? build_panel_f32(P.get(), SEG_OUTPUT, fa, st) : s1;
     if (s2 == TNL_OK) {
@@ -1067,9 +1267,10 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
           fa, DT_F32, P->r_cut, 1, P->aout, DT_BF16, P->r_pad, 1, rows_local, P->r_cut);
     }
     cudaStreamSynchronize(st);
-    cudaFree(fb);
-    cudaFree(fa);
+    dev_free(fb);
+    dev_free(fa);
     if (s2 != TNL_OK) return s2;
+    bt.mark("panels");
   }
   if (cut32) {
     P->bin32 = reinterpret_cast<float*>(base + off_b32);
@@ -1114,13 +1315,17 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
 
+  bt.mark("chain_ops");
   // ---- host staging for tnl_forward_host ----
   P->max_m = max_m;
   if (max_m > 0) {
     const size_t es = bf16 ? 2 : 4;
-    CUDA_TRY(cudaMalloc(&P->stage_x, es * max_m * P->cols));
-    CUDA_TRY(cudaMalloc(&P->stage_y, es * max_m * rows_local));
+    CUDA_TRY(dev_alloc(&P->stage_x, es * max_m * P->cols));
+    CUDA_TRY(dev_alloc(&P->stage_y, es * max_m * rows_local));
   }
+  if (bt.on)
+    fprintf(stderr, "[tnl build] family=%d d=%d rm=%d rows=%lld cols=%lld r_cut=%lld%s\n", P->family, P->d, P->rm,
+            (long long)P->rows, (long long)P->cols, (long long)P->r_cut, bt.buf);
   *out = P.release();
   return TNL_OK;
 }
@@ -2012,7 +2217,7 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
   if (B->gated) {
     const int64_t rgu = B->rg + B->ru;
     const size_t bytes = 2 * rgu * B->inter;
-    CUDA_TRY(cudaMalloc(&B->agu, bytes));
+    CUDA_TRY(dev_alloc(&B->agu, bytes));
     CUDA_TRY(cudaMemset(B->agu, 0, bytes));
     CUDA_TRY(cudaMemcpy2D(B->agu, 2 * rgu, gate->aout, 2 * gate->r_pad, 2 * gate->r_pad, B->inter,
                           cudaMemcpyDeviceToDevice));
@@ -2021,7 +2226,7 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
   }
   if (B->fused || B->dual || B->gated) {
     const size_t bytes = 2 * (B->rg + B->ru) * B->hidden;
-    CUDA_TRY(cudaMalloc(&B->bgu, bytes));
+    CUDA_TRY(dev_alloc(&B->bgu, bytes));
     CUDA_TRY(cudaMemset(B->bgu, 0, bytes));
     CUDA_TRY(cudaMemcpy(B->bgu, gate->bin, 2 * gate->r_pad * B->hidden, cudaMemcpyDeviceToDevice));
     CUDA_TRY(cudaMemcpy(B->bgu + B->rg * B->hidden, up->bin, 2 * up->r_pad * B->hidden, cudaMemcpyDeviceToDevice));
@@ -2033,8 +2238,9 @@ tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_pl
 
 tnl_status tnl_mlp_destroy(tnl_mlp* B) {
   if (!B) return TNL_OK;
-  cudaFree(B->bgu);
-  cudaFree(B->agu);
+  cudaDeviceSynchronize();
+  dev_free(B->bgu);
+  dev_free(B->agu);
   if (B->ev_fork) cudaEventDestroy(B->ev_fork);
   if (B->ev_join) cudaEventDestroy(B->ev_join);
   if (B->side) cudaStreamDestroy(B->side);
@@ -2281,6 +2487,44 @@ tnl_status tnl_jacobi_sweeps(double* work, double* rot, int64_t batch, int64_t n
   return TNL_OK;
 }
 
+tnl_status tnl_jacobi_sweeps_parallel(double* work, double* rot, int64_t n, int64_t m, int64_t nv, double tol,
+                                      int32_t max_sweeps, int32_t* sweeps, void* stream) {
+  if (n < 1 || m < 1 || nv < 0 || n > INT32_MAX || m > INT32_MAX || nv > INT32_MAX)
+    return fail(TNL_ERR_SHAPE, "jacobi problem shape n=%lld m=%lld nv=%lld", (long long)n, (long long)m,
+                (long long)nv);
+  if (!work || (nv > 0 && !rot)) return fail(TNL_ERR_ARG, "null argument");
+  if (!(tol >= 0.0) || max_sweeps < 0) return fail(TNL_ERR_ARG, "tol must be >= 0 and max_sweeps >= 0");
+  int dev = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // grid-barrier words (count, generation, last rotating sweep): one small buffer per device,
+  // allocated on first use; calls on one device are serialised by the caller's stream order
+  static unsigned int* sync_buf[64] = {nullptr};
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (dev < 64 && !sync_buf[dev]) CUDA_TRY(dev_alloc(&sync_buf[dev], 4 * sizeof(unsigned int)));
+  }
+  if (dev >= 64) return fail(TNL_ERR_UNSUPPORTED, "device index %d", dev);
+  const int err = tnl::launch_jacobi_parallel(work, rot, (int)n, (int)m, (int)nv, tol, max_sweeps, sweeps, sync_buf[dev],
+                                             sms, static_cast<cudaStream_t>(stream));
+  if (err) return fail(TNL_ERR_CUDA, "jacobi (parallel order) launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
+}
+
+tnl_status tnl_svd_finish(const double* work, const double* rot, int64_t batch, int64_t n, int64_t m, double* left,
+                          double* values, double* right, double* scratch, void* stream) {
+  if (batch < 0) return fail(TNL_ERR_ARG, "negative batch %lld", (long long)batch);
+  if (batch == 0) return TNL_OK;
+  if (n < 1 || m < n || n > INT32_MAX || m > INT32_MAX)
+    return fail(TNL_ERR_SHAPE, "svd problem shape m=%lld n=%lld (needs m >= n >= 1)", (long long)m, (long long)n);
+  if (!work || !rot || !left || !values || !right || !scratch) return fail(TNL_ERR_ARG, "null argument");
+  const int err = tnl::launch_svd_finish(work, rot, batch, (int)n, (int)m, left, values, right, scratch,
+                                         static_cast<cudaStream_t>(stream));
+  if (err) return fail(TNL_ERR_CUDA, "svd finish launch: %s", cudaGetErrorString((cudaError_t)err));
+  return TNL_OK;
+}
+
 tnl_status tnl_plan_set_trace(tnl_plan* plan, void* device_buffer) {
   if (!plan) return fail(TNL_ERR_ARG, "null plan");
   plan->trace = static_cast<unsigned long long*>(device_buffer);
@@ -2300,10 +2544,11 @@ tnl_status tnl_plan_create_rows(const tnl_layer_desc* desc, int32_t compute_dtyp
 
 tnl_status tnl_plan_destroy(tnl_plan* plan) {
   if (!plan) return TNL_OK;
-  cudaFree(plan->arena);
-  cudaFree(plan->stage_x);
-  cudaFree(plan->stage_y);
-  cudaFree(plan->stage_ws);
+  cudaDeviceSynchronize();  // work of any stream may still read the arena
+  dev_free(plan->arena);
+  dev_free(plan->stage_x);
+  dev_free(plan->stage_y);
+  dev_free(plan->stage_ws);
   delete plan;
   return TNL_OK;
 }
@@ -2386,9 +2631,9 @@ tnl_status tnl_forward_host(tnl_plan* P, const void* x_host, int64_t m, void* y_
   tnl_status s = tnl_workspace_size(P, P->max_m, &need);
   if (s) return s;
   if (P->stage_ws_bytes < need) {
-    cudaFree(P->stage_ws);
+    dev_free(P->stage_ws);
     P->stage_ws = nullptr;
-    CUDA_TRY(cudaMalloc(&P->stage_ws, need));
+    CUDA_TRY(dev_alloc(&P->stage_ws, need));
     CUDA_TRY(cudaMemset(P->stage_ws, 0, need));  // decode accumulator is zero at rest
     P->stage_ws_bytes = need;
   }
@@ -2411,10 +2656,10 @@ tnl_status tnl_reconstruct(const tnl_plan* plan, void* w, int64_t ldw, int32_t o
   const int64_t chunk = std::min<int64_t>(P->cols, 512);
   float *eye = nullptr, *ws0 = nullptr, *ws1 = nullptr, *tmp = nullptr;
   const int64_t mst = std::max<int64_t>(P->max_state, 1);
-  CUDA_TRY(cudaMalloc(&eye, sizeof(float) * chunk * P->cols));
-  CUDA_TRY(cudaMalloc(&ws0, sizeof(float) * chunk * mst));
-  CUDA_TRY(cudaMalloc(&ws1, sizeof(float) * chunk * mst));
-  CUDA_TRY(cudaMalloc(&tmp, sizeof(float) * chunk * P->rows));
+  CUDA_TRY(dev_alloc(&eye, sizeof(float) * chunk * P->cols));
+  CUDA_TRY(dev_alloc(&ws0, sizeof(float) * chunk * mst));
+  CUDA_TRY(dev_alloc(&ws1, sizeof(float) * chunk * mst));
+  CUDA_TRY(dev_alloc(&tmp, sizeof(float) * chunk * P->rows));
   tnl_status ret = TNL_OK;
   const int odt = out_dtype == TNL_BF16 ? DT_BF16 : DT_F32;
   for (int64_t c0 = 0; c0 < P->cols && ret == TNL_OK; c0 += chunk) {
@@ -2435,10 +2680,10 @@ tnl_status tnl_reconstruct(const tnl_plan* plan, void* w, int64_t ldw, int32_t o
                                                           odt, 1, ldw, m, rows_local);
   }
   cudaError_t e = cudaStreamSynchronize(st);
-  cudaFree(eye);
-  cudaFree(ws0);
-  cudaFree(ws1);
-  cudaFree(tmp);
+  dev_free(eye);
+  dev_free(ws0);
+  dev_free(ws1);
+  dev_free(tmp);
   if (ret == TNL_OK && e != cudaSuccess) ret = fail(TNL_ERR_CUDA, "reconstruct: %s", cudaGetErrorString(e));
   return ret;
 }

@@ -8,11 +8,15 @@ Drop-in for the reference's only native component and its caller:
 * ``jacobi_sweeps_batched(work, rot, tol, max_sweeps)`` — a batch of independent problems as
   CUDA float64 tensors ``(B, n, m)`` / ``(B, n, nv)`` (one warp per problem, `csrc/jacobi.cu`);
 * ``full_svd`` / ``truncated_svd`` / ``svd_batched`` — `tensor_core._jacobi_svd`
-  (`tensor_core.py:203-235`) with the sweeps on the GPU and the reference's post-processing
-  (stable sort by column norm, normalisation, zero-column completion `:185-200`, sign
-  convention `:226-230`) and truncation policies (`:238-288`).
+  (`tensor_core.py:203-235`) with the sweeps AND the post-processing (stable sort by column norm,
+  normalisation, zero-column completion `:185-200`, sign convention `:226-230`) on the GPU
+  (``tnl_svd_finish``), and the reference's truncation policies (`:238-288`) applied to the
+  returned spectrum;
+* ``parallel=True`` — one large problem (a Qwen-shaped unfolding) swept in the round-robin
+  parallel order (``tnl_jacobi_sweeps_parallel``, one warp per pair across all SMs) instead of the
+  reference's cyclic order; equal up to rounding.
 
-All sweeps run in ``libtnl.so`` (``tnl_jacobi_sweeps``); there is no CPU fallback.
+All numerics run in ``libtnl.so``; there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -99,42 +103,12 @@ def jacobi_sweeps(work: np.ndarray, rot: np.ndarray, tol: float, max_sweeps: int
 # --- SVD (tensor_core.py:185-288) --------------------------------------------------------
 
 
-def _complete_basis(u: np.ndarray, fixed: int) -> None:
-    """Columns ``fixed:`` of ``u`` <- orthonormal filler, greedy canonical pick (tensor_core.py:185-200)."""
-    m, k = u.shape
-    for j in range(fixed, k):
-        basis = u[:, :j]
-        resid = np.eye(m) - basis @ basis.T
-        pick = int(np.argmax(np.linalg.norm(resid, axis=0)))
-        v = resid[:, pick]
-        v = v - basis @ (basis.T @ v)
-        u[:, j] = v / np.linalg.norm(v)
-
-
-def _finish(work: np.ndarray, rot: np.ndarray, m: int, n: int, transposed: bool) -> SvdResult:
-    """tensor_core.py:214-235: order by column norm, normalise, complete, sign-fix, un-transpose."""
-    norms = np.linalg.norm(work, axis=1)
-    order = np.argsort(-norms, kind="stable")
-    values = norms[order]
-    left = np.zeros((m, n))
-    right = rot[order].T.copy()
-    positive = int(np.count_nonzero(values > 0.0))
-    for j in range(positive):
-        left[:, j] = work[order[j]] / values[j]
-    if positive < n:
-        _complete_basis(left, positive)
-    for j in range(n):
-        pivot = int(np.argmax(np.abs(left[:, j])))
-        if left[pivot, j] < 0.0:
-            left[:, j] = -left[:, j]
-            right[:, j] = -right[:, j]
-    if transposed:
-        left, right = right, left
-    return SvdResult(left=left, values=values, right=right)
-
-
-def svd_batched(mats, tol: float = JACOBI_TOL, max_sweeps: int = JACOBI_MAX_SWEEPS) -> list:
-    """Full deterministic SVDs of same-shape matrices (list or (B, m, n) array), one GPU launch."""
+def svd_batched(mats, tol: float = JACOBI_TOL, max_sweeps: int = JACOBI_MAX_SWEEPS, parallel: bool = False) -> list:
+    """Full deterministic SVDs of same-shape matrices (list or (B, m, n) array), all on the GPU:
+    the sweeps (``tnl_jacobi_sweeps``, one launch for the batch — or, ``parallel=True``, the
+    round-robin ``tnl_jacobi_sweeps_parallel`` per problem for large single unfoldings) and the
+    post-processing of ``_jacobi_svd`` (tensor_core.py:214-235: ordering, normalisation, basis
+    completion, sign convention) by ``tnl_svd_finish``. Only the results return to the host."""
     a = np.asarray(mats, dtype=np.float64)
     if a.ndim != 3:
         raise ShapeError(f"expected a batch of rank-2 arrays, got shape {a.shape}")
@@ -150,9 +124,26 @@ def svd_batched(mats, tol: float = JACOBI_TOL, max_sweeps: int = JACOBI_MAX_SWEE
     dev = _device()
     work = torch.from_numpy(np.ascontiguousarray(np.swapaxes(a, 1, 2))).to(dev)  # (B, n, m): a.T per problem
     rot = torch.eye(n, dtype=torch.float64, device=dev).expand(b, n, n).contiguous()
-    jacobi_sweeps_batched(work, rot, tol, max_sweeps)
-    w, r = work.cpu().numpy(), rot.cpu().numpy()
-    return [_finish(w[i], r[i], m, n, transposed) for i in range(b)]
+    lib = N.load()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if parallel:
+        for i in range(b):
+            N.check(lib.tnl_jacobi_sweeps_parallel(ctypes.c_void_p(work[i].data_ptr()), ctypes.c_void_p(rot[i].data_ptr()),
+                                                   n, m, n, float(tol), int(max_sweeps), None, ctypes.c_void_p(stream)))
+    else:
+        jacobi_sweeps_batched(work, rot, tol, max_sweeps)
+    left = torch.empty((b, m, n), dtype=torch.float64, device=dev)
+    values = torch.empty((b, n), dtype=torch.float64, device=dev)
+    right = torch.empty((b, n, n), dtype=torch.float64, device=dev)
+    scratch = torch.empty((b, 2 * n + 2 * m), dtype=torch.float64, device=dev)
+    N.check(lib.tnl_svd_finish(ctypes.c_void_p(work.data_ptr()), ctypes.c_void_p(rot.data_ptr()), b, n, m,
+                               ctypes.c_void_p(left.data_ptr()), ctypes.c_void_p(values.data_ptr()),
+                               ctypes.c_void_p(right.data_ptr()), ctypes.c_void_p(scratch.data_ptr()),
+                               ctypes.c_void_p(stream)))
+    lh, vh, rh = left.cpu().numpy(), values.cpu().numpy(), right.cpu().numpy()
+    if transposed:
+        lh, rh = rh, lh
+    return [SvdResult(left=lh[i], values=vh[i], right=rh[i]) for i in range(b)]
 
 
 def _select_rank(values: np.ndarray, shape, policy) -> int:
@@ -186,20 +177,20 @@ def _select_rank(values: np.ndarray, shape, policy) -> int:
     raise TypeError(f"unknown truncation policy: {policy!r}")
 
 
-def truncated_svd(matrix, policy) -> SvdResult:
-    """Deterministic truncated SVD (tensor_core.py:269-288), sweeps on the GPU."""
+def truncated_svd(matrix, policy, parallel: bool = False) -> SvdResult:
+    """Deterministic truncated SVD (tensor_core.py:269-288), computed on the GPU."""
     m = np.asarray(matrix, dtype=np.float64)
     if m.ndim != 2:
         raise ShapeError(f"expected a rank-2 tensor, got rank {m.ndim}")
-    full = svd_batched(m[None])[0]
+    full = svd_batched(m[None], parallel=parallel)[0]
     r = _select_rank(full.values, m.shape, policy)
     return SvdResult(left=np.ascontiguousarray(full.left[:, :r]), values=full.values[:r].copy(),
                      right=np.ascontiguousarray(full.right[:, :r]))
 
 
-def full_svd(matrix) -> SvdResult:
+def full_svd(matrix, parallel: bool = False) -> SvdResult:
     """All ``min(m, n)`` singular triplets (tensor_core.py:291-296)."""
     m = np.asarray(matrix, dtype=np.float64)
     if m.ndim != 2:
         raise ShapeError(f"expected a rank-2 tensor, got rank {m.ndim}")
-    return truncated_svd(m, FixedRank(min(m.shape)))
+    return truncated_svd(m, FixedRank(min(m.shape)), parallel=parallel)

@@ -23,9 +23,10 @@ SiLU*mul kernel); each residual add is fused with the next RMSNorm into one pass
 
 from __future__ import annotations
 
-import torch
-
 import ctypes
+import time
+
+import torch
 
 from . import _native as N
 from . import synthetic as S
@@ -69,6 +70,7 @@ class QwenTNStack:
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.layers = []
+        self.build_s = {"host_cores": 0.0, "device_plans": 0.0}  # construction time split
         for l in range(n_layers):
             kinds = layer_kinds(l, n_layers)
             if mlp_kinds is not None:
@@ -76,10 +78,16 @@ class QwenTNStack:
             blk = {}
             for j, name in enumerate(("q", "k", "v", "o", "gate", "up", "down")):
                 rows, cols = SHAPES[name]
+                t0 = time.perf_counter()
                 layer = _tn(kinds[name], rows, cols, seed=seed + 100 * l + 10 * j)
+                t1 = time.perf_counter()
                 blk[name] = (kinds[name], layer, layer.plan(dtype, self.device))
+                self.build_s["host_cores"] += t1 - t0
+                self.build_s["device_plans"] += time.perf_counter() - t1
+            t1 = time.perf_counter()
             blk["mlp"] = TNMLP(blk["gate"][1], blk["up"][1], blk["down"][1], dtype=dtype, device=self.device,
                                fused=fused_mlp)
+            self.build_s["device_plans"] += time.perf_counter() - t1
             # decode: q -> (pass-through attention) -> o as one two-layer stack (one fused
             # boundary kernel: q's output rows never leave the SM)
             blk["qo"] = (ctypes.c_void_p * 2)(blk["q"][2].handle.value, blk["o"][2].handle.value)
