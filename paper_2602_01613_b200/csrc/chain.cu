@@ -213,11 +213,30 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const int m = tile_m * 128 + lrow;
       const bool ok = m < a.M;
+      // vector path: unit cut stride and a bond that fills whole 16-column groups -> one 16-byte
+      // bf16 store / four red.global.add.v4.f32 per 16 values (rows start 32-byte aligned: s_m is
+      // the padded cut width, a multiple of 16)
+      const bool vec = a.s_k == 1 && a.b % 16 == 0 && a.s_m % 16 == 0;
       for (int al = 0; al < a.r0; ++al) {
         for (int bb = 0; bb < a.b_pad; bb += 16) {
           float v[16];
           tmem_ld16(tD2 + lane_base + al * a.b_pad + bb, v);
           if (!ok) continue;
+          if (vec) {
+            const int64_t k = (int64_t)al * a.b + bb;
+            if (a.out_f32_atomic) {
+              float* o = static_cast<float*>(a.out) + (int64_t)m * a.s_m + k;
+#pragma unroll
+              for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+            } else {
+              uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + (int64_t)m * a.s_m + k);
+              o[0] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                                pack_bf16x2(v[6], v[7]));
+              o[1] = make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]), pack_bf16x2(v[12], v[13]),
+                                pack_bf16x2(v[14], v[15]));
+            }
+            continue;
+          }
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             if (bb + e >= a.b) continue;

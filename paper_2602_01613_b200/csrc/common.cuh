@@ -1,5 +1,6 @@
 // common.cuh — shared host helpers for libtnl.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -53,6 +54,11 @@ int launch_copy16(void* dst, const void* src, size_t bytes, int sms, cudaStream_
 // jacobi.cu: batched one-sided Jacobi sweeps (tnl_jacobi_sweeps)
 int launch_jacobi_sweeps(double* work, double* rot, int64_t batch, int n, int m, int nv, double tol, int max_sweeps,
                          int32_t* sweeps, cudaStream_t st);
+// tucker_chain.cu: fused Tucker-2 prefill chain y = U0 G U1^T x (maps: x box {64,128}; u1 box {64, r1p/2}
+// when r1p % 128 == 0 else {64, r1p}; g box {64, r0p}; u0 box {64, 256}; y box {64, 128} SW128).
+bool tucker2_chain_ok(int r1p, int r0p);
+int launch_tucker2_chain(const CUtensorMap& x, const CUtensorMap& u1, const CUtensorMap& g, const CUtensorMap& u0,
+                         const CUtensorMap& y, int M, int rows, int cols, int r1p, int r0p, cudaStream_t st);
 int launch_jacobi_parallel(double* work, double* rot, int n, int m, int nv, double tol, int max_sweeps,
                            int32_t* sweeps, unsigned int* sync, int sms, cudaStream_t st);
 int launch_svd_finish(const double* work, const double* rot, int64_t batch, int n, int m, double* left, double* values,

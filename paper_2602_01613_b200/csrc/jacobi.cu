@@ -252,32 +252,36 @@ __device__ __forceinline__ int rr_member(int pos, int step, int np) {
   return pos == 0 ? 0 : 1 + ((pos - 1 + step) % (np - 1));
 }
 
-__global__ void __launch_bounds__(256) jacobi_parallel_kernel(double* __restrict__ W, double* __restrict__ R, int n,
-                                                              int m, int nv, double tol, int max_sweeps,
-                                                              int32_t* sweeps_out, unsigned int* sync) {
+// one CTA (4 warps) per pair of a step: the three dot products and the rotation are spread over
+// 128 threads (40 elements each at m = 5120) instead of one warp, so the per-pair latency chain is
+// 4x shorter; CTAs loop over the step's pairs, one grid barrier per step.
+constexpr int JP_THREADS = 128;
+
+__global__ void __launch_bounds__(JP_THREADS) jacobi_parallel_kernel(double* __restrict__ W, double* __restrict__ R, int n,
+                                                                     int m, int nv, double tol, int max_sweeps,
+                                                                     int32_t* sweeps_out, unsigned int* sync) {
+  __shared__ double red[3][JP_THREADS / 32];
   unsigned int* bar_count = sync;
   unsigned int* bar_gen = sync + 1;
   unsigned int* rot_sweep = sync + 2;  // 1 + index of the last sweep that rotated (monotonic)
   const int np = n + (n & 1);
   const int pairs = np / 2;
-  const int lane = threadIdx.x & 31;
-  const int gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int sweeps = 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int step = 0; step < np - 1; ++step) {
-      for (int k = gwarp; k < pairs; k += nwarps) {
+      for (int k = blockIdx.x; k < pairs; k += gridDim.x) {
         int p = rr_member(k, step, np), q = rr_member(np - 1 - k, step, np);
         if (p > q) {
           const int t = p;
           p = q;
           q = t;
         }
-        if (q >= n) continue;  // the dummy column of an odd n
+        if (q >= n) continue;  // the dummy column of an odd n (uniform over the CTA)
         double* wp_row = W + (int64_t)p * m;
         double* wq_row = W + (int64_t)q * m;
         double app = 0.0, aqq = 0.0, apq = 0.0;
-        for (int i = lane; i < m; i += 32) {
+        for (int i = threadIdx.x; i < m; i += JP_THREADS) {
           const double wp = wp_row[i], wq = wq_row[i];
           app = __dadd_rn(app, __dmul_rn(wp, wp));
           aqq = __dadd_rn(aqq, __dmul_rn(wq, wq));
@@ -286,25 +290,39 @@ __global__ void __launch_bounds__(256) jacobi_parallel_kernel(double* __restrict
         app = warp_sum(app);
         aqq = warp_sum(aqq);
         apq = warp_sum(apq);
+        if (lane == 0) {
+          red[0][wid] = app;
+          red[1][wid] = aqq;
+          red[2][wid] = apq;
+        }
+        __syncthreads();
+        app = aqq = apq = 0.0;
+#pragma unroll
+        for (int w = 0; w < JP_THREADS / 32; ++w) {
+          app = __dadd_rn(app, red[0][w]);
+          aqq = __dadd_rn(aqq, red[1][w]);
+          apq = __dadd_rn(apq, red[2][w]);
+        }
+        __syncthreads();  // red[] is rewritten by the next pair
         if (app == 0.0 || aqq == 0.0) continue;
         if (fabs(apq) <= __dmul_rn(tol, sqrt(__dmul_rn(app, aqq)))) continue;
         const double zeta = __ddiv_rn(__dsub_rn(aqq, app), __dmul_rn(2.0, apq));
         const double t = __ddiv_rn(copysign(1.0, zeta), __dadd_rn(fabs(zeta), sqrt(__dadd_rn(1.0, __dmul_rn(zeta, zeta)))));
         const double c = __ddiv_rn(1.0, sqrt(__dadd_rn(1.0, __dmul_rn(t, t))));
         const double s = __dmul_rn(c, t);
-        for (int i = lane; i < m; i += 32) {
+        for (int i = threadIdx.x; i < m; i += JP_THREADS) {
           const double wp = wp_row[i], wq = wq_row[i];
           wp_row[i] = __dsub_rn(__dmul_rn(c, wp), __dmul_rn(s, wq));
           wq_row[i] = __dadd_rn(__dmul_rn(s, wp), __dmul_rn(c, wq));
         }
         double* rp_row = R + (int64_t)p * nv;
         double* rq_row = R + (int64_t)q * nv;
-        for (int i = lane; i < nv; i += 32) {
+        for (int i = threadIdx.x; i < nv; i += JP_THREADS) {
           const double vp = rp_row[i], vq = rq_row[i];
           rp_row[i] = __dsub_rn(__dmul_rn(c, vp), __dmul_rn(s, vq));
           rq_row[i] = __dadd_rn(__dmul_rn(s, vp), __dmul_rn(c, vq));
         }
-        if (lane == 0) atomicMax(rot_sweep, (unsigned int)sweep + 1u);
+        if (threadIdx.x == 0) atomicMax(rot_sweep, (unsigned int)sweep + 1u);
       }
       grid_barrier(bar_count, bar_gen, gridDim.x);
     }
@@ -476,17 +494,15 @@ __global__ void __launch_bounds__(256) svd_finish_kernel(const double* __restric
 
 int launch_jacobi_parallel(double* work, double* rot, int n, int m, int nv, double tol, int max_sweeps,
                            int32_t* sweeps, unsigned int* sync, int sms, cudaStream_t st) {
-  // one warp per pair of a step, four warps per CTA, spread over as many SMs as there are pairs
+  // one CTA per pair of a step (up to all pairs at once), co-resident for the grid barrier
   const int pairs = (n + 1) / 2;
-  constexpr int kThreads = 128;
-  int blocks = std::min(sms, std::max(1, (pairs + 3) / 4));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_parallel_kernel, kThreads, 0);
-  blocks = std::min(blocks, std::max(1, per_sm) * sms);  // co-residency for the grid barrier
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_parallel_kernel, JP_THREADS, 0);
+  const int blocks = std::max(1, std::min(pairs, std::max(1, per_sm) * sms));
   if (cudaMemsetAsync(sync, 0, 4 * sizeof(unsigned int), st) != cudaSuccess) return (int)cudaGetLastError();
   void* args[] = {&work, &rot, &n, &m, &nv, &tol, &max_sweeps, &sweeps, &sync};
   cudaError_t e =
-      cudaLaunchCooperativeKernel((const void*)jacobi_parallel_kernel, dim3(blocks), dim3(kThreads), args, 0, st);
+      cudaLaunchCooperativeKernel((const void*)jacobi_parallel_kernel, dim3(blocks), dim3(JP_THREADS), args, 0, st);
   count_launch();
   return (int)e;
 }

@@ -1646,6 +1646,24 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
     }
     return tc_step_p(P, t0, P->r_pad, P->aout, P->r_pad, M, rows_local, P->r_cut, y, ldy, false, 1, st);
   }
+  // Tucker-2 chain plan, prefill: the fused on-chip chain (tucker_chain.cu) — U1, G and U0 in one
+  // kernel, T1/T2 in TMEM/smem, a 2-CTA cluster per token tile
+  static const bool no_fused_tucker = getenv("TNL_TUCKER_FUSED") && atoi(getenv("TNL_TUCKER_FUSED")) == 0;  // A/B
+  if (P->tucker_chain && !swap && !fold && !no_fused_tucker && tucker2_chain_ok((int)P->r1p, (int)P->r0p) &&
+      !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0) {
+    const int64_t r1h = P->r1p % 128 == 0 ? P->r1p / 2 : P->r1p;
+    CUtensorMap tx, tu1, tg, tu0, ty;
+    int err;
+    if ((err = get_tmap(P, &tx, x, P->cols, M, ldx, 128)) || (err = get_tmap(P, &tu1, P->u1t, P->cols, P->r1p, P->cols, (int)r1h)) ||
+        (err = get_tmap(P, &tg, P->gmat, P->r1p, P->r0p, P->r1p, (int)P->r0p)) ||
+        (err = get_tmap(P, &tu0, P->u0, P->r0p, rows_local, P->r0p, 256)) ||
+        (err = get_tmap2(P, &ty, y, false, rows_local, M, ldy, 64, 128, 128)))
+      return fail(TNL_ERR_CUDA, "tensor map (fused Tucker-2 chain) failed: %d", err);
+    if ((err = launch_tucker2_chain(tx, tu1, tg, tu0, ty, (int)M, (int)rows_local, (int)P->cols, (int)P->r1p,
+                                    (int)P->r0p, st)))
+      return fail(TNL_ERR_CUDA, "fused Tucker-2 chain launch: %s", cudaGetErrorString((cudaError_t)err));
+    return TNL_OK;
+  }
   const __nv_bfloat16* win = P->tucker_chain ? P->u1t : P->bin;
   const int64_t k1 = P->tucker_chain ? P->r1p : P->r_pad;
   const __nv_bfloat16* wout = P->tucker_chain ? P->u0 : P->aout;

@@ -306,3 +306,31 @@ def test_qwen_stack_matches_oracle(m):
     assert np.isfinite(got).all()
     assert rel(ref, got) <= BF16_TOL
     assert rel(ref - x0, got - x0) <= 2 * BF16_TOL  # the four layers' contribution itself
+
+
+# --- the fused Tucker-2 chain (N2: U1 -> G -> U0 in one kernel, T1/T2 on chip) ------------------
+
+
+@pytest.mark.parametrize("shape", [(5120, 5120, 64), (5120, 5120, 128), (5120, 5120, 256), (8192, 5120, 256),
+                                   (1024, 5120, 128), (25600, 5120, 256), (5120, 25600, 256), (4160, 1024, 128),
+                                   (5120, 8192, 192)])
+@pytest.mark.parametrize("m", [65, 300, 4096])
+def test_tucker2_fused_chain(shape, m):
+    """TNL_PLAN_CHAIN on Tucker-2 at prefill sizes runs tucker2_chain_kernel (one launch): against
+    the oracle on the same bf16 values, and against the merged-cut plan."""
+    rows, cols, R = shape
+    L = O.synthetic_layer("tucker", (rows, cols), 1, (R, R), seed=67_000 + rows + R)
+    layer, Lr = tnl.CompressedLayer("tucker", (rows, cols), 1, core=O.round_bf16(L.core),
+                                    factors=[O.round_bf16(u) for u in L.factors]), None
+    x = O.round_bf16(O.synthetic_x(m, cols, seed=67_100 + m))
+    p = layer.plan(torch.bfloat16, flags=tnl.PLAN_CHAIN)
+    assert p.info["plan_large_name"] == "chain"
+    tnl.launch_count(reset=True)
+    y = p.forward(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
+    torch.cuda.synchronize()
+    assert tnl.launch_count(reset=True) == 1  # the whole chain is one kernel
+    ref = O.forward_torch_orient(oracle_of(layer, bf16=True), x)
+    got = y.double().cpu().numpy()
+    assert rel(ref, got) <= BF16_TOL
+    cut = fwd(layer, x, torch.bfloat16, tnl.PLAN_CUT)
+    assert rel(cut, got) <= BF16_TOL
