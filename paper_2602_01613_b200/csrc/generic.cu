@@ -157,6 +157,9 @@ int launch_b(const GStep& s, int64_t ti, int64_t tj, int64_t blocks, int64_t spl
 
 }  // namespace
 
+static thread_local bool t_deterministic = false;
+void set_generic_deterministic(bool on) { t_deterministic = on; }
+
 int launch_generic_step(const GStep& in, cudaStream_t stream) {
   GStep s = in;
   if (s.I <= 0 || s.J <= 0 || s.b1 <= 0 || s.b2 <= 0) return 0;
@@ -178,7 +181,7 @@ int launch_generic_step(const GStep& in, cudaStream_t stream) {
   // split P over CTAs and reduce with fp32 atomics (fp32 C only; summation order changes, the
   // exactness contract is fp32 rounding, not bitwise)
   int64_t splits = 1;
-  if (s.c_dt == DT_F32 && blocks < 148 && s.P >= 4 * TP * 2)
+  if (!t_deterministic && s.c_dt == DT_F32 && blocks < 148 && s.P >= 4 * TP * 2)
     splits = std::max<int64_t>(1, std::min<int64_t>((2 * 148 + blocks - 1) / blocks, s.P / (4 * TP)));
   if (splits > 1 && !s.accumulate) {
     const int64_t n = s.b1 * s.b2 * s.I * s.J;

@@ -29,4 +29,8 @@ struct GStep {
 // from wasting 64x64 tiles), then launches. Returns cudaError_t as int.
 int launch_generic_step(const GStep& s, cudaStream_t stream);
 
+// Plan building runs with split-K disabled (fixed summation order), so a plan's panels do not
+// depend on its row range: output-sharded plans reproduce the full plan's rows bit for bit.
+void set_generic_deterministic(bool on);
+
 }  // namespace tnl

@@ -1071,6 +1071,10 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   if (compute_dtype != TNL_F32 && compute_dtype != TNL_BF16)
     return fail(TNL_ERR_ARG, "compute dtype must be TNL_F32 or TNL_BF16");
   std::unique_ptr<tnl_plan> P(new tnl_plan());
+  struct DetGuard {  // deterministic panel construction (generic.cuh)
+    DetGuard() { set_generic_deterministic(true); }
+    ~DetGuard() { set_generic_deterministic(false); }
+  } det_guard;
   BuildTimer bt;
   P->family = L->family;
   P->d = L->ndim;

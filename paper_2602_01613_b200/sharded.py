@@ -10,8 +10,15 @@ Three ways to spread the work:
                   contiguous because row modes come first,
                   tn_decompositions.py:59-63) and computes only those; the
                   input side up to the cut is recomputed on every rank (r_cut
-                  per token). One ``all_gather_into_tensor`` (NCCL over NVLink)
-                  assembles y; the gathered layout is [G][M][rows/G].
+                  per token). Its kernels store the slice straight into its
+                  columns of the token-major y (a strided TMA store, no staging).
+                  Exchange, NCCL groups: y lives in symmetric memory and every
+                  rank writes its slice into the same columns of every peer's y
+                  over NVLink (P2P stores), then one device-side barrier — the
+                  only traffic beyond the local store is the (G-1)/G * M * rows
+                  NVLink ingress, and there is no gather buffer and no permute.
+                  Other backends (gloo in the CPU tests) all-gather the slices
+                  into [G][M][rows/G] and place them.
 
 The local compute is the C-ABI forward of a row-restricted plan
 (``tnl_plan_create_rows``). For CPU tests the compute callable can be
@@ -53,10 +60,14 @@ def token_shard_range(m: int, rank: int, world: int) -> tuple[int, int]:
 
 
 class OutputShardedLayer:
-    """Output-mode-sharded forward with one all-gather (prefill / large M)."""
+    """Output-mode-sharded forward with one exchange step (prefill / large M).
+
+    exchange: "auto" (symmetric-memory P2P on NCCL groups, else all-gather), "p2p", "allgather".
+    The P2P path returns its own symmetric buffer (valid until the next forward on this layer);
+    pass ``out`` to get a copy instead."""
 
     def __init__(self, layer: CompressedLayer, group=None, dtype=torch.bfloat16, device=None,
-                 local_forward: Callable | None = None):
+                 local_forward: Callable | None = None, exchange: str = "auto"):
         self.layer = layer
         self.group = group
         self.world = dist.get_world_size(group)
@@ -69,12 +80,51 @@ class OutputShardedLayer:
             plan = layer.plan(dtype, device, row_range=self.row_range)
             local_forward = plan.forward
         self.local_forward = local_forward
+        if exchange not in ("auto", "p2p", "allgather"):
+            raise ValueError(f"exchange must be auto / p2p / allgather, got {exchange!r}")
+        self.exchange = exchange
+        self._symm = None  # (m, device, buffer, handle)
+
+    def _use_p2p(self, device) -> bool:
+        if self.exchange == "allgather" or device.type != "cuda":
+            return False
+        try:
+            nccl = dist.get_backend(self.group) == "nccl"
+        except Exception:
+            nccl = False
+        if not nccl:
+            if self.exchange == "p2p":
+                raise ShapeError("exchange='p2p' needs an NCCL process group")
+            return False
+        return True
+
+    def _symm_buffer(self, m: int, device):
+        if self._symm is None or self._symm[0] != m or self._symm[1] != device:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            buf = symm_mem.empty((m, self.rows), dtype=self.dtype, device=device)
+            hdl = symm_mem.rendezvous(buf, self.group if self.group is not None else dist.group.WORLD)
+            self._symm = (m, device, buf, hdl)
+        return self._symm[2], self._symm[3]
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         m = x.shape[0]
-        per = self.row_range[1] - self.row_range[0]
-        # this rank's rows are computed straight into its slot of the gather buffer, and the
-        # all-gather runs in place (input = output slot `rank`): no staging copy
+        lo, hi = self.row_range
+        per = hi - lo
+        if self._use_p2p(x.device):
+            y, hdl = self._symm_buffer(m, x.device)
+            hdl.barrier(channel=0)  # every rank is done with the previous result in its y
+            self.local_forward(x, out=y[:, lo:hi])  # this rank's columns, stored in place
+            for p in range(self.world):
+                if p != self.rank:  # P2P stores of exactly this slice into the peer's y
+                    hdl.get_buffer(p, (m, self.rows), self.dtype)[:, lo:hi].copy_(y[:, lo:hi])
+            hdl.barrier(channel=1)  # every peer's slice has landed in our y
+            if out is not None:
+                out.copy_(y)
+                return out
+            return y
+        # all-gather: this rank's rows go straight into its slot of the gather buffer, the gather
+        # runs in place (input = output slot `rank`), then the slots are placed into y's columns
         flat = torch.empty((self.world * m, per), dtype=self.dtype, device=x.device)
         gathered = flat.view(self.world, m, per)
         try:
@@ -86,7 +136,6 @@ class OutputShardedLayer:
             gathered[self.rank].copy_(y_local)
         dist.all_gather_into_tensor(flat, gathered[self.rank], group=self.group)
         y = out if out is not None else torch.empty((m, self.rows), dtype=flat.dtype, device=flat.device)
-        # [G][M][rows/G] -> (M, rows): rank g's slice lands in columns [g*per, (g+1)*per)
         y.view(m, self.world, per).copy_(gathered.permute(1, 0, 2))
         return y
 

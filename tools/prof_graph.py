@@ -15,7 +15,10 @@ bank = S.cfg2_bank(copies)
 st = TNStack([l for _, l in bank], torch.bfloat16)
 st.capture(64, host_io=False, microbatches=2)
 st.x_dev.copy_(torch.tensor(S.make_x(64, 5120, seed=29_999), dtype=torch.bfloat16, device="cuda"))
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("replay")
 for _ in range(int(os.environ.get("REPLAYS", "5"))):
     st.replay()
+torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 print("ok", st.launches_per_pass)
