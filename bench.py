@@ -302,6 +302,27 @@ def ncu_traffic():
         return None, "no ncu capture committed"
 
 
+def ncu_graph_step_bytes():
+    """DRAM bytes of one replay of the decode graph (`ncu --graph-profiling graph`, the whole
+    70-layer step as one workload: profiles/r02/ncu_graph_decode_step.csv, tools/prof_graph.py);
+    median over the captured replays. (None, reason) if absent."""
+    import csv
+
+    path = os.path.join(ROOT, "profiles", "r02", "ncu_graph_decode_step.csv")
+    try:
+        lines = [ln for ln in open(path) if ln.startswith('"')]
+        rows = list(csv.reader(lines))
+        h = rows[0]
+        per = {}
+        for r in rows[1:]:
+            per.setdefault(r[0], {})[r[h.index("Metric Name")]] = float(r[h.index("Metric Value")].replace(",", ""))
+        tot = sorted(v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in per.values())
+        return tot[len(tot) // 2], (f"ncu --graph-profiling graph, dram__bytes_read.sum + dram__bytes_write.sum per "
+                                    f"replay of the whole step, median of {len(tot)} replays ({os.path.relpath(path, ROOT)})")
+    except (OSError, ValueError, KeyError, IndexError):
+        return None, "no graph-level ncu capture committed"
+
+
 def time_graph(replay, steps, warmup, torch, dist=None):
     for _ in range(warmup):
         replay()
@@ -751,6 +772,9 @@ def main():
             "frac": achieved_gbs / hbm,
             "traffic": ncu_traffic()[0],
             "traffic_note": ncu_traffic()[1],
+            "dram_bytes_per_step_graph": ncu_graph_step_bytes()[0],
+            "dram_bytes_per_step_graph_note": ncu_graph_step_bytes()[1] + "; the two token groups each stream "
+                                              "the 223 MB of panels (latency-bound chain: L2-hot runs no faster)",
             "algorithmic_bytes_per_step": alg_bytes,
             "plan_weight_bytes_per_step": plan_bytes,
             "t_roofline_ms": 1e3 * t_roof,

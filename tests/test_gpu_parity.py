@@ -178,6 +178,14 @@ def test_cfg3_full_size_properties():
     xs = x[idx].float().cpu().numpy().astype(np.float64)
     ref = O.forward_torch_orient(Lr, xs)
     assert rel(ref, y[idx].float().cpu().numpy()) <= BF16_TOL
+    # 1024 rows against the oracle: every token tile (64) and tile position contributes
+    g = torch.Generator().manual_seed(31_001)
+    rows = torch.cat([torch.arange(0, 8192, 128), torch.randperm(8192, generator=g)[:960]]).to(DEV)
+    ref_r = O.forward_torch_orient(Lr, x[rows].float().cpu().numpy().astype(np.float64))
+    got_r = y[rows].float().cpu().numpy()
+    assert rel(ref_r, got_r) <= BF16_TOL
+    per_row = np.linalg.norm(ref_r - got_r, axis=1) / np.linalg.norm(ref_r, axis=1)
+    assert float(per_row.max()) <= 2 * BF16_TOL  # no bad tile hides behind the aggregate
     # linearity: f(2x) == 2 f(x) (power-of-two scaling is exact; only summation order varies)
     y2 = p.forward((2 * x.float()).to(torch.bfloat16))
     d2 = (y2.float() - 2 * y.float()).norm() / (2 * y.float()).norm()
