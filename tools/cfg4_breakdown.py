@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2602_01613_b200.qwen_stack import QwenTNStack, HIDDEN, QDIM, KVDIM
 
-st = QwenTNStack(4)  # layers 0/3: Tucker-2 R256 edges; 1: TR4; 2: Tucker-4 (l % 3 = 1, 2)
+st = QwenTNStack(4, mlp_kinds=["tt64", "tr4", "tucker4", "tucker2-256"])  # one decoder layer per MLP kind
 M = 8192
 ws = st.workspace(M)
 b = st._buffers(M)
