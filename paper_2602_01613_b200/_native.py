@@ -108,7 +108,8 @@ _lock = threading.Lock()
 
 
 def lib_path() -> str:
-    return LIB_PATH
+    # TNL_LIB_AB: load an alternative in-tree build (A/B measurements of compile-time variants)
+    return os.environ.get("TNL_LIB_AB") or LIB_PATH
 
 
 def load():
@@ -117,12 +118,13 @@ def load():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
+        path = lib_path()
+        if not os.path.exists(path):
             raise DeviceError(
-                f"{LIB_PATH} is missing: build it with `python -m paper_2602_01613_b200.build` "
+                f"{path} is missing: build it with `python -m paper_2602_01613_b200.build` "
                 "(there is no CPU fallback)"
             )
-        lib = ctypes.CDLL(LIB_PATH)
+        lib = ctypes.CDLL(path)
         P = ctypes.c_void_p
         i64 = ctypes.c_int64
         lib.tnl_abi_version.restype = ctypes.c_int

@@ -163,10 +163,15 @@ __global__ void __launch_bounds__(192, 1)
           // the TMA store that used this staging buffer two chunks ago must have read it
           if (et == 0) tma_store_wait_read_le1();
           named_bar_sync(1, 128);
+          uint32_t raw[64];  // the chunk's 64 columns: two loads in flight, one wait
+          tmem_ld32_nowait(d + c0, raw);
+          tmem_ld32_nowait(d + c0 + 32, raw + 32);
+          tmem_wait_ld();
 #pragma unroll
           for (int c = 0; c < 64; c += 16) {
             float v[16];
-            tmem_ld16(d + c0 + c, v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(raw[c + e]);
             if constexpr (SCALE) {  // folded RMSNorm of the step's input rows
 #pragma unroll
               for (int e = 0; e < 16; ++e) v[e] *= rscale;
