@@ -115,7 +115,17 @@ __global__ void __launch_bounds__(FT, 1)
     if (elect_one()) {
       // both layers' weights first (independent of the previous kernel)
       mbar_arrive_expect_tx(wfull, (kbB + (LARGE ? 0 : 2 * nT)) * WBLK);
+      // L2 policy of the weight stream (TNL_DEC_WPOL at build time, A/B): 0 evict_first (default:
+      // keeps the accumulators and activations resident), 2 evict_last (the concurrent token
+      // groups re-read each layer's panels from L2 instead of HBM)
+#if defined(TNL_DEC_WPOL) && TNL_DEC_WPOL == 2
+      const uint64_t pol = policy_evict_last();
+#elif defined(TNL_DEC_WPOL) && TNL_DEC_WPOL == 1
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
       const uint64_t pol = policy_evict_first();
+#endif
       for (int kb = 0; kb < kbB; ++kb)
         tma_load_2d_hint(sWo + kb * WBLK, &tmWo, wfull, kb * 64, tile * 128, pol);
       if (!LARGE)
