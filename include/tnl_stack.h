@@ -103,6 +103,20 @@ TNL_API int64_t tnl_launch_count(int32_t reset);
  * NULL disables. Not for production use (adds global stores). */
 TNL_API tnl_status tnl_plan_set_trace(tnl_plan* plan, void* device_buffer);
 
+/* Shared-input group: plans that read the same activations (a decoder's q, k and v projections of
+ * one normalised hidden state). For prefill (M > 64) over bf16 merged-cut plans their B_in panels
+ * are stacked at create time, so ONE first-step GEMM reads x once into the concatenated cut
+ * activations (folded RMSNorm row scale applied there, opts->ss_in), then each plan's output step
+ * writes its own y. Otherwise (decode, other plan kinds) it runs the plans one after another.
+ * The plans must outlive the group; opts->accumulate is not supported by the stacked path. */
+typedef struct tnl_group tnl_group;
+TNL_API tnl_status tnl_group_create(const tnl_plan* const* plans, int32_t n, tnl_group** out);
+TNL_API tnl_status tnl_group_destroy(tnl_group* group);
+TNL_API tnl_status tnl_group_workspace_size(const tnl_group* group, int64_t m, size_t* bytes);
+TNL_API tnl_status tnl_group_forward_ex(const tnl_group* group, const void* x, int64_t m, int64_t ldx, void* const* ys,
+                                        const int64_t* ldys, void* workspace, size_t workspace_bytes,
+                                        const tnl_fwd_opts* opts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,10 @@ EXPORTED_STACK = (
     "tnl_copy_async",
     "tnl_launch_count",
     "tnl_plan_set_trace",
+    "tnl_group_create",
+    "tnl_group_destroy",
+    "tnl_group_workspace_size",
+    "tnl_group_forward_ex",
 )
 
 
@@ -158,6 +162,15 @@ def load():
         lib.tnl_plan_set_trace.restype = ctypes.c_int
         lib.tnl_jacobi_sweeps.argtypes = [P, P, i64, i64, i64, i64, ctypes.c_double, ctypes.c_int32, P, P]
         lib.tnl_jacobi_sweeps.restype = ctypes.c_int
+        lib.tnl_group_create.argtypes = [ctypes.POINTER(P), ctypes.c_int32, ctypes.POINTER(P)]
+        lib.tnl_group_create.restype = ctypes.c_int
+        lib.tnl_group_destroy.argtypes = [P]
+        lib.tnl_group_destroy.restype = ctypes.c_int
+        lib.tnl_group_workspace_size.argtypes = [P, i64, ctypes.POINTER(ctypes.c_size_t)]
+        lib.tnl_group_workspace_size.restype = ctypes.c_int
+        lib.tnl_group_forward_ex.argtypes = [P, P, i64, i64, ctypes.POINTER(P), ctypes.POINTER(i64), P, ctypes.c_size_t,
+                                             P, P]
+        lib.tnl_group_forward_ex.restype = ctypes.c_int
         lib.tnl_jacobi_sweeps_parallel.argtypes = [P, P, i64, i64, i64, ctypes.c_double, ctypes.c_int32, P, P]
         lib.tnl_jacobi_sweeps_parallel.restype = ctypes.c_int
         lib.tnl_svd_finish.argtypes = [P, P, i64, i64, i64, P, P, P, P, P]

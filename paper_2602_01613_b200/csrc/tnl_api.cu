@@ -2186,6 +2186,132 @@ static tnl_status mlp_decode_gated(tnl_mlp* B, const void* x, int64_t m, int64_t
   return TNL_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Shared-input groups (tnl_stack.h): plans that read the same activations (a decoder's q, k, v)
+// ---------------------------------------------------------------------------
+struct tnl_group {
+  std::vector<tnl_plan*> p;
+  std::vector<int64_t> off;  // column of each plan's cut block in the stacked T
+  int64_t cols = 0, r_total = 0;
+  bool stacked = false;          // bf16 cut plans: one first-step GEMM over the stacked B_in panels
+  __nv_bfloat16* bstack = nullptr;  // [B_in(p0); B_in(p1); ...] (r_total x cols)
+};
+
+static size_t group_ws_bytes(const tnl_group* G, int64_t m, size_t* o_t32, size_t* o_t) {
+  size_t per = 0, a, b, c;
+  for (const tnl_plan* P : G->p) per = std::max(per, ws_layout(P, std::max<int64_t>(m, 1), &a, &b, &c));
+  size_t bytes = per;
+  *o_t32 = bytes;
+  bytes += round_up((int64_t)sizeof(float) * m * G->r_total, 256);
+  *o_t = bytes;
+  bytes += round_up((int64_t)2 * m * G->r_total, 256);
+  return bytes;
+}
+
+tnl_status tnl_group_create(const tnl_plan* const* plans, int32_t n, tnl_group** out) {
+  if (!plans || n < 1 || !out) return fail(TNL_ERR_ARG, "null argument");
+  *out = nullptr;
+  std::unique_ptr<tnl_group> G(new tnl_group);
+  G->cols = plans[0]->cols;
+  bool stack = true;
+  for (int i = 0; i < n; ++i) {
+    const tnl_plan* P = plans[i];
+    if (!P) return fail(TNL_ERR_ARG, "null plan %d", i);
+    if (P->cols != G->cols)
+      return fail(TNL_ERR_SHAPE, "group plans must share the input width: %lld vs %lld", (long long)P->cols,
+                  (long long)G->cols);
+    stack = stack && P->compute_dtype == TNL_BF16 && P->plan_large == TNL_PLAN_CUT && P->bin &&
+            P->family != TNL_FAMILY_DENSE && !P->tucker_chain;
+    G->p.push_back(const_cast<tnl_plan*>(P));
+    G->off.push_back(G->r_total);
+    G->r_total += P->r_pad;
+  }
+  G->stacked = stack && n > 1;
+  if (G->stacked) {
+    CUDA_TRY(dev_alloc(&G->bstack, 2 * G->r_total * G->cols));
+    for (int i = 0; i < n; ++i)
+      CUDA_TRY(cudaMemcpy(G->bstack + G->off[i] * G->cols, G->p[i]->bin, 2 * G->p[i]->r_pad * G->cols,
+                          cudaMemcpyDeviceToDevice));
+  }
+  *out = G.release();
+  return TNL_OK;
+}
+
+tnl_status tnl_group_destroy(tnl_group* G) {
+  if (!G) return TNL_OK;
+  cudaDeviceSynchronize();
+  dev_free(G->bstack);
+  delete G;
+  return TNL_OK;
+}
+
+tnl_status tnl_group_workspace_size(const tnl_group* G, int64_t m, size_t* bytes) {
+  if (!G || !bytes) return fail(TNL_ERR_ARG, "null argument");
+  size_t a, b;
+  *bytes = group_ws_bytes(G, m, &a, &b);
+  return TNL_OK;
+}
+
+tnl_status tnl_group_forward_ex(const tnl_group* Gc, const void* x, int64_t m, int64_t ldx, void* const* ys,
+                                const int64_t* ldys, void* ws, size_t ws_bytes, const tnl_fwd_opts* o, void* stream) {
+  tnl_group* G = const_cast<tnl_group*>(Gc);
+  if (!G || !x || !ys || !ldys) return fail(TNL_ERR_ARG, "null argument");
+  const int n = (int)G->p.size();
+  size_t o_t32, o_t;
+  const size_t need = group_ws_bytes(G, m, &o_t32, &o_t);
+  if (ws_bytes < need) return fail(TNL_ERR_ARG, "group workspace %zu < required %zu bytes", ws_bytes, need);
+  if (m == 0) return TNL_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool aligned = !(reinterpret_cast<uintptr_t>(x) & 15) && ldx % 8 == 0;
+  bool ys_ok = true;
+  for (int i = 0; i < n; ++i) ys_ok = ys_ok && ys[i] && !(reinterpret_cast<uintptr_t>(ys[i]) & 15) && ldys[i] % 8 == 0;
+  if (!G->stacked || m <= kSwapMaxM || !aligned || !ys_ok || (o && o->accumulate)) {
+    for (int i = 0; i < n; ++i) {  // per-plan forwards (decode, or plans that do not stack)
+      tnl_status s = (o && (o->accumulate || o->ss_in))
+                         ? tnl_forward_ex(G->p[i], x, m, ldx, ys[i], ldys[i], ws, o_t32, o, stream)
+                         : tnl_forward(G->p[i], x, m, ldx, ys[i], ldys[i], ws, o_t32, stream);
+      if (s) return s;
+    }
+    return TNL_OK;
+  }
+  // one first step over x (read once) into the stacked cut activations T (M x r_total)
+  char* w = static_cast<char*>(ws);
+  float* t32 = reinterpret_cast<float*>(w + o_t32);
+  __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(w + o_t);
+  tnl_plan* P0 = G->p[0];
+  tnl_fwd_opts in_o = {};
+  if (o && o->ss_in) {
+    if (o->rms_n <= 0) return fail(TNL_ERR_ARG, "rms_n must be > 0");
+    in_o.ss_in = o->ss_in;
+    in_o.rms_n = o->rms_n;
+    in_o.rms_eps = o->rms_eps;
+  }
+  const tnl_fwd_opts* ino = (o && o->ss_in) ? &in_o : nullptr;
+  const int64_t tiles1 = ((m + 127) / 128) * ((G->r_total + 255) / 256);
+  const int64_t kb = (G->cols + 63) / 64;
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb / 8));
+  tnl_status s;
+  if (splits > 1) {
+    if ((s = tc_step_p(P0, x, ldx, G->bstack, G->cols, m, G->r_total, G->cols, t32, G->r_total, true, splits, st)))
+      return s;
+    if (ino)
+      to_bf16_scaled(t32, t, m, G->r_total, ino, st);
+    else
+      to_bf16(t32, t, m * G->r_total, st);
+  } else if ((s = tc_step_p(P0, x, ldx, G->bstack, G->cols, m, G->r_total, G->cols, t, G->r_total, false, 1, st, 0,
+                            ino))) {
+    return s;
+  }
+  // each plan's output step on its block of T
+  for (int i = 0; i < n; ++i) {
+    tnl_plan* P = G->p[i];
+    if ((s = tc_step_p(P, t + G->off[i], G->r_total, P->aout, P->r_pad, m, P->row_end - P->row_begin, P->r_pad, ys[i],
+                       ldys[i], false, 1, st)))
+      return s;
+  }
+  return TNL_OK;
+}
+
 tnl_status tnl_mlp_create(const tnl_plan* gate, const tnl_plan* up, const tnl_plan* down, int32_t flags,
                           tnl_mlp** out) {
   if (!gate || !up || !down || !out) return fail(TNL_ERR_ARG, "null argument");

@@ -31,6 +31,7 @@ import torch
 from . import _native as N
 from . import synthetic as S
 from .mlp import TNMLP
+from .stack import TNGroup
 from .modes import default_mode_shape
 
 HIDDEN, QDIM, KVDIM, FFN = 5120, 8192, 1024, 25600
@@ -87,6 +88,8 @@ class QwenTNStack:
             t1 = time.perf_counter()
             blk["mlp"] = TNMLP(blk["gate"][1], blk["up"][1], blk["down"][1], dtype=dtype, device=self.device,
                                fused=fused_mlp)
+            # prefill: k, v and q read the same normalised hidden state -> one stacked first step
+            blk["kvq"] = TNGroup([blk["k"][1], blk["v"][1], blk["q"][1]], dtype=dtype, device=self.device)
             self.build_s["device_plans"] += time.perf_counter() - t1
             # decode: q -> (pass-through attention) -> o as one two-layer stack (one fused
             # boundary kernel: q's output rows never leave the SM)
@@ -95,6 +98,7 @@ class QwenTNStack:
         self.fuse_qo = True
         # prefill: residual adds and RMSNorms folded into the projections' epilogues (tnl_fwd_opts)
         self.fold_prefill = True
+        self.group_kvq = True
         self._ws = None
         self._ws_side = None
         self._side = None
@@ -117,7 +121,8 @@ class QwenTNStack:
 
     def workspace(self, m: int):
         need = max(max(p.workspace_bytes(m) for _, _, p in self.projections()),
-                   max(blk["mlp"].workspace_bytes(m) for blk in self.layers))
+                   max(blk["mlp"].workspace_bytes(m) for blk in self.layers),
+                   max(blk["kvq"].workspace_bytes(m) for blk in self.layers))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws
@@ -134,7 +139,8 @@ class QwenTNStack:
         """Private workspaces (zero-filled: decode accumulators) and k/v side streams for one
         concurrently running token group (decode microbatches)."""
         need = max(max(p.workspace_bytes(m) for _, _, p in self.projections()),
-                   max(blk["mlp"].workspace_bytes(m) for blk in self.layers))
+                   max(blk["mlp"].workspace_bytes(m) for blk in self.layers),
+                   max(blk["kvq"].workspace_bytes(m) for blk in self.layers))
         need_side = max(max(blk[n][2].workspace_bytes(m) for n in ("k", "v")) for blk in self.layers)
         z = lambda n: torch.zeros(max(n, 256), dtype=torch.uint8, device=self.device)  # noqa: E731
         return {"ws": z(need), "ws_side": [z(need_side), z(need_side)],
@@ -171,10 +177,13 @@ class QwenTNStack:
         o_both = N.FwdOpts(1, ss.data_ptr(), HIDDEN, eps)
         for blk in self.layers:
             N.check(lib.tnl_rms_stats(vp(x), x.stride(0), m, HIDDEN, vp(ss), st))
-            for name in ("k", "v", "q"):
-                pl = blk[name][2]
-                N.check(lib.tnl_forward_ex(pl.handle, vp(x), m, x.stride(0), vp(b[name]), b[name].stride(0),
-                                           vp(ws), ws.numel(), ctypes.byref(o_norm), st))
+            if self.group_kvq:  # one first step over x for k, v and q (x read once)
+                blk["kvq"].forward(x, outs=[b["k"], b["v"], b["q"]], ws=ws, opts=o_norm)
+            else:
+                for name in ("k", "v", "q"):
+                    pl = blk[name][2]
+                    N.check(lib.tnl_forward_ex(pl.handle, vp(x), m, x.stride(0), vp(b[name]), b[name].stride(0),
+                                               vp(ws), ws.numel(), ctypes.byref(o_norm), st))
             pl = blk["o"][2]  # attention core: pass-through; x += o
             N.check(lib.tnl_forward_ex(pl.handle, vp(b["q"]), m, b["q"].stride(0), vp(x), x.stride(0), vp(ws),
                                        ws.numel(), ctypes.byref(o_acc), st))

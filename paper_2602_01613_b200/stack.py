@@ -161,3 +161,68 @@ class TNStack:
 
     def replay(self):
         self.graph.replay()
+
+
+class TNGroup:
+    """Plans that read the same input — a decoder's q, k and v of one normalised hidden state
+    (``tnl_group_*`` in include/tnl_stack.h). Prefill runs ONE first-step GEMM over the stacked
+    B_in panels (x read once, the folded RMSNorm applied there), then each layer's output step;
+    decode-sized M runs the layers one after another."""
+
+    def __init__(self, layers: list[CompressedLayer], dtype=torch.bfloat16, device=None):
+        if not layers:
+            raise ShapeError("empty group")
+        self.lib = N.load()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dtype = dtype
+        self.plans = [l.plan(dtype, self.device) for l in layers]
+        self.cols = self.plans[0].info["cols"]
+        arr = (ctypes.c_void_p * len(self.plans))(*[p.handle.value for p in self.plans])
+        h = ctypes.c_void_p()
+        N.check(self.lib.tnl_group_create(arr, len(self.plans), ctypes.byref(h)))
+        self.handle = h
+        self._ws = None
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.lib.tnl_group_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace_bytes(self, m: int) -> int:
+        n = ctypes.c_size_t()
+        N.check(self.lib.tnl_group_workspace_size(self.handle, int(m), ctypes.byref(n)))
+        return int(n.value)
+
+    def workspace(self, m: int):
+        n = self.workspace_bytes(m)
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = torch.zeros(max(n, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def forward(self, x: torch.Tensor, outs=None, ws=None, opts=None):
+        """ys[i] = layers[i](x); opts: an ``N.FwdOpts`` (folded RMSNorm of x via ss_in)."""
+        m = x.shape[0]
+        if x.dim() != 2 or x.shape[1] != self.cols or x.dtype != self.dtype or not x.is_cuda:
+            raise ShapeError(f"x {tuple(x.shape)} {x.dtype} does not match the group's {self.cols} {self.dtype} inputs")
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        if outs is None:
+            outs = [torch.empty((m, p.rows_local), dtype=self.dtype, device=x.device) for p in self.plans]
+        for o, p in zip(outs, self.plans):
+            check_out(o, m, p.rows_local, self.dtype, x.device)
+        ws = ws if ws is not None and ws.numel() >= self.workspace_bytes(m) else self.workspace(m)
+        ys = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        lds = (ctypes.c_int64 * len(outs))(*[o.stride(0) if m > 1 else o.shape[1] for o in outs])
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        N.check(self.lib.tnl_group_forward_ex(self.handle, ctypes.c_void_p(x.data_ptr()), m,
+                                              x.stride(0) if m > 1 else self.cols, ys, lds,
+                                              ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                              ctypes.byref(opts) if opts is not None else None,
+                                              ctypes.c_void_p(stream)))
+        return outs

@@ -338,3 +338,40 @@ def test_tucker2_fused_chain(shape, m):
     assert rel(ref, got) <= BF16_TOL
     cut = fwd(layer, x, torch.bfloat16, tnl.PLAN_CUT)
     assert rel(cut, got) <= BF16_TOL
+
+
+# --- shared-input group (tnl_group_*: k, v, q of one hidden state) ------------------------------
+
+
+@pytest.mark.parametrize("m", [16, 300, 8192])
+def test_group_matches_separate_forwards(m):
+    """One stacked first step over x for k, v, q (prefill) == each layer's own forward, with and
+    without the folded RMSNorm row scale; decode-sized M runs the layers one by one."""
+    import ctypes
+
+    from paper_2602_01613_b200 import _native as N
+    from paper_2602_01613_b200.stack import TNGroup
+
+    lays = [Q._tn("tucker2-128", Q.KVDIM, Q.HIDDEN, seed=68_001), Q._tn("tucker2-128", Q.KVDIM, Q.HIDDEN, seed=68_002),
+            Q._tn("tucker2-256", Q.QDIM, Q.HIDDEN, seed=68_003)]
+    g = TNGroup(lays)
+    x = torch.randn(m, Q.HIDDEN, device=DEV).to(torch.bfloat16)
+    ys = g.forward(x)
+    for lay, y in zip(lays, ys):
+        ref = lay.plan(torch.bfloat16).forward(x)
+        torch.cuda.synchronize()
+        assert rel(ref.double().cpu().numpy(), y.double().cpu().numpy()) <= 1e-2
+        assert rel(O.forward_torch_orient(oracle_of(lay, True), x.double().cpu().numpy()),
+                   y.double().cpu().numpy()) <= BF16_TOL
+    if m > 64:  # folded RMSNorm: y_i = layer_i(x / rms(x))
+        lib = N.load()
+        ss = torch.zeros(m, dtype=torch.float32, device=DEV)
+        st = torch.cuda.current_stream().cuda_stream
+        N.check(lib.tnl_rms_stats(ctypes.c_void_p(x.data_ptr()), Q.HIDDEN, m, Q.HIDDEN, ctypes.c_void_p(ss.data_ptr()),
+                                  ctypes.c_void_p(st)))
+        opts = N.FwdOpts(0, ss.data_ptr(), Q.HIDDEN, 1e-6)
+        ys = g.forward(x, opts=opts)
+        xn = (x.float() * torch.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-6)).double().cpu().numpy()
+        torch.cuda.synchronize()
+        for lay, y in zip(lays, ys):
+            assert rel(O.forward_torch_orient(oracle_of(lay, True), xn), y.double().cpu().numpy()) <= BF16_TOL
