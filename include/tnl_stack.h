@@ -34,6 +34,11 @@ typedef struct {
   const float* ss_in;
   int32_t rms_n;
   float rms_eps;
+  /* rms_fused != 0 (tnl_group_forward_ex / tnl_mlp_forward_ex only): normalise by the RMS of x
+   * without ss_in — the first step, which streams every full row of x through shared memory,
+   * sums the squares itself (no separate statistics pass over x). TNL_ERR_UNSUPPORTED when that
+   * step would split K; the caller then uses tnl_rms_stats + ss_in. */
+  int32_t rms_fused;
 } tnl_fwd_opts;
 
 /* ss[i] = sum_j x[i][j]^2 for a bf16 [m][n] matrix (row pitch ldx % 8 == 0, n % 8 == 0). */

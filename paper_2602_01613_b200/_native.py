@@ -72,6 +72,7 @@ class FwdOpts(ctypes.Structure):
         ("ss_in", ctypes.c_void_p),
         ("rms_n", ctypes.c_int32),
         ("rms_eps", ctypes.c_float),
+        ("rms_fused", ctypes.c_int32),
     ]
 
 

@@ -28,7 +28,30 @@ struct TcGemmArgs {
   const float* ss_in = nullptr;  // D row i scaled by rsqrt(ss_in[i] / rms_n + rms_eps) (folded RMSNorm)
   int32_t rms_n = 0;
   float rms_eps = 0.f;
+  // ss_fused (with ss_in set to any non-null marker): the kernel computes sum_k A[i][k]^2 itself
+  // from the A tiles streaming through shared memory (full K per tile, no split-K) — the epilogue
+  // warps read each stage's own row before releasing it — instead of reading ss_in
+  int32_t ss_fused = 0;
 };
+
+// sum of squares of row `lrow` of a 128 x 64 bf16 SW128 tile in shared memory
+__device__ __forceinline__ float tile_row_sumsq(uint32_t tile_saddr, int lrow) {
+  const uint32_t rowp = tile_saddr + (lrow >> 3) * 1024 + (lrow & 7) * 128;
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(rowp + ((c ^ (lrow & 7)) << 4)));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float lo = __uint_as_float(w[t] << 16), hi = __uint_as_float(w[t] & 0xffff0000u);
+      s = fmaf(lo, lo, fmaf(hi, hi, s));
+    }
+  }
+  return s;
+}
 
 // Epilogue helper shared by the persistent and pair kernels (bf16 output mode): the folded-RMSNorm
 // scale of output row `row`.

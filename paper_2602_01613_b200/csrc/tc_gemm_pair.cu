@@ -56,7 +56,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2] leader: 4 epilogue warps x 2 CTAs
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* afull = tempty + 2;      // [STAGES] ss_fused: stage consumed by the MMAs (multicast commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + STAGES);
 
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -72,7 +73,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     if (args.out_mode == TC_OUT_BF16) tma_prefetch_desc(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], SCALE && args.ss_fused ? 5 : 1);  // + 4 epilogue warps reading the A rows
+      mbar_init(&afull[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -134,6 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           for (int k = 0; k < PBK / 16; ++k)
             mma_bf16_ss_pair(d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           mma_commit_pair(&empty[s], 3);
+          if (SCALE && args.ss_fused) mma_commit_pair(&afull[s], 3);
         }
         mma_commit_pair(&tfull[acc], 3);
       }
@@ -142,18 +145,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   } else {
     const uint32_t q = warp & 3;
     const int et = threadIdx.x - 64;
-    int lt = 0, chunk_ct = 0;
+    int lt = 0, chunk_ct = 0, it_e = 0;
     for (int t = cluster; t < num_tiles; t += nclusters, ++lt) {
       int tm, tn, sp;
       decode_tile(t, tm, tn, sp);
       const int acc = lt & 1;
+      float fused_ss = 0.f;
+      if (SCALE && args.ss_fused) {  // this CTA's 128 A rows of every k-block: sum this row's squares
+        const int kb0 = sp * kb_per, kb1 = min(total_kb, kb0 + kb_per);
+        const int lr = (warp & 3) * 32 + lane_id();
+        for (int kb = kb0; kb < kb1; ++kb, ++it_e) {
+          const int s = it_e % STAGES;
+          // only the leader sees the full barriers: wait for the MMA commit of this stage, multicast to
+          // both CTAs (the A rows are in our smem; the slot is not refilled before our empty arrival)
+          mbar_wait(&afull[s], (it_e / STAGES) & 1);
+          fused_ss += tile_row_sumsq(smem_u32(sA + s * P_A_STAGE), lr);
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&empty[s]);
+        }
+      }
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t d = tmem + acc * BN + ((q * 32) << 16);
       const int lrow = q * 32 + lane_id();
       const int row = tm * PBM + lrow;
       if (args.out_mode == TC_OUT_BF16) {
-        const float rscale = SCALE ? row_rms_scale(args, row) : 1.f;
+        const float rscale = !SCALE ? 1.f
+                             : args.ss_fused ? rsqrtf(fused_ss / (float)args.rms_n + args.rms_eps)
+                                             : row_rms_scale(args, row);
         for (int c0 = 0; c0 < BN; c0 += 64) {
           // Dead chunk (ragged N, or a CTA whose half tile lies past M): skip it entirely so the
           // staging ring advances only on committed stores (wait_read_le<P_NC-1> guards reuse).
@@ -280,9 +299,9 @@ int launch_tc_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtens
                         int bn, int splits, cudaStream_t st) {
   switch (bn) {
     case 128:
-      return args.ss_in ? launch_pair<128, 6, true>(a, b, c, args, splits, st) : launch_pair<128, 6, false>(a, b, c, args, splits, st);
+      return (args.ss_in || args.ss_fused) ? launch_pair<128, 6, true>(a, b, c, args, splits, st) : launch_pair<128, 6, false>(a, b, c, args, splits, st);
     case 256:
-      return args.ss_in ? launch_pair<256, 5, true>(a, b, c, args, splits, st) : launch_pair<256, 5, false>(a, b, c, args, splits, st);
+      return (args.ss_in || args.ss_fused) ? launch_pair<256, 5, true>(a, b, c, args, splits, st) : launch_pair<256, 5, false>(a, b, c, args, splits, st);
     default:
       return (int)cudaErrorInvalidValue;
   }

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(192, 1)
     if (args.out_mode == TC_OUT_BF16) tma_prefetch_desc(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], SCALE && args.ss_fused ? 5 : 1);  // + 4 epilogue warps reading the A rows
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -136,18 +136,32 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     const uint32_t q = warp & 3;
     const int et = threadIdx.x - 64;
-    int lt = 0, chunk_ct = 0;
+    int lt = 0, chunk_ct = 0, it_e = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       int tm, tn, sp;
       decode_tile(t, tm, tn, sp);
       const int acc = lt & 1;
+      float fused_ss = 0.f;
+      if (SCALE && args.ss_fused) {  // the tile's full K streams through the ring: sum this row's squares
+        const int kb0 = sp * kb_per, kb1 = min(total_kb, kb0 + kb_per);
+        const int lr = (warp & 3) * 32 + lane_id();
+        for (int kb = kb0; kb < kb1; ++kb, ++it_e) {
+          const int s = it_e % STAGES;
+          mbar_wait(&full[s], (it_e / STAGES) & 1);
+          fused_ss += tile_row_sumsq(smem_u32(sA + s * A_STAGE), lr);
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&empty[s]);
+        }
+      }
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t d = tmem + acc * ACC_COLS + ((q * 32) << 16);
       const int lrow = q * 32 + lane_id();
       const int row = tm * BM + lrow;
       if (args.out_mode == TC_OUT_BF16) {
-        const float rscale = SCALE ? row_rms_scale(args, row) : 1.f;
+        const float rscale = !SCALE ? 1.f
+                             : args.ss_fused ? rsqrtf(fused_ss / (float)args.rms_n + args.rms_eps)
+                                             : row_rms_scale(args, row);
         for (int c0 = 0; c0 < BN; c0 += 64) {
           // Dead chunk (ragged N): no TMEM read, no smem write, no store; the staging ring only
           // advances on committed stores so wait_read_le1 always guards the buffer being reused.
@@ -275,11 +289,11 @@ int launch_tc_gemm_persistent(const CUtensorMap& a, const CUtensorMap& b, const 
                               cudaStream_t st) {
   switch (bn) {
     case 64:
-      return args.ss_in ? launch_p<64, 8, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<64, 8, false>(a, b, c, args, splits, max_ctas, pdl, st);
+      return (args.ss_in || args.ss_fused) ? launch_p<64, 8, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<64, 8, false>(a, b, c, args, splits, max_ctas, pdl, st);
     case 128:
-      return args.ss_in ? launch_p<128, 5, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<128, 5, false>(a, b, c, args, splits, max_ctas, pdl, st);
+      return (args.ss_in || args.ss_fused) ? launch_p<128, 5, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<128, 5, false>(a, b, c, args, splits, max_ctas, pdl, st);
     case 256:
-      return args.ss_in ? launch_p<256, 3, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<256, 3, false>(a, b, c, args, splits, max_ctas, pdl, st);
+      return (args.ss_in || args.ss_fused) ? launch_p<256, 3, true>(a, b, c, args, splits, max_ctas, pdl, st) : launch_p<256, 3, false>(a, b, c, args, splits, max_ctas, pdl, st);
     default:
       return (int)cudaErrorInvalidValue;
   }

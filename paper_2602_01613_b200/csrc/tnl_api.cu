@@ -212,31 +212,39 @@ static void to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_
   }
 }
 // ss[row] = sum_j x[row][j]^2 (one CTA per row; the folded RMSNorm's statistics)
+// one warp per row, 8 rows per CTA: every lane keeps its row's 16-byte loads in flight at once
+// (a CTA per row left ~2 loads per thread and the SMs mostly waiting on block launches)
 __global__ void __launch_bounds__(256) row_sumsq_bf16(const __nv_bfloat16* __restrict__ x, int64_t ldx, int64_t n,
-                                                      float* __restrict__ ss) {
+                                                      int64_t m, float* __restrict__ ss) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const uint4* r = reinterpret_cast<const uint4*>(x + (int64_t)blockIdx.x * ldx);
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= m) return;
+  const int lane = threadIdx.x & 31;
+  const uint4* r = reinterpret_cast<const uint4*>(x + row * ldx);
+  const int64_t nv = n / 8;
   float s = 0.f;
-  for (int64_t c = threadIdx.x; c < n / 8; c += 256) {
-    const uint4 w = r[c];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+  constexpr int U = 8;
+  for (int64_t c0 = 0; c0 < nv; c0 += 32 * U) {
+    uint4 w[U];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const float2 f = __bfloat1622float2(h[t]);
-      s = fmaf(f.x, f.x, fmaf(f.y, f.y, s));
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = c0 + u * 32 + lane;
+      w[u] = c < nv ? r[c] : make_uint4(0u, 0u, 0u, 0u);  // default caching: the next GEMM re-reads x from L2
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[u]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = __bfloat1622float2(h[t]);
+        s = fmaf(f.x, f.x, fmaf(f.y, f.y, s));
+      }
     }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  __shared__ float red[8];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < 8; ++w) t += red[w];
-    ss[blockIdx.x] = t;
-  }
+  if (lane == 0) ss[row] = s;
 }
 // unfused MLP fallback: g <- silu(g) * u (bf16, 8 elements per thread)
 __global__ void silu_mul_bf16(__nv_bfloat16* g, const __nv_bfloat16* u, int64_t n8) {
@@ -1581,8 +1589,9 @@ static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void*
     a.out_mode = TC_OUT_BF16;
     if ((err = get_tmap2(P, &tc, out, false, N, M, ldo, 64, 128, 128)))
       return fail(TNL_ERR_CUDA, "tensor map (output) failed: %d", err);
-    if (in_o && in_o->ss_in) {  // folded RMSNorm of X: scale the output rows
+    if (in_o && (in_o->ss_in || in_o->rms_fused)) {  // folded RMSNorm of X: scale the output rows
       a.ss_in = in_o->ss_in;
+      a.ss_fused = (in_o->rms_fused && splits == 1) ? 1 : 0;  // statistics from the streamed A tiles
       a.rms_n = in_o->rms_n;
       a.rms_eps = in_o->rms_eps;
     }
@@ -1866,7 +1875,10 @@ static tnl_status mlp_tgu(tnl_mlp* B, const void* x, int64_t m, int64_t ldx, flo
   const int64_t kb = (B->hidden + 63) / 64;
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb / 8));
   tnl_status s;
-  if (rgu <= 128 && ((m + 127) / 128) * ((rgu + 63) / 64) >= 96) {
+  const bool one_pass = rgu <= 128 && ((m + 127) / 128) * ((rgu + 63) / 64) >= 96;
+  if (in_o && in_o->rms_fused && !one_pass && splits > 1)
+    return fail(TNL_ERR_UNSUPPORTED, "rms_fused: the gate/up input step splits K at M = %lld", (long long)m);
+  if (one_pass) {
     // enough 64-wide output tiles to fill the SMs: no split-K, bf16 straight from the epilogue
     return tc_step_p(B->g, x, ldx, B->bgu, B->hidden, m, rgu, B->hidden, tgu, rgu, false, 1, st, 64, in_o);
   }
@@ -2266,6 +2278,7 @@ tnl_status tnl_group_forward_ex(const tnl_group* Gc, const void* x, int64_t m, i
   bool ys_ok = true;
   for (int i = 0; i < n; ++i) ys_ok = ys_ok && ys[i] && !(reinterpret_cast<uintptr_t>(ys[i]) & 15) && ldys[i] % 8 == 0;
   if (!G->stacked || m <= kSwapMaxM || !aligned || !ys_ok || (o && o->accumulate)) {
+    if (o && o->rms_fused) return fail(TNL_ERR_UNSUPPORTED, "rms_fused: needs the stacked prefill path");
     for (int i = 0; i < n; ++i) {  // per-plan forwards (decode, or plans that do not stack)
       tnl_status s = (o && (o->accumulate || o->ss_in))
                          ? tnl_forward_ex(G->p[i], x, m, ldx, ys[i], ldys[i], ws, o_t32, o, stream)
@@ -2286,10 +2299,18 @@ tnl_status tnl_group_forward_ex(const tnl_group* Gc, const void* x, int64_t m, i
     in_o.rms_n = o->rms_n;
     in_o.rms_eps = o->rms_eps;
   }
-  const tnl_fwd_opts* ino = (o && o->ss_in) ? &in_o : nullptr;
+  if (o && o->rms_fused) {
+    if (o->rms_n <= 0) return fail(TNL_ERR_ARG, "rms_n must be > 0");
+    in_o.rms_fused = 1;
+    in_o.rms_n = o->rms_n;
+    in_o.rms_eps = o->rms_eps;
+  }
+  const tnl_fwd_opts* ino = (o && (o->ss_in || o->rms_fused)) ? &in_o : nullptr;
   const int64_t tiles1 = ((m + 127) / 128) * ((G->r_total + 255) / 256);
   const int64_t kb = (G->cols + 63) / 64;
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(tiles1, 1), kb / 8));
+  if (o && o->rms_fused && splits > 1)
+    return fail(TNL_ERR_UNSUPPORTED, "rms_fused: the stacked first step splits K at M = %lld", (long long)m);
   tnl_status s;
   if (splits > 1) {
     if ((s = tc_step_p(P0, x, ldx, G->bstack, G->cols, m, G->r_total, G->cols, t32, G->r_total, true, splits, st)))
@@ -2424,14 +2445,18 @@ static tnl_status mlp_forward_impl(const tnl_mlp* Bc, const void* x, int64_t m, 
   if (!B || !x || !y) return fail(TNL_ERR_ARG, "null argument");
   // folded RMSNorm of the block input (ss_in) and accumulation into its output
   tnl_fwd_opts in_o = {}, out_o = {};
-  const bool fold = o && (o->accumulate || o->ss_in);
+  const bool fold = o && (o->accumulate || o->ss_in || o->rms_fused);
   if (fold) {
     in_o.ss_in = o->ss_in;
+    in_o.rms_fused = o->rms_fused;
     in_o.rms_n = o->rms_n;
     in_o.rms_eps = o->rms_eps;
     out_o.accumulate = o->accumulate;
     if (m <= kSwapMaxM) return fail(TNL_ERR_UNSUPPORTED, "folded residual / RMSNorm: prefill (M > %lld) only", (long long)kSwapMaxM);
-    if (o->ss_in && o->rms_n <= 0) return fail(TNL_ERR_ARG, "rms_n must be > 0");
+    if ((o->ss_in || o->rms_fused) && o->rms_n <= 0) return fail(TNL_ERR_ARG, "rms_n must be > 0");
+    // the in-GEMM statistics need the stacked gate/up input step (fused and dual blocks)
+    if (o->rms_fused && !(B->fused || B->dual))
+      return fail(TNL_ERR_UNSUPPORTED, "rms_fused: needs a fused or dual MLP block");
   }
   if (m == 0) return TNL_OK;
   size_t off[4], need;
@@ -2614,8 +2639,8 @@ tnl_status tnl_rms_stats(const void* x, int64_t ldx, int64_t m, int64_t n, float
     return fail(TNL_ERR_SHAPE, "rms_stats: m=%lld n=%lld ldx=%lld (n, ldx %% 8 == 0, 16-byte aligned x)", (long long)m,
                 (long long)n, (long long)ldx);
   if (m == 0) return TNL_OK;
-  if (launch_pdl(row_sumsq_bf16, dim3((unsigned)m), dim3(256), 0, static_cast<cudaStream_t>(stream),
-                 static_cast<const __nv_bfloat16*>(x), ldx, n, ss))
+  if (launch_pdl(row_sumsq_bf16, dim3((unsigned)((m + 7) / 8)), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                 static_cast<const __nv_bfloat16*>(x), ldx, n, m, ss))
     return fail(TNL_ERR_CUDA, "rms_stats launch failed");
   return TNL_OK;
 }
@@ -2754,6 +2779,8 @@ tnl_status tnl_forward(const tnl_plan* plan, const void* x, int64_t m, int64_t l
 
 tnl_status tnl_forward_ex(const tnl_plan* plan, const void* x, int64_t m, int64_t ldx, void* y, int64_t ldy,
                           void* workspace, size_t workspace_bytes, const tnl_fwd_opts* opts, void* stream) {
+  if (opts && opts->rms_fused)
+    return fail(TNL_ERR_UNSUPPORTED, "rms_fused: use tnl_group_forward_ex / tnl_mlp_forward_ex (stacked input steps)");
   if (!opts || (!opts->accumulate && !opts->ss_in))
     return tnl_forward(plan, x, m, ldx, y, ldy, workspace, workspace_bytes, stream);
   tnl_plan* P = const_cast<tnl_plan*>(plan);

@@ -29,6 +29,7 @@ import time
 import torch
 
 from . import _native as N
+from .errors import UnsupportedError
 from . import synthetic as S
 from .mlp import TNMLP
 from .stack import TNGroup
@@ -99,6 +100,7 @@ class QwenTNStack:
         # prefill: residual adds and RMSNorms folded into the projections' epilogues (tnl_fwd_opts)
         self.fold_prefill = True
         self.group_kvq = True
+        self.fuse_rms = True  # RMS statistics summed inside the stacked input steps
         self._ws = None
         self._ws_side = None
         self._side = None
@@ -175,11 +177,28 @@ class QwenTNStack:
         o_norm = N.FwdOpts(0, ss.data_ptr(), HIDDEN, eps)
         o_acc = N.FwdOpts(1, None, 0, 0.0)
         o_both = N.FwdOpts(1, ss.data_ptr(), HIDDEN, eps)
-        for blk in self.layers:
+        # rms_fused: the stacked k/v/q and gate/up input steps sum the squares of x themselves while
+        # streaming it (no statistics pass over x); on TNL_ERR_UNSUPPORTED (a K-split step) the
+        # statistics pass + ss_in is used instead
+        o_norm_f = N.FwdOpts(0, None, HIDDEN, eps, 1)
+        o_both_f = N.FwdOpts(1, None, HIDDEN, eps, 1)
+
+        def fused_or_stats(run_fused, run_stats):
+            if self.fuse_rms and self.group_kvq:
+                try:
+                    run_fused()
+                    return
+                except UnsupportedError:
+                    pass
             N.check(lib.tnl_rms_stats(vp(x), x.stride(0), m, HIDDEN, vp(ss), st))
+            run_stats()
+
+        for blk in self.layers:
             if self.group_kvq:  # one first step over x for k, v and q (x read once)
-                blk["kvq"].forward(x, outs=[b["k"], b["v"], b["q"]], ws=ws, opts=o_norm)
+                fused_or_stats(lambda: blk["kvq"].forward(x, outs=[b["k"], b["v"], b["q"]], ws=ws, opts=o_norm_f),
+                               lambda: blk["kvq"].forward(x, outs=[b["k"], b["v"], b["q"]], ws=ws, opts=o_norm))
             else:
+                N.check(lib.tnl_rms_stats(vp(x), x.stride(0), m, HIDDEN, vp(ss), st))
                 for name in ("k", "v", "q"):
                     pl = blk[name][2]
                     N.check(lib.tnl_forward_ex(pl.handle, vp(x), m, x.stride(0), vp(b[name]), b[name].stride(0),
@@ -187,9 +206,11 @@ class QwenTNStack:
             pl = blk["o"][2]  # attention core: pass-through; x += o
             N.check(lib.tnl_forward_ex(pl.handle, vp(b["q"]), m, b["q"].stride(0), vp(x), x.stride(0), vp(ws),
                                        ws.numel(), ctypes.byref(o_acc), st))
-            N.check(lib.tnl_rms_stats(vp(x), x.stride(0), m, HIDDEN, vp(ss), st))
-            N.check(lib.tnl_mlp_forward_ex(blk["mlp"].handle, vp(x), m, x.stride(0), vp(x), x.stride(0), vp(ws),
-                                           ws.numel(), ctypes.byref(o_both), st))  # x += mlp(norm(x))
+            fused_or_stats(  # x += mlp(norm(x))
+                lambda: N.check(lib.tnl_mlp_forward_ex(blk["mlp"].handle, vp(x), m, x.stride(0), vp(x), x.stride(0),
+                                                       vp(ws), ws.numel(), ctypes.byref(o_both_f), st)),
+                lambda: N.check(lib.tnl_mlp_forward_ex(blk["mlp"].handle, vp(x), m, x.stride(0), vp(x), x.stride(0),
+                                                       vp(ws), ws.numel(), ctypes.byref(o_both), st)))
         return x
 
     def forward(self, x: torch.Tensor, bufs=None, ctx=None) -> torch.Tensor:

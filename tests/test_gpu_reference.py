@@ -375,3 +375,57 @@ def test_group_matches_separate_forwards(m):
         torch.cuda.synchronize()
         for lay, y in zip(lays, ys):
             assert rel(O.forward_torch_orient(oracle_of(lay, True), xn), y.double().cpu().numpy()) <= BF16_TOL
+
+
+@pytest.mark.parametrize("m,n", [(1, 8), (7, 5120), (8192, 5120), (300, 25600), (13, 1032)])
+def test_rms_stats(m, n):
+    """tnl_rms_stats (warp per row) against float64 sums of squares of the same bf16 values."""
+    import ctypes
+
+    from paper_2602_01613_b200 import _native as N
+
+    x = torch.randn(m, n + 8, device=DEV).to(torch.bfloat16)[:, :n]  # padded row pitch
+    ss = torch.full((m,), -1.0, dtype=torch.float32, device=DEV)
+    N.check(N.load().tnl_rms_stats(ctypes.c_void_p(x.data_ptr()), n + 8, m, n, ctypes.c_void_p(ss.data_ptr()),
+                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    ref = (x.double() ** 2).sum(-1).cpu().numpy()
+    assert np.max(np.abs(ss.double().cpu().numpy() - ref) / ref) <= 1e-5
+
+
+@pytest.mark.parametrize("kind", ["tt64", "tr4", "tucker4", "tucker2-256"])
+def test_rms_fused_matches_stats_pass(kind):
+    """rms_fused (the stacked input steps sum the squares of x while streaming it) == the separate
+    statistics pass + ss_in, for the k/v/q group and every cfg4 MLP kind, at M = 8192."""
+    import ctypes
+
+    from paper_2602_01613_b200 import _native as N
+    from paper_2602_01613_b200.mlp import TNMLP
+    from paper_2602_01613_b200.stack import TNGroup
+
+    lib = N.load()
+    m = 8192
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    x = torch.randn(m, Q.HIDDEN, device=DEV).to(torch.bfloat16)
+    ss = torch.zeros(m, dtype=torch.float32, device=DEV)
+    N.check(lib.tnl_rms_stats(ctypes.c_void_p(x.data_ptr()), Q.HIDDEN, m, Q.HIDDEN, ctypes.c_void_p(ss.data_ptr()), st))
+    o_stats, o_fused = N.FwdOpts(0, ss.data_ptr(), Q.HIDDEN, 1e-6), N.FwdOpts(0, None, Q.HIDDEN, 1e-6, 1)
+    if kind == "tt64":  # the group once is enough
+        g = TNGroup([Q._tn("tucker2-128", Q.KVDIM, Q.HIDDEN, seed=69_001), Q._tn("tucker2-256", Q.QDIM, Q.HIDDEN, seed=69_002)])
+        a = g.forward(x, opts=o_stats)
+        b = g.forward(x, opts=o_fused)
+        torch.cuda.synchronize()
+        for ya, yb in zip(a, b):
+            assert rel(ya.double().cpu().numpy(), yb.double().cpu().numpy()) <= 5e-3
+    lays = [Q._tn(kind, r, c, seed=69_100 + i) for i, (r, c) in enumerate(((Q.FFN, Q.HIDDEN), (Q.FFN, Q.HIDDEN),
+                                                                             (Q.HIDDEN, Q.FFN)))]
+    blk = TNMLP(*lays)
+    ws = blk.workspace(m)
+    ya = torch.zeros(m, Q.HIDDEN, device=DEV, dtype=torch.bfloat16)
+    yb = torch.zeros(m, Q.HIDDEN, device=DEV, dtype=torch.bfloat16)
+    for y, o in ((ya, o_stats), (yb, o_fused)):
+        N.check(lib.tnl_mlp_forward_ex(blk.handle, ctypes.c_void_p(x.data_ptr()), m, Q.HIDDEN, ctypes.c_void_p(y.data_ptr()),
+                                       Q.HIDDEN, ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.byref(o), st))
+    torch.cuda.synchronize()
+    assert torch.isfinite(yb.float()).all()
+    assert rel(ya.double().cpu().numpy(), yb.double().cpu().numpy()) <= 5e-3
