@@ -9,8 +9,9 @@ import torch  # noqa: E402
 from paper_2602_01613_b200.qwen_stack import HIDDEN, QwenTNStack  # noqa: E402
 
 st = QwenTNStack(3, mlp_kinds=["tt64", "tr4", "tucker4"])
-x = torch.randn(8192, HIDDEN, device="cuda").to(torch.bfloat16)
-b = st._buffers(8192)
+M = int(os.environ.get("M", "8192"))
+x = torch.randn(M, HIDDEN, device="cuda").to(torch.bfloat16)
+b = st._buffers(M)
 for _ in range(2):
     st.forward(x.clone(), b)
 torch.cuda.synchronize()
