@@ -2670,17 +2670,14 @@ tnl_status tnl_jacobi_sweeps_parallel(double* work, double* rot, int64_t n, int6
   int dev = 0, sms = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // grid-barrier words (count, generation, last rotating sweep): one small buffer per device,
-  // allocated on first use; calls on one device are serialised by the caller's stream order
-  static unsigned int* sync_buf[64] = {nullptr};
-  static std::mutex mu;
-  {
-    std::lock_guard<std::mutex> g(mu);
-    if (dev < 64 && !sync_buf[dev]) CUDA_TRY(dev_alloc(&sync_buf[dev], 4 * sizeof(unsigned int)));
-  }
-  if (dev >= 64) return fail(TNL_ERR_UNSUPPORTED, "device index %d", dev);
-  const int err = tnl::launch_jacobi_parallel(work, rot, (int)n, (int)m, (int)nv, tol, max_sweeps, sweeps, sync_buf[dev],
-                                             sms, static_cast<cudaStream_t>(stream));
+  // grid-barrier words (count, generation, last rotating sweep): a stream-ordered allocation per
+  // call, so concurrent calls on different streams never share a barrier
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned int* sync_buf = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&sync_buf), 4 * sizeof(unsigned int), st));
+  const int err = tnl::launch_jacobi_parallel(work, rot, (int)n, (int)m, (int)nv, tol, max_sweeps, sweeps, sync_buf,
+                                             sms, st);
+  cudaFreeAsync(sync_buf, st);
   if (err) return fail(TNL_ERR_CUDA, "jacobi (parallel order) launch: %s", cudaGetErrorString((cudaError_t)err));
   return TNL_OK;
 }
