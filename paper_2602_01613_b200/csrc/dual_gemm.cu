@@ -19,6 +19,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tc_gemm.cuh"
@@ -233,6 +235,8 @@ int launch_dual_silu(const CUtensorMap& t, const CUtensorMap& g, const CUtensorM
     const long cost = waves * (per + 2);
     if (best < 0 || cost < best) best = cost, slices = s;
   }
+  static const int env_slices = getenv("TNL_DUAL_SLICES") ? atoi(getenv("TNL_DUAL_SLICES")) : 0;  // A/B switch
+  if (env_slices > 0) slices = env_slices < tiles_n ? env_slices : tiles_n;
   const int per = (tiles_n + slices - 1) / slices;
   slices = (tiles_n + per - 1) / per;
   cudaLaunchConfig_t cfg = {};

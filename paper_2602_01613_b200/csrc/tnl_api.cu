@@ -2576,13 +2576,15 @@ static tnl_status mlp_forward_impl(const tnl_mlp* Bc, const void* x, int64_t m, 
   if (pair) tiles_m = (tiles_m + 1) / 2 * 2;
   const int64_t nchunks = B->inter / 64;
   // Slice the intermediate so the grid's waves are nearly full: one CTA per SM (smem-bound),
-  // each CTA pays ~4 chunk-times of fixed cost (T tile load, pipeline fill, T_d flush).
+  // each CTA pays ~10 chunk-times of fixed cost (T tile load, pipeline fill, T_d flush) — fitted
+  // to the slice sweep at M = 8192 (profiles/r02/mlp_slices_sweep.jsonl: 1 wave of 2 slices
+  // 0.147 ms vs 0.161 ms with the earlier 4-chunk estimate, which picked 9 slices / 4 waves).
   int slices = 1;
   {
     int64_t best = INT64_MAX;
     for (int64_t s = 1; s <= nchunks; ++s) {
       const int64_t waves = (tiles_m * s + 147) / 148;
-      const int64_t cost = waves * ((nchunks + s - 1) / s + 4);
+      const int64_t cost = waves * ((nchunks + s - 1) / s + 10);
       if (cost < best) best = cost, slices = (int)s;
     }
     static const int env_slices = getenv("TNL_MLP_SLICES") ? atoi(getenv("TNL_MLP_SLICES")) : 0;  // A/B switch
