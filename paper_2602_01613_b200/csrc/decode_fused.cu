@@ -133,8 +133,10 @@ __global__ void __launch_bounds__(FT, 1)
           for (int h = 0; h < 2; ++h)
             tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull, tile * 128 + h * 64, t * 128, pol);
       TRACE(2);
-      pdl_wait();
-      TRACE(3);
+      if (!a.flag_wait) {
+        pdl_wait();
+        TRACE(3);
+      }
       if constexpr (LARGE) {  // B_in into the gate's A blocks once the gate MMAs have read them
         mbar_wait(gdone, 0);
         mbar_arrive_expect_tx(wfull2, 2 * nT * WBLK);
@@ -146,7 +148,12 @@ __global__ void __launch_bounds__(FT, 1)
     __syncwarp();
     // T_{l-1} was read only by the previous kernel, which has completed: zero this CTA's slice
     if (a.t_zero) {
-      pdl_wait();
+      if (a.flag_wait) {
+        if (lane_id() == 0) flag_wait_geq(a.flag_wait, a.flag_target);
+        __syncwarp();
+      } else {
+        pdl_wait();
+      }
       const int64_t n4 = a.zero_elems / 4, per = (n4 + gridDim.x - 1) / gridDim.x;
       float4* z = reinterpret_cast<float4*>(a.t_zero);
       const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(n4, e0 + per);
@@ -185,7 +192,15 @@ __global__ void __launch_bounds__(FT, 1)
     __syncwarp();
   } else {
     const int et = threadIdx.x - 64;
-    pdl_wait();
+    if (a.flag_wait) {
+      if (et == 0) {
+        flag_wait_geq(a.flag_wait, a.flag_target);
+        TRACE(3);
+      }
+      nbar(2, FEPI);
+    } else {
+      pdl_wait();
+    }
     if (et == 0) TRACE(11);
     // T_l: fp32 [64 kappa][BN tokens] -> bf16 MN-major SW128 [64 kappa][128 B] per k-block
     // (the accumulator's kappa-major layout is the MMA's MN-major B operand: no transpose).
@@ -205,7 +220,9 @@ __global__ void __launch_bounds__(FT, 1)
           const int e = et + u * FEPI;
           const int kap = kb * 64 + e / QPR, quad = e % QPR;
           v[kb][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#ifndef TNL_DIAG_NOTLOAD  // timing diagnostic only: skip the T_l read (wrong results)
           if (kb < kbB && e < ITEMS && kap < a.kB) v[kb][u] = ldg128_cg(a.t_in + (int64_t)kap * 64 + quad * 4);
+#endif
         }
       if (et == 0) TRACE(12);
 #pragma unroll
@@ -306,14 +323,20 @@ __global__ void __launch_bounds__(FT, 1)
         const int kap = e / SLOTS, sl = e % SLOTS;
         if (sl >= tok_slots) continue;
         const float4 v = lds128f(slot_addr(kap, sl));
+#ifdef TNL_DIAG_NORED  // timing diagnostic only: plain stores instead of reductions (wrong results)
+        *reinterpret_cast<float4*>(a.t_out + (int64_t)kap * 64 + sl * 4) = v;
+#else
         red_add_v4(a.t_out + (int64_t)kap * 64 + sl * 4, v.x, v.y, v.z, v.w);
+#endif
       }
     }
     if (et == 0) TRACE(9);
 
   }
   tc_fence_before();
+  if (a.flag_signal) __threadfence();  // this thread's reductions / zeroing stores, before the signal
   __syncthreads();
+  if (a.flag_signal && threadIdx.x == 0) red_release_add_u32(a.flag_signal, 1u);
   if (warp == 1) tmem_dealloc<256>(tmem);
   if (threadIdx.x == 32) TRACE(10);
 #undef TRACE

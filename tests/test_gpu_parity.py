@@ -381,6 +381,36 @@ def test_stack_fused_matches_oracle_chain(m):
     assert float(d) < 2e-2
 
 
+@pytest.mark.parametrize("mb", [1, 2])
+def test_stack_flag_handoff_replays(mb):
+    """21 boundaries of the cfg2 variants in one CUDA graph (flag handoff between the boundary
+    kernels, zero-at-rest accumulators and flags): 30 replays with a fresh input each, every one
+    against the per-layer C-ABI path. A premature read, a missed zeroing or a stale flag shows up
+    as a wrong replay."""
+    from paper_2602_01613_b200 import synthetic as S
+    from paper_2602_01613_b200.stack import TNStack
+
+    layers = []
+    for c in range(3):
+        for v, (_, fam, ms, rm, ranks) in enumerate(S.CFG2_VARIANTS):
+            L = O.synthetic_layer(fam, ms, rm, ranks, seed=49_000 + 10 * c + v)
+            layers.append(to_layer(L, round_bf16=True)[0])
+    st = TNStack(layers, torch.bfloat16)
+    st.capture(64, host_io=False, microbatches=mb)
+    plans = [l.plan(torch.bfloat16) for l in layers]
+    g = torch.Generator(device="cpu").manual_seed(49_999)
+    for it in range(30):
+        x = torch.randn(64, 5120, generator=g).to(torch.bfloat16).to(DEV)
+        st.x_dev.copy_(x)
+        st.replay()
+        torch.cuda.synchronize()
+        cur = x
+        for p in plans:
+            cur = p.forward(cur)
+        d = (cur.float() - st.y_dev.float()).norm() / cur.float().norm()
+        assert float(d) < 2e-2, (it, float(d))
+
+
 @pytest.mark.parametrize("spec", [("tucker", (5120, 5120), 1, (128, 128)), ("tr", (64, 80, 64, 80), 2, (16, 16, 16, 16)),
                                   ("tr", (5120, 5120), 1, (8, 8)), ("tt", (16, 16, 16, 16), 2, (8, 8, 8))])
 @pytest.mark.parametrize("m", [1, 5, 8])
