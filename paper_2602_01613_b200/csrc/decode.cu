@@ -122,10 +122,6 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       }
     }
     __syncwarp();
-    if (a.flags_reset && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-      pdl_wait();
-      for (int i = lane_id(); i < a.flags_n; i += 32) a.flags_reset[i] = 0u;
-    }
     if (a.zero_prev) {  // a buffer only the previous kernel read: zero this CTA's slice
       pdl_wait();
       const int64_t ncta = (int64_t)gridDim.x * gridDim.y * gridDim.z;

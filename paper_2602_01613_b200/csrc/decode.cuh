@@ -52,10 +52,6 @@ struct DecArgs {
   int64_t ldx_host;
   __nv_bfloat16* y_host;
   int64_t ldy_host;
-  // decode stacks with the flag handoff: CTA 0 re-zeroes these boundary flags after its dependency
-  // wait (the previous boundary kernel has completed, so every flag has been consumed)
-  unsigned int* flags_reset;
-  int32_t flags_n;
 };
 
 // phase A: weights (TMA map `w`, rows=M_rows, K) x activations (TMA map `x`, bf16 tokens x K)
@@ -84,25 +80,11 @@ struct FusedArgs {
   unsigned long long* trace;  // optional per-CTA %globaltimer stamps [cta][16]
   int32_t kg;          // gated MLP boundary (0: plain): the first kg 64-blocks of kappa are the gate's
                        // cut (T_g, A_g), the rest the up projection's; y = silu(A_g T_g) * (A_u T_u)
-  // Flag handoff between consecutive boundary kernels (decode stacks): instead of griddepcontrol.wait
-  // (full completion of the previous grid), wait until flag_wait >= flag_target (every CTA of the
-  // previous boundary has issued its reductions and zeroing, then fenced and signalled); signal
-  // flag_signal the same way. Zero-at-rest: the stack's last phase-B kernel resets the flags.
-  unsigned int* flag_wait;
-  unsigned int flag_target;
-  unsigned int* flag_signal;
 };
 // wo: A_out^l map (box {64, 128}, SW128); t: T_l fp32 map (box {BN, 64}); wi: B_in^{l+1}
 // map (box {64, 128}, SW128). grid = rows / 128.
 int launch_dec_fused(const CUtensorMap& wo, const CUtensorMap& t, const CUtensorMap& wi,
                      const FusedArgs& a, int grid, cudaStream_t st);
-
-// The same boundary over CTA pairs (decode_pair.cu): 2x1 clusters own 256 rows, M=256
-// cta_group::2 MMAs; T_l read split by tokens, T_{l+1} reductions split by kappa (plain
-// boundaries: kB, nA <= 256, rows % 256 == 0, no flag handoff). grid = rows / 128.
-bool dec_fused_pair_ok(const FusedArgs& a);
-int launch_dec_fused_pair(const CUtensorMap& wo, const CUtensorMap& wi, const FusedArgs& a, int grid,
-                          cudaStream_t st);
 
 // CUDA-core GEMV variants (tokens <= 8): warp per weight row, no atomics.
 // T is fp32 [tokens][ldt] (plain stores, no zero-at-rest requirement).

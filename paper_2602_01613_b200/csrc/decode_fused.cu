@@ -133,10 +133,8 @@ __global__ void __launch_bounds__(FT, 1)
           for (int h = 0; h < 2; ++h)
             tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull, tile * 128 + h * 64, t * 128, pol);
       TRACE(2);
-      if (!a.flag_wait) {
-        pdl_wait();
-        TRACE(3);
-      }
+      pdl_wait();
+      TRACE(3);
       if constexpr (LARGE) {  // B_in into the gate's A blocks once the gate MMAs have read them
         mbar_wait(gdone, 0);
         mbar_arrive_expect_tx(wfull2, 2 * nT * WBLK);
@@ -148,12 +146,7 @@ __global__ void __launch_bounds__(FT, 1)
     __syncwarp();
     // T_{l-1} was read only by the previous kernel, which has completed: zero this CTA's slice
     if (a.t_zero) {
-      if (a.flag_wait) {
-        if (lane_id() == 0) flag_wait_geq(a.flag_wait, a.flag_target);
-        __syncwarp();
-      } else {
-        pdl_wait();
-      }
+      pdl_wait();
       const int64_t n4 = a.zero_elems / 4, per = (n4 + gridDim.x - 1) / gridDim.x;
       float4* z = reinterpret_cast<float4*>(a.t_zero);
       const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(n4, e0 + per);
@@ -192,15 +185,7 @@ __global__ void __launch_bounds__(FT, 1)
     __syncwarp();
   } else {
     const int et = threadIdx.x - 64;
-    if (a.flag_wait) {
-      if (et == 0) {
-        flag_wait_geq(a.flag_wait, a.flag_target);
-        TRACE(3);
-      }
-      nbar(2, FEPI);
-    } else {
-      pdl_wait();
-    }
+    pdl_wait();
     if (et == 0) TRACE(11);
     // T_l: fp32 [64 kappa][BN tokens] -> bf16 MN-major SW128 [64 kappa][128 B] per k-block
     // (the accumulator's kappa-major layout is the MMA's MN-major B operand: no transpose).
@@ -334,9 +319,7 @@ __global__ void __launch_bounds__(FT, 1)
 
   }
   tc_fence_before();
-  if (a.flag_signal) __threadfence();  // this thread's reductions / zeroing stores, before the signal
   __syncthreads();
-  if (a.flag_signal && threadIdx.x == 0) red_release_add_u32(a.flag_signal, 1u);
   if (warp == 1) tmem_dealloc<256>(tmem);
   if (threadIdx.x == 32) TRACE(10);
 #undef TRACE

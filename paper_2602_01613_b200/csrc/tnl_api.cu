@@ -1828,7 +1828,7 @@ static bool stack_fusable(const tnl_plan* const* plans, int32_t n, int64_t m) {
 }
 
 static size_t stack_ws_bytes(const tnl_plan* const* plans, int32_t n, int64_t m) {
-  if (stack_fusable(plans, n, m)) return kDecSlots * kDecSlotBytes + round_up(sizeof(unsigned) * (size_t)n, 256);
+  if (stack_fusable(plans, n, m)) return kDecSlots * kDecSlotBytes;
   size_t mx = 0;
   int64_t width = 0;
   for (int i = 0; i < n; ++i) {
@@ -2026,11 +2026,6 @@ static tnl_status stack_forward_impl(const tnl_plan* const* plans, int32_t n, co
   float* tacc[3] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + kDecSlotBytes),
                     reinterpret_cast<float*>(base + 2 * kDecSlotBytes)};
   unsigned int* cnt = reinterpret_cast<unsigned int*>(base + 2 * kDecSlotBytes + kDecHeadBytes);
-  // boundary flags (zero at rest): boundary l signals flags[l]; boundary l+1 waits for all of its
-  // CTAs there instead of for the grid's completion (TNL_DEC_FLAGS=1; default griddepcontrol.wait)
-  unsigned int* flags = reinterpret_cast<unsigned int*>(base + kDecSlots * kDecSlotBytes);
-  // measured slower than griddepcontrol.wait (profiles/r02/ab_decode_flags_pair.jsonl): opt-in A/B
-  static const bool use_flags = getenv("TNL_DEC_FLAGS") && atoi(getenv("TNL_DEC_FLAGS")) == 1;
   const int bn = pick_bn(m);
   int err = 0;
   // layer 0, phase A
@@ -2082,18 +2077,9 @@ static tnl_status stack_forward_impl(const tnl_plan* const* plans, int32_t n, co
     f.t_zero = l >= 1 ? tacc[(l + 2) % 3] : nullptr;
     f.zero_elems = l >= 1 ? 64 * Pv[l - 1]->r_pad : 0;
     f.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
-    if (use_flags) {
-      f.flag_signal = flags + l;
-      if (l >= 1) {
-        f.flag_wait = flags + l - 1;
-        f.flag_target = (unsigned)(Pv[l - 1]->rows / 128);  // the previous boundary's grid
-      }
-    }
-    // CTA-pair boundary where a side has rank > 128 (TNL_DEC_PAIR: 0 never, 2 every plain boundary)
-    static const int pair_mode = getenv("TNL_DEC_PAIR") ? atoi(getenv("TNL_DEC_PAIR")) : 1;
-    const bool pair = pair_mode && dec_fused_pair_ok(f) && (pair_mode == 2 || f.kB > 128 || f.nA > 128);
-    if ((err = pair ? launch_dec_fused_pair(two, twi, f, (int)(P->rows / 128), st)
-                    : launch_dec_fused(two, tt, twi, f, (int)(P->rows / 128), st)))
+    // (griddepcontrol.wait handoff and one CTA per 128 rows: a flag handoff and a CTA-pair
+    // boundary kernel were built and measured slower, profiles/r02/ab_decode_flags_pair.jsonl)
+    if ((err = launch_dec_fused(two, tt, twi, f, (int)(P->rows / 128), st)))
       return fail(TNL_ERR_CUDA, "stack boundary launch: %s", cudaGetErrorString((cudaError_t)err));
   }
   // last layer, phase B
@@ -2125,10 +2111,6 @@ static tnl_status stack_forward_impl(const tnl_plan* const* plans, int32_t n, co
       b.zero_prev_elems = 64 * Pv[l - 1]->r_pad;
     }
     b.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
-    if (use_flags && n >= 2) {
-      b.flags_reset = flags;
-      b.flags_n = n - 1;
-    }
     if (host_io) {
       b.y_host = static_cast<__nv_bfloat16*>(y);
       b.ldy_host = ldy;
