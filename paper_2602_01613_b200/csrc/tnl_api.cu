@@ -38,6 +38,7 @@
 #include "common.cuh"
 #include "decode.cuh"
 #include "generic.cuh"
+#include "tc_generic.cuh"
 #include "mlp.cuh"
 #include "tc_gemm.cuh"
 
@@ -321,6 +322,11 @@ struct tnl_plan {
   __nv_bfloat16* chain_d = nullptr;  // Dp [(alpha, c_pad)][n_b]
   __nv_bfloat16* chain_c = nullptr;  // Cp [(j_a, b_pad)][c_pad]
   int32_t ch_na = 0, ch_nb = 0, ch_r0 = 0, ch_c = 0, ch_cpad = 0, ch_b = 0, ch_bpad = 0;
+  // bf16 core-by-core chain on the tensor cores (tc_generic.cu), TNL_PLAN_CHAIN: the GENERIC step
+  // list with bf16 cores / intermediates. tcg_out: two-mode input chain kernel, then the output
+  // cores one by one; tcg_full: every core one by one (TT/TR of any shape, Tucker d >= 3).
+  std::vector<__nv_bfloat16*> gcore16;
+  bool tcg_out = false, tcg_full = false;
 
   float* gen_w_out = nullptr;       // generic dense rows slice (fp32) for sharded generic plans
   // fp32 merged cut (CUDA-core FFMA): B_in (r_cut x cols), A_out rows (rows_local x r_cut)
@@ -777,6 +783,91 @@ static int64_t max_state_per_token(const tnl_plan* P) {
   return mx;
 }
 
+// One GENERIC step as a tensor-core step (tc_generic.cu): batch dims that only one operand depends on
+// are folded into that operand's free side (a core shared by every token becomes the B operand of
+// an MMA whose N side runs over the tokens), the larger side becomes the MMA's M = 128 side.
+static bool tcg_from_gstep(const GStep& g, TcgArgs* t) {
+  if (g.a_dt != DT_BF16 || g.b_dt != DT_BF16) return false;
+  struct D {
+    int64_t size, so, sc;
+  };
+  std::vector<D> Is = {{g.I, g.sai, g.sci}}, Js = {{g.J, g.sbj, g.scj}}, Zs;
+  std::vector<std::pair<int64_t, int64_t>> zab;  // (sa, sb) of the true batch dims
+  auto batch = [&](int64_t b, int64_t sa, int64_t sb, int64_t sc) {
+    if (b <= 1) return;
+    if (sa == 0 && sb != 0)
+      Js.insert(Js.begin(), {b, sb, sc});
+    else if (sb == 0 && sa != 0)
+      Is.insert(Is.begin(), {b, sa, sc});
+    else {
+      Zs.push_back({b, 0, sc});
+      zab.push_back({sa, sb});
+    }
+  };
+  batch(g.b2, g.sa2, g.sb2, g.sc2);
+  batch(g.b1, g.sa1, g.sb1, g.sc1);
+  auto squeeze = [](std::vector<D>& v) {
+    std::vector<D> o;
+    for (auto& e : v)
+      if (e.size > 1) o.push_back(e);
+    if (o.empty()) o.push_back({1, 0, 0});
+    v = o;
+  };
+  squeeze(Is);
+  squeeze(Js);
+  if (Is.size() > 3 || Js.size() > 3 || Zs.size() > 2) return false;
+  auto total = [](const std::vector<D>& v) {
+    int64_t n = 1;
+    for (auto& e : v) n *= e.size;
+    return n;
+  };
+  const bool swap = total(Js) > total(Is);
+  const std::vector<D>& Ms = swap ? Js : Is;
+  const std::vector<D>& Ns = swap ? Is : Js;
+  memset(t, 0, sizeof *t);
+  t->A = static_cast<const __nv_bfloat16*>(swap ? g.B : g.A);
+  t->B = static_cast<const __nv_bfloat16*>(swap ? g.A : g.B);
+  t->ka = swap ? g.sbp : g.sap;
+  t->kb = swap ? g.sap : g.sbp;
+  t->C = g.C;
+  t->c_f32 = g.c_dt == DT_F32;
+  t->accumulate = g.accumulate;
+  t->K = g.P;
+  auto fill = [](const std::vector<D>& v, TcgSide& sd) {
+    sd.nd = (int32_t)v.size();
+    for (size_t i = 0; i < v.size(); ++i) {
+      sd.size[i] = v[i].size;
+      sd.so[i] = v[i].so;
+      sd.sc[i] = v[i].sc;
+    }
+  };
+  fill(Ms, t->m);
+  fill(Ns, t->n);
+  t->M = total(Ms);
+  t->N = total(Ns);
+  t->z1 = Zs.size() == 2 ? Zs[0].size : 1;
+  t->z2 = Zs.empty() ? 1 : Zs.back().size;
+  if (Zs.size() == 2) {
+    t->za1 = swap ? zab[0].second : zab[0].first;
+    t->zb1 = swap ? zab[0].first : zab[0].second;
+    t->zc1 = Zs[0].sc;
+  }
+  if (!Zs.empty()) {
+    t->za2 = swap ? zab.back().second : zab.back().first;
+    t->zb2 = swap ? zab.back().first : zab.back().second;
+    t->zc2 = Zs.back().sc;
+  }
+  auto vec_ok = [&](const __nv_bfloat16* p, int64_t ks, const TcgSide& sd, int64_t z1s, int64_t z2s) {
+    if (ks != 1 || t->K % 8 || (reinterpret_cast<uintptr_t>(p) & 15) || z1s % 8 || z2s % 8) return 0;
+    for (int i = 0; i < sd.nd; ++i)
+      if (sd.size[i] > 1 && sd.so[i] % 8) return 0;
+    return 1;
+  };
+  t->a_vec = vec_ok(t->A, t->ka, t->m, t->za1, t->za2);
+  t->b_vec = vec_ok(t->B, t->kb, t->n, t->zb1, t->zb2);
+  return true;
+}
+
 static int run_steps(const std::vector<GStep>& steps, cudaStream_t st) {
   for (const auto& s : steps) {
     int e = launch_generic_step(s, st);
@@ -1195,6 +1286,16 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   const bool cut32 = !bf16 && P->family != TNL_FAMILY_DENSE && !(flags & (TNL_PLAN_GENERIC | TNL_PLAN_CHAIN)) &&
                      P->cut_flops <= P->chain_flops;
   if (cut32) large = TNL_PLAN_CUT;
+  // bf16 core-by-core chain for every other TT/TR/Tucker shape (unsharded plans)
+  if (tc_ok && (flags & TNL_PLAN_CHAIN) && P->family != TNL_FAMILY_DENSE && !tucker2 && P->row_begin == 0 &&
+      P->row_end == P->rows) {
+    if (P->chain_ok) {
+      P->tcg_out = rm >= 2;  // rm == 1: the output "panel" is the single output core itself
+    } else {
+      P->tcg_full = true;
+      large = TNL_PLAN_CHAIN;
+    }
+  }
   P->plan_large = large;
   P->plan_small = large;
   P->decode_max_m = (tc_ok && P->family != TNL_FAMILY_DENSE && round_up(P->r_cut, 16) <= 256 &&
@@ -1228,6 +1329,12 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
     off_a32 = bytes;
     bytes += round_up(rows_local * P->r_cut * 4, 256);
   }
+  std::vector<size_t> off16;
+  if (P->tcg_out || P->tcg_full)
+    for (auto& h : host) {
+      off16.push_back(bytes);
+      bytes += round_up((int64_t)h.size() * 2, 256);
+    }
   size_t off_chd = 0, off_chc = 0;
   if (P->chain_ok) {
     off_chd = bytes;
@@ -1257,6 +1364,11 @@ static tnl_status create_impl(const tnl_layer_desc* L, int32_t compute_dtype, in
   }
   bt.mark("upload");
   cudaStream_t st = 0;
+  for (size_t i = 0; i < off16.size(); ++i) {
+    __nv_bfloat16* d16 = reinterpret_cast<__nv_bfloat16*>(base + off16[i]);
+    to_bf16(P->gcore[i], d16, (int64_t)host[i].size(), st);
+    P->gcore16.push_back(d16);
+  }
   if (large == TNL_PLAN_CUT && dense) {
     P->wdense = reinterpret_cast<__nv_bfloat16*>(base + off_w);
     copy_2d_any<<<grid_for(rows_local * P->cols), 256, 0, st>>>(
@@ -1355,7 +1467,8 @@ constexpr size_t kDecHeadBytes = sizeof(float) * 64 * 512;  // decode accumulato
 constexpr size_t kDecSlotBytes = kDecHeadBytes + 256 + sizeof(float) * 8 * 256;
 constexpr int kDecSlots = 3;  // slots 0..2 double as the three rotating accumulators of a fused stack
 
-static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b0, size_t* o_b1) {
+static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b0, size_t* o_b1,
+                        size_t* o_s = nullptr) {
   size_t bytes = 0;
   auto take = [&](size_t n) {
     size_t o = bytes;
@@ -1382,6 +1495,12 @@ static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b
   *o_f32 = take(sizeof(float) * M * kmax);
   *o_b0 = take(2 * M * kmax);
   *o_b1 = take(2 * M * kmax);
+  if (P->tcg_out || P->tcg_full) {  // the bf16 chain's two intermediate states + split-K scratch
+    const size_t s0 = take(2 * M * P->max_state);
+    take(2 * M * P->max_state);
+    take(4 * M * std::max<int64_t>(P->max_state, std::max(P->rows, P->r_pad)));  // zero at rest
+    if (o_s) *o_s = s0;
+  }
   return bytes;
 }
 
@@ -1617,6 +1736,67 @@ static bool no_splitk2() {  // A/B switch (TNL_SPLITK2=0: fp32 split-K + convers
   return v;
 }
 
+// TNL_PLAN_CHAIN in bf16 for the shapes without a fused chain kernel: the GENERIC core-by-core step
+// list (cores in their permuted layouts, ring closure carried as a batch index) with bf16 cores and
+// bf16 intermediates, every step on the tensor cores (tc_generic.cu). tcg_out plans run the input
+// side in the two-mode chain kernel (intermediates on chip) and only the output cores as steps.
+static tnl_status forward_tcg(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y, int64_t ldy, void* ws,
+                              size_t ws_bytes, cudaStream_t st) {
+  size_t o_f32, o_b0, o_b1, o_s = 0;
+  const size_t need = ws_layout(P, M, &o_f32, &o_b0, &o_b1, &o_s);
+  if (ws_bytes < need) return fail(TNL_ERR_ARG, "workspace %zu < required %zu bytes", ws_bytes, need);
+  char* w = static_cast<char*>(ws);
+  ChainIO io;
+  io.ws[0] = reinterpret_cast<float*>(w + o_s);  // bf16 states (the step builder only passes them on)
+  io.ws[1] = reinterpret_cast<float*>(w + o_s + round_up(2 * M * P->max_state, 256));
+  float* acc32 = reinterpret_cast<float*>(w + o_s + 2 * round_up(2 * M * P->max_state, 256));
+  io.out = {y, DT_BF16, ldy, 1};
+  int seg = SEG_FULL;
+  if (P->tcg_out) {
+    __nv_bfloat16* t0 = reinterpret_cast<__nv_bfloat16*>(w + o_b0);
+    float* tf = reinterpret_cast<float*>(w + o_f32);
+    const int64_t tiles_m = (M + 127) / 128;
+    const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(P->ch_na / 4, 148 / tiles_m));
+    tnl_status cs;
+    if (splits > 1) {
+      if (cudaMemsetAsync(tf, 0, sizeof(float) * M * P->r_pad, st) != cudaSuccess)
+        return fail(TNL_ERR_CUDA, "memset failed");
+      cs = chain_in(P, x, ldx, M, tf, P->r_pad, 1, true, splits, st);
+      if (cs) return cs;
+      to_bf16(tf, t0, M * P->r_pad, st);
+    } else {
+      cs = chain_in(P, x, ldx, M, t0, P->r_pad, 1, false, 1, st);
+      if (cs) return cs;
+    }
+    io.in = {t0, DT_BF16, P->r_pad, 1};
+    seg = SEG_OUTPUT;
+  } else {
+    io.in = {x, DT_BF16, ldx, 1};
+  }
+  std::vector<GStep> steps;
+  build_steps(P, seg, M, io, steps);
+  auto is_state = [&](const void* p) { return p == io.ws[0] || p == io.ws[1]; };
+  for (GStep g : steps) {
+    auto to16 = [&](const void*& p, int32_t& dt) {
+      if (is_state(p)) dt = DT_BF16;
+      for (size_t k = 0; k < P->gcore.size(); ++k)
+        if (p == P->gcore[k]) {
+          p = P->gcore16[k];
+          dt = DT_BF16;
+        }
+    };
+    to16(g.A, g.a_dt);
+    to16(g.B, g.b_dt);
+    if (is_state(g.C)) g.c_dt = DT_BF16;
+    TcgArgs t;
+    if (!tcg_from_gstep(g, &t)) return fail(TNL_ERR_UNSUPPORTED, "bf16 chain: step not expressible on the tensor cores");
+    t.acc32 = acc32;
+    const int err = launch_tc_generic(t, st);
+    if (err) return fail(TNL_ERR_CUDA, "bf16 chain step launch: %s", cudaGetErrorString((cudaError_t)err));
+  }
+  return TNL_OK;
+}
+
 static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx, void* y, int64_t ldy,
                              void* ws, size_t ws_bytes, cudaStream_t st, const tnl_fwd_opts* o = nullptr) {
   const bool fold = o && (o->accumulate || o->ss_in);
@@ -1632,6 +1812,7 @@ static tnl_status forward_tc(tnl_plan* P, const void* x, int64_t M, int64_t ldx,
   if (fold && (M <= kSwapMaxM || P->family == TNL_FAMILY_DENSE || P->plan_large == TNL_PLAN_CHAIN ||
                (reinterpret_cast<uintptr_t>(y) & 15) || ldy % 8 || (P->r_pad % 8)))
     return fail(TNL_ERR_UNSUPPORTED, "folded residual / RMSNorm: prefill (M > %lld) cut plans only", (long long)kSwapMaxM);
+  if (P->tcg_out || P->tcg_full) return forward_tcg(P, x, M, ldx, y, ldy, ws, ws_bytes, st);
   if (M <= kDecMaxM && P->decode_max_m && !(reinterpret_cast<uintptr_t>(y) & 15) && ldy % 8 == 0)
     return forward_decode(P, x, M, ldx, y, ldy, ws, st);
   tnl_status s;
