@@ -80,6 +80,8 @@ struct FusedArgs {
   unsigned long long* trace;  // optional per-CTA %globaltimer stamps [cta][16]
   int32_t kg;          // gated MLP boundary (0: plain): the first kg 64-blocks of kappa are the gate's
                        // cut (T_g, A_g), the rest the up projection's; y = silu(A_g T_g) * (A_u T_u)
+  int32_t ksplit;      // plain boundaries with nA > 128: 2 CTAs per row tile, one kappa' half each
+                       // (grid = 2 * rows / 128); 0/1: one CTA per row tile
 };
 // wo: A_out^l map (box {64, 128}, SW128); t: T_l fp32 map (box {BN, 64}); wi: B_in^{l+1}
 // map (box {64, 128}, SW128). grid = rows / 128.

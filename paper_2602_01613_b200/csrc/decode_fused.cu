@@ -54,7 +54,11 @@ __global__ void __launch_bounds__(FT, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int kbB = (a.kB + 63) / 64;
-  const int nT = (a.nA + 127) / 128;
+  // kappa split (plain boundaries, a.ksplit == 2): two CTAs per row tile, each computing phase B
+  // for the tile and phase A for one 128-row half of kappa' (half the partial-T egress per CTA)
+  const int ks = a.ksplit > 1 ? a.ksplit : 1;
+  const int nT = ks > 1 ? 1 : (a.nA + 127) / 128;
+  const int t0 = ks > 1 ? (int)(blockIdx.x % ks) : 0;  // first kappa' tile of this CTA
   constexpr bool LARGE = KMAX > 4;        // B_in aliases the gate's A blocks (loaded after their MMAs)
   uint8_t* sWo = smem;                    // kbB blocks
   uint8_t* sWi = LARGE ? sWo : sWo + kbB * WBLK;  // nT x 2 blocks (then the D_A transpose stage)
@@ -73,7 +77,7 @@ __global__ void __launch_bounds__(FT, 1)
   uint64_t* wfull2 = bars + 17;  // LARGE: B_in landed
   uint32_t* last_flag = tmem_slot + 1;
 
-  const int tile = blockIdx.x;
+  const int tile = blockIdx.x / ks;
   unsigned long long* tr = a.trace ? a.trace + 16 * blockIdx.x : nullptr;
 #ifdef TNL_TRACE_CLOCK  // SM-local cycle stamps (diagnostic builds)
 #define TRACE(ev) \
@@ -131,7 +135,7 @@ __global__ void __launch_bounds__(FT, 1)
       if (!LARGE)
         for (int t = 0; t < nT; ++t)
           for (int h = 0; h < 2; ++h)
-            tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull, tile * 128 + h * 64, t * 128, pol);
+            tma_load_2d_hint(sWi + (t * 2 + h) * WBLK, &tmWi, wfull, tile * 128 + h * 64, (t0 + t) * 128, pol);
       TRACE(2);
       pdl_wait();
       TRACE(3);
@@ -284,12 +288,12 @@ __global__ void __launch_bounds__(FT, 1)
       return stage + (uint32_t)(kap * SLOTS + (sl ^ (kap & 7 & (SLOTS - 1)))) * 16u;
     };
     for (int t = 0; t < nT; ++t) {
-      const int kap = t * 128 + lrow;
+      const int kap = t * 128 + lrow;  // local row of this CTA's kappa' range
 #pragma unroll 1
       for (int c = c_begin; c < c_begin + HALF && c < BN; c += 16) {
         float v[16];
         tmem_ld16(tDA + t * BN + ((q * 32) << 16) + c, v);
-        if (kap >= a.nA) continue;
+        if (t0 * 128 + kap >= a.nA) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint4 p;
@@ -304,14 +308,16 @@ __global__ void __launch_bounds__(FT, 1)
     nbar(1, FEPI);
     {
       const int tok_slots = (a.tokens + 3) / 4 < SLOTS ? (a.tokens + 3) / 4 : SLOTS;
-      for (int e = et; e < a.nA * SLOTS; e += FEPI) {
+      const int rows_here = min(a.nA - t0 * 128, nT * 128);
+      float* t_out = a.t_out + (int64_t)t0 * 128 * 64;
+      for (int e = et; e < rows_here * SLOTS; e += FEPI) {
         const int kap = e / SLOTS, sl = e % SLOTS;
         if (sl >= tok_slots) continue;
         const float4 v = lds128f(slot_addr(kap, sl));
 #ifdef TNL_DIAG_NORED  // timing diagnostic only: plain stores instead of reductions (wrong results)
-        *reinterpret_cast<float4*>(a.t_out + (int64_t)kap * 64 + sl * 4) = v;
+        *reinterpret_cast<float4*>(t_out + (int64_t)kap * 64 + sl * 4) = v;
 #else
-        red_add_v4(a.t_out + (int64_t)kap * 64 + sl * 4, v.x, v.y, v.z, v.w);
+        red_add_v4(t_out + (int64_t)kap * 64 + sl * 4, v.x, v.y, v.z, v.w);
 #endif
       }
     }

@@ -2260,7 +2260,9 @@ static tnl_status stack_forward_impl(const tnl_plan* const* plans, int32_t n, co
     f.trace = P->trace ? P->trace + 16 * 1024 : nullptr;
     // (griddepcontrol.wait handoff and one CTA per 128 rows: a flag handoff and a CTA-pair
     // boundary kernel were built and measured slower, profiles/r02/ab_decode_flags_pair.jsonl)
-    if ((err = launch_dec_fused(two, tt, twi, f, (int)(P->rows / 128), st)))
+    static const int ksplit_env = getenv("TNL_DEC_KSPLIT") ? atoi(getenv("TNL_DEC_KSPLIT")) : 0;  // A/B
+    f.ksplit = (ksplit_env == 2 && f.nA > 128) ? 2 : 1;
+    if ((err = launch_dec_fused(two, tt, twi, f, (int)(P->rows / 128) * f.ksplit, st)))
       return fail(TNL_ERR_CUDA, "stack boundary launch: %s", cudaGetErrorString((cudaError_t)err));
   }
   // last layer, phase B
