@@ -39,6 +39,7 @@
 #include "decode.cuh"
 #include "generic.cuh"
 #include "tc_generic.cuh"
+#include "dec32.cuh"
 #include "mlp.cuh"
 #include "tc_gemm.cuh"
 
@@ -1941,6 +1942,16 @@ static tnl_status forward_generic(tnl_plan* P, const void* x, int64_t M, int64_t
   if (ws_bytes < need) return fail(TNL_ERR_ARG, "workspace %zu < required %zu bytes", ws_bytes, need);
   char* w = static_cast<char*>(ws);
   const int dt = P->compute_dtype == TNL_BF16 ? DT_BF16 : DT_F32;
+  if (P->bin32 && M <= 32 && P->r_cut <= kDec32MaxCut && !(P->flags & TNL_PLAN_NO_DECODE)) {
+    // small M: the two fp32 decode phases (dec32.cu), accumulator + counter at the workspace head
+    float* tacc = reinterpret_cast<float*>(w);
+    unsigned int* counter = reinterpret_cast<unsigned int*>(w + kDecHeadBytes);
+    const int err = launch_dec32(P->bin32, P->cols, P->aout32, P->r_cut, (int)(P->row_end - P->row_begin),
+                                 (int)P->r_cut, (int)P->cols, static_cast<const float*>(x), ldx, (int)M,
+                                 static_cast<float*>(y), ldy, tacc, counter, st);
+    if (err) return fail(TNL_ERR_CUDA, "fp32 decode launch: %s", cudaGetErrorString((cudaError_t)err));
+    return TNL_OK;
+  }
   if (P->bin32) {
     // fp32 merged cut: T[kappa][m] = sum_j B_in[kappa][j] x[m][j] (split-K FFMA, fp32 atomics),
     // then y[m][i] = sum_kappa A_out[i][kappa] T[kappa][m]

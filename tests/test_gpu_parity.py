@@ -131,6 +131,34 @@ def test_cfg1_tt_fp32():
     check_bf16(L, 300, seed=12, flags=tnl.PLAN_CHAIN)
 
 
+@pytest.mark.parametrize("spec", [("tt", (64, 64, 64, 64), 2, (32, 32, 32)), ("tr", (5120, 5120), 1, (16, 16)),
+                                  ("tucker", (40, 24, 16), 1, (5, 4, 6)), ("tr", (6, 10, 8, 4), 2, (3, 2, 4, 2))])
+def test_fp32_small_m_cut_repeated(spec):
+    """fp32 merged cut at M <= 32 (dec32.cu: split-K phase A into the zero-at-rest accumulator,
+    phase B with the last-CTA re-zero) against the float64 oracle, call after call, M straddling
+    the 32-token limit (M = 33 takes the generic FFMA steps)."""
+    fam, ms, rm, ranks = spec
+    L = O.synthetic_layer(fam, ms, rm, ranks, seed=50_500)
+    kw = dict(family=L.family, mode_shape=L.mode_shape, row_mode_count=L.row_mode_count)
+    if fam == "tucker":
+        kw.update(core=L.core.astype(np.float32), factors=[u.astype(np.float32) for u in L.factors])
+        L32 = O.OracleLayer(core=L.core.astype(np.float32).astype(np.float64),
+                            factors=[u.astype(np.float32).astype(np.float64) for u in L.factors], **{k: kw[k] for k in ("family", "mode_shape", "row_mode_count")})
+    else:
+        kw.update(cores=[c.astype(np.float32) for c in L.cores])
+        L32 = O.OracleLayer(cores=[c.astype(np.float32).astype(np.float64) for c in L.cores],
+                            **{k: kw[k] for k in ("family", "mode_shape", "row_mode_count")})
+    layer = tnl.CompressedLayer(**kw)
+    p = layer.plan(torch.float32)
+    rows, cols = layer.matrix_shape
+    for m in (1, 5, 16, 32, 33, 1):
+        x = O.synthetic_x(m, cols, seed=50_600 + m).astype(np.float32).astype(np.float64)
+        for _ in range(2):
+            y = p.forward(torch.tensor(x, dtype=torch.float32, device=DEV))
+            torch.cuda.synchronize()
+            assert rel(O.forward_torch_orient(L32, x), y.double().cpu().numpy()) <= FP32_TOL, (spec, m)
+
+
 @pytest.mark.parametrize("R", [64, 128, 256])
 @pytest.mark.parametrize("m", [1, 7, 16, 64, 200])
 def test_cfg2_tucker2(R, m):
