@@ -77,8 +77,9 @@ typedef enum { TNL_F64 = 0, TNL_F32 = 1, TNL_BF16 = 2 } tnl_dtype;
 enum {
   TNL_PLAN_AUTO = 0,
   TNL_PLAN_CUT = 1,     /* merged cut: y = A_out (B_in x), two tensor-core GEMMs */
-  TNL_PLAN_CHAIN = 2,   /* core-by-core chain (Tucker-2: U_in, G, U_out; TT/TR:
-                           input modes streamed, cut kept on chip)            */
+  TNL_PLAN_CHAIN = 2,   /* core-by-core chain, every family and shape (bf16:
+                           tcgen05 steps; Tucker-2 and a two-mode TT/TR input
+                           side in fused kernels with intermediates on chip)  */
   TNL_PLAN_GENERIC = 4, /* CUDA-core strided chain (exact fp32 FFMA path)     */
   TNL_PLAN_NO_DECODE = 8, /* disable the small-M decode kernels                 */
   TNL_PLAN_GEMV = 16     /* M <= 8: CUDA-core GEMV decode variant (warp per row) */
