@@ -191,6 +191,27 @@ def test_cfg3_mlp_tt(which):
             check_bf16(L, m, seed=30_999 + m, flags=flags)
 
 
+@pytest.mark.parametrize("r", [32, 128])
+def test_cfg3_ranks_projections_and_block(r):
+    """cfg3 at the other SURVEY ranks (r in {32, 64, 128}): gate/down projections (cut and chain
+    plans) and the MLP block (fused when the kernels take the ranks, else unfused) vs the oracle."""
+    from paper_2602_01613_b200.mlp import TNMLP
+
+    specs = [(160, 160, 64, 80), (160, 160, 64, 80), (64, 80, 160, 160)]
+    Ls = [O.synthetic_layer("tt", ms, 2, (r, r, r), seed=52_000 + 10 * r + i) for i, ms in enumerate(specs)]
+    for L in (Ls[0], Ls[2]):
+        for flags in (tnl.PLAN_AUTO, tnl.PLAN_CHAIN):
+            for m in (1, 64, 256):
+                check_bf16(L, m, seed=52_999 + m, flags=flags)
+    pairs = [to_layer(L, round_bf16=True) for L in Ls]
+    mlp = TNMLP(*[p[0] for p in pairs])
+    for m in (1, 64, 256):
+        x = O.round_bf16(O.synthetic_x(m, 5120, seed=53_000 + m))
+        y = mlp(torch.tensor(x, dtype=torch.bfloat16, device=DEV))
+        torch.cuda.synchronize()
+        assert rel(_mlp_ref(*[p[1] for p in pairs], x), y.float().cpu().numpy()) <= 2 * BF16_TOL, (r, m, mlp.fused)
+
+
 def test_cfg3_full_size_properties():
     """M=8192 prefill: token independence and linearity (up to the fp32 summation order of the
     split-K first step); sampled rows match the oracle."""
