@@ -27,15 +27,18 @@ constexpr int GM = 128, GN = 64, GK = 64;
 constexpr int GT = 192;  // warps 0-3: A rows (+ epilogue), warps 4-5: B rows
 constexpr uint32_t GA_STAGE = GM * GK * 2, GB_STAGE = GN * GK * 2;
 
-__device__ __forceinline__ int64_t side_offset(const TcgSide& s, int64_t idx, bool c_view) {
+// element offset of index `idx` of a side (sub-dims outermost first); the host keeps every side
+// below 2^31 elements, so the index arithmetic is 32-bit (int64 division is a long software sequence)
+__device__ __forceinline__ int64_t side_offset(const TcgSide& s, int64_t idx64, bool c_view) {
   int64_t off = 0;
+  uint32_t idx = (uint32_t)idx64;
 #pragma unroll
   for (int d = 2; d >= 0; --d) {
     if (d >= s.nd) continue;
-    const int64_t sz = s.size[d];
-    const int64_t i = idx % sz;
+    const uint32_t sz = (uint32_t)s.size[d];
+    const uint32_t i = idx % sz;
     idx /= sz;
-    off += i * (c_view ? s.sc[d] : s.so[d]);
+    off += (int64_t)i * (c_view ? s.sc[d] : s.so[d]);
   }
   return off;
 }
@@ -67,11 +70,14 @@ template <>
 struct RowChunk<false> {
   uint16_t e[64];
   __device__ __forceinline__ void load(const __nv_bfloat16* base, int64_t ks, int64_t k0, int64_t K, bool valid) {
+    const unsigned short* p = reinterpret_cast<const unsigned short*>(base) + k0 * ks;
+    if (valid && k0 + 64 <= K) {  // full chunk: no per-element bound checks
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const int64_t k = k0 + j;
-      e[j] = (valid && k < K) ? __bfloat16_as_ushort(base[k * ks]) : (uint16_t)0;
+      for (int j = 0; j < 64; ++j) e[j] = __ldg(p + j * ks);
+      return;
     }
+#pragma unroll
+    for (int j = 0; j < 64; ++j) e[j] = (valid && k0 + j < K) ? __ldg(p + j * ks) : (unsigned short)0;
   }
   __device__ __forceinline__ void store(uint32_t dst_block, int r) const {
 #pragma unroll
@@ -207,11 +213,18 @@ __global__ void __launch_bounds__(GT, TCG_MINB) tc_generic_kernel(const TcgArgs 
     tc_fence_after();
     const bool rvalid = m0 + tid < a.M;
     const int64_t coff = cz + (rvalid ? side_offset(a.m, m0 + tid, true) : 0);
+    const bool full_n = n0 + GN <= a.N;
+    __nv_bfloat16* c16 = static_cast<__nv_bfloat16*>(a.C) + coff;
 #pragma unroll 1
     for (int c0 = 0; c0 < GN; c0 += 16) {
       float v[16];
       tmem_ld16(tmem + ((warp * 32) << 16) + c0, v);
       if (!rvalid) continue;
+      if (!a.c_f32 && full_n) {  // bf16 intermediate / output, no column tail
+#pragma unroll
+        for (int e = 0; e < 16; ++e) c16[cN[c0 + e]] = __float2bfloat16_rn(v[e]);
+        continue;
+      }
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const int64_t cn = cN[c0 + e];
@@ -220,7 +233,7 @@ __global__ void __launch_bounds__(GT, TCG_MINB) tc_generic_kernel(const TcgArgs 
           float* p = static_cast<float*>(a.C) + coff + cn;
           *p = a.accumulate ? *p + v[e] : v[e];
         } else {
-          static_cast<__nv_bfloat16*>(a.C)[coff + cn] = __float2bfloat16_rn(v[e]);
+          c16[cn] = __float2bfloat16_rn(v[e]);
         }
       }
     }
@@ -237,7 +250,8 @@ size_t tc_generic_smem() { return 1024 + 2 * (GA_STAGE + GB_STAGE) + GN * sizeof
 int launch_tc_generic(const TcgArgs& a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return 0;
   const int64_t tm = (a.M + GM - 1) / GM, tn = (a.N + GN - 1) / GN, zz = a.z1 * a.z2;
-  if (tm > 0x7fffffff || tn > 65535 || zz > 65535 || zz < 1) return (int)cudaErrorInvalidValue;
+  if (tm > 0x7fffffff || tn > 65535 || zz > 65535 || zz < 1 || a.M >= (1ll << 31) || a.N >= (1ll << 31))
+    return (int)cudaErrorInvalidValue;
   static AttrOnce attr;
   int attr_dev = 0;
   if (attr.needed(&attr_dev)) {
