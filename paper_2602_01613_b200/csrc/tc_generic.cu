@@ -24,7 +24,6 @@ namespace tnl {
 namespace {
 
 constexpr int GM = 128, GN = 64, GK = 64;
-constexpr int GT = 192;  // warps 0-3: A rows (+ epilogue), warps 4-5: B rows
 constexpr uint32_t GA_STAGE = GM * GK * 2, GB_STAGE = GN * GK * 2;
 
 // element offset of index `idx` of a side (sub-dims outermost first); the host keeps every side
@@ -92,35 +91,6 @@ struct RowChunk<false> {
   }
 };
 
-// the K loop of one CTA: every thread gathers its row of each chunk (one chunk of lookahead: the
-// loads of chunk c+1 are in flight while chunk c is stored, the CTA synchronises and thread 0
-// issues the chunk's MMAs into the TMEM accumulator)
-template <bool VEC>
-__device__ __forceinline__ void k_loop(const __nv_bfloat16* rbase, int64_t ks, int64_t K, bool valid, int c_beg,
-                                       int nk, uint32_t my_stage0, uint32_t my_stage_bytes, int r, uint32_t sa0,
-                                       uint32_t sb0, uint32_t tmem, uint64_t* mdone) {
-  constexpr uint32_t idesc = idesc_bf16_f32(128, 64);
-  RowChunk<VEC> f;
-  if (nk > 0) f.load(rbase, ks, (int64_t)c_beg * 64, K, valid);
-  for (int c = 0; c < nk; ++c) {
-    const int s = c & 1;
-    if (c >= 2) mbar_wait(&mdone[s], ((c - 2) >> 1) & 1);
-    f.store(my_stage0 + s * my_stage_bytes, r);
-    if (c + 1 < nk) f.load(rbase, ks, (int64_t)(c_beg + c + 1) * 64, K, valid);
-    fence_proxy_async_smem();
-    asm volatile("bar.sync 1, 192;" ::: "memory");
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-      const uint64_t ad = smem_desc_sw128(sa0 + s * (128 * 64 * 2));
-      const uint64_t bd = smem_desc_sw128(sb0 + s * (64 * 64 * 2));
-#pragma unroll
-      for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem, ad + 2 * k, bd + 2 * k, idesc, (c | k) != 0);
-      mma_commit(&mdone[s]);
-      if (c == nk - 1) mma_commit(&mdone[2]);
-    }
-  }
-}
-
 __global__ void finalize_kernel(const TcgArgs a) {
   // split-K partials (dense fp32 [z][M][N], zero at rest) -> C through the strided view
   pdl_wait();
@@ -140,117 +110,203 @@ __global__ void finalize_kernel(const TcgArgs a) {
   }
 }
 
-#ifndef TCG_MINB
-#define TCG_MINB 3  // co-resident CTAs per SM (96 registers)
-#endif
-__global__ void __launch_bounds__(GT, TCG_MINB) tc_generic_kernel(const TcgArgs a) {
+// Persistent, warp-specialised: warps 0-5 gather operand rows (A: 128, B: 64) into a 2-stage
+// ring with one chunk of register lookahead, thread 0 issues each chunk's MMAs into one of two TMEM
+// accumulators; warps 6-9 run the epilogue of tile t while the loaders gather tile t+1. Steps of the
+// chain are often a single 64-k chunk over thousands of tiles, so the per-tile setup (TMEM
+// allocation, barrier initialisation, offset arithmetic) is paid once per CTA, not per tile.
+constexpr int GT_LOAD = 192, GT_ALL = 320;
+
+__global__ void __launch_bounds__(GT_ALL, 2) tc_generic_kernel(const TcgArgs a, int tiles_m, int tiles_n) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sA = smem;                       // 2 stages
-  uint8_t* sB = sA + 2 * GA_STAGE;          // 2 stages
-  int64_t* cN = reinterpret_cast<int64_t*>(sB + 2 * GB_STAGE);  // C offset of each tile column
-  uint64_t* mdone = reinterpret_cast<uint64_t*>(cN + GN);        // [2] stage consumed, [2] all done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + 4);
+  uint8_t* sA = smem;                                             // 2 stages
+  uint8_t* sB = sA + 2 * GA_STAGE;                                // 2 stages
+  int64_t* cN = reinterpret_cast<int64_t*>(sB + 2 * GB_STAGE);   // [2][GN] C offset of each tile column
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cN + 2 * GN);
+  uint64_t* sdone = bars;       // [2] ring stage consumed by its MMAs
+  uint64_t* tfull = bars + 2;   // [2] accumulator complete
+  uint64_t* tempty = bars + 4;  // [2] accumulator read by the 4 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
 
   const int tid = threadIdx.x;
   const uint32_t warp = warp_id();
-  const int64_t m0 = (int64_t)blockIdx.x * GM, n0 = (int64_t)blockIdx.y * GN;
-  const int split = (int)(blockIdx.z % a.splits);
-  const int64_t z = blockIdx.z / a.splits, z1 = z / a.z2, z2 = z % a.z2;
-  const __nv_bfloat16* A = a.A + z1 * a.za1 + z2 * a.za2;
-  const __nv_bfloat16* B = a.B + z1 * a.zb1 + z2 * a.zb2;
-  const int64_t cz = z1 * a.zc1 + z2 * a.zc2;
+  const int nk_all = (int)((a.K + GK - 1) / GK);
+  const int64_t zz = a.z1 * a.z2;
+  const int64_t num_tiles = (int64_t)tiles_m * tiles_n * zz * a.splits;
+  auto decode = [&](int64_t t, int64_t& m0, int64_t& n0, int64_t& z, int& split) {
+    const int64_t tm = t % tiles_m;  // token-side tiles fastest: consecutive CTAs share B rows in L2
+    int64_t r = t / tiles_m;
+    const int64_t tn = r % tiles_n;
+    r /= tiles_n;
+    split = (int)(r % a.splits);
+    z = r / a.splits;
+    m0 = tm * GM;
+    n0 = tn * GN;
+  };
 
   if (tid == 0) {
-    mbar_init(&mdone[0], 1);
-    mbar_init(&mdone[1], 1);
-    mbar_init(&mdone[2], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sdone[i], 1);
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc<GN>(tmem_slot);
-  // this thread's operand row: A rows for warps 0-3, B rows (= tile columns) for warps 4-5
-  const bool is_a = tid < GM;
-  const int r = is_a ? tid : tid - GM;
-  const int64_t grow = is_a ? m0 + r : n0 + r;
-  const bool valid = is_a ? grow < a.M : grow < a.N;
-  const TcgSide& side = is_a ? a.m : a.n;
-  const int64_t roff = valid ? side_offset(side, grow, false) : 0;
-  const __nv_bfloat16* rbase = (is_a ? A : B) + roff;
-  const int64_t ks = is_a ? a.ka : a.kb;
-  const bool vec = (is_a ? a.a_vec : a.b_vec) != 0;
-  if (!is_a) cN[r] = valid ? side_offset(a.n, grow, true) : -1;
+  if (warp == 0) tmem_alloc<2 * GN>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // the previous step's output is this step's operand
 
-  const int nk_all = (int)((a.K + GK - 1) / GK);
-  const int c_beg = split * a.cps, c_end = min(nk_all, c_beg + a.cps), nk = c_end - c_beg;
-  const uint32_t my0 = smem_u32(is_a ? sA : sB), my_bytes = is_a ? GA_STAGE : GB_STAGE;
-  if (vec)
-    k_loop<true>(rbase, ks, a.K, valid, c_beg, nk, my0, my_bytes, r, smem_u32(sA), smem_u32(sB), tmem, mdone);
-  else
-    k_loop<false>(rbase, ks, a.K, valid, c_beg, nk, my0, my_bytes, r, smem_u32(sA), smem_u32(sB), tmem, mdone);
-  pdl_launch_dependents();
-  if (warp < 4 && nk > 0 && a.splits > 1) {  // fp32 partial of this K range -> dense scratch
-    mbar_wait(&mdone[2], 0);
-    tc_fence_after();
-    const bool rvalid = m0 + tid < a.M;
-    float* acc = a.acc32 + (z * a.M + (m0 + tid)) * a.N + n0;
-#pragma unroll 1
-    for (int c0 = 0; c0 < GN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((warp * 32) << 16) + c0, v);
-      if (!rvalid) continue;
+  if (tid < GT_LOAD) {
+    const bool is_a = tid < GM;
+    const int r = is_a ? tid : tid - GM;
+    const TcgSide& side = is_a ? a.m : a.n;
+    const int64_t ks = is_a ? a.ka : a.kb;
+    const bool vec = (is_a ? a.a_vec : a.b_vec) != 0;
+    const uint32_t my0 = smem_u32(is_a ? sA : sB), my_bytes = is_a ? GA_STAGE : GB_STAGE;
+    constexpr uint32_t idesc = idesc_bf16_f32(GM, GN);
+    uint32_t g = 0;  // chunks issued by this CTA (ring position)
+    int lt = 0;
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      int64_t m0, n0, z;
+      int split;
+      decode(t, m0, n0, z, split);
+      const int64_t z1 = z / a.z2, z2 = z % a.z2;
+      const int64_t grow = is_a ? m0 + r : n0 + r;
+      const bool valid = is_a ? grow < a.M : grow < a.N;
+      const __nv_bfloat16* base = is_a ? a.A + z1 * a.za1 + z2 * a.za2 : a.B + z1 * a.zb1 + z2 * a.zb2;
+      const __nv_bfloat16* rbase = base + (valid ? side_offset(side, grow, false) : 0);
+      const int c_beg = split * a.cps, c_end = min(nk_all, c_beg + a.cps);
+      const int acc = lt & 1;
+      auto run = [&](auto chunk) {
+        chunk.load(rbase, ks, (int64_t)c_beg * GK, a.K, valid);
+        for (int c = c_beg; c < c_end; ++c, ++g) {
+          const int s = g & 1;
+          if (g >= 2) mbar_wait(&sdone[s], ((g - 2) >> 1) & 1);
+          chunk.store(my0 + s * my_bytes, r);
+          if (c + 1 < c_end) chunk.load(rbase, ks, (int64_t)(c + 1) * GK, a.K, valid);
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 1, 192;" ::: "memory");
+          if (tid == 0) {
+            if (c == c_beg && lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint64_t ad = smem_desc_sw128(smem_u32(sA) + s * GA_STAGE);
+            const uint64_t bd = smem_desc_sw128(smem_u32(sB) + s * GB_STAGE);
 #pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if (n0 + c0 + e < a.N) atomicAdd(acc + c0 + e, v[e]);
+            for (int k = 0; k < GK / 16; ++k)
+              mma_bf16_ss(tmem + acc * GN, ad + 2 * k, bd + 2 * k, idesc, (c > c_beg || k > 0) ? 1u : 0u);
+            mma_commit(&sdone[s]);
+            if (c == c_end - 1) mma_commit(&tfull[acc]);
+          }
+        }
+      };
+      if (vec)
+        run(RowChunk<true>());
+      else
+        run(RowChunk<false>());
     }
-  } else if (warp < 4 && nk > 0) {
-    mbar_wait(&mdone[2], 0);
-    tc_fence_after();
-    const bool rvalid = m0 + tid < a.M;
-    const int64_t coff = cz + (rvalid ? side_offset(a.m, m0 + tid, true) : 0);
-    const bool full_n = n0 + GN <= a.N;
-    __nv_bfloat16* c16 = static_cast<__nv_bfloat16*>(a.C) + coff;
-#pragma unroll 1
-    for (int c0 = 0; c0 < GN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((warp * 32) << 16) + c0, v);
-      if (!rvalid) continue;
-      if (!a.c_f32 && full_n) {  // bf16 intermediate / output, no column tail
-#pragma unroll
-        for (int e = 0; e < 16; ++e) c16[cN[c0 + e]] = __float2bfloat16_rn(v[e]);
-        continue;
+  } else {
+    // epilogue: TMEM lane quarter q = warp % 4 -> tile rows q*32 .. q*32+31
+    const int et = tid - GT_LOAD;
+    const uint32_t q = warp & 3;
+    const int lrow = q * 32 + lane_id();
+    int lt = 0;
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      int64_t m0, n0, z;
+      int split;
+      decode(t, m0, n0, z, split);
+      const int acc = lt & 1;
+      const int64_t z1 = z / a.z2, z2 = z % a.z2;
+      if (et < GN) {  // this tile's column offsets (the previous user of cN[acc] finished two tiles ago)
+        const int64_t col = n0 + et;
+        cN[acc * GN + et] = col < a.N ? side_offset(a.n, col, true) : -1;
       }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      const int64_t row = m0 + lrow;
+      const bool rvalid = row < a.M;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * GN + ((q * 32) << 16);
+      const int64_t* cn_t = cN + acc * GN;
+      if (a.splits > 1) {  // fp32 partial of this K range -> dense scratch (finalize_kernel)
+        float* accp = a.acc32 + (z * a.M + row) * a.N + n0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < GN; c0 += 16) {
+          float v[16];
+          tmem_ld16(d + c0, v);
+          if (!rvalid) continue;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int64_t cn = cN[c0 + e];
-        if (cn < 0) continue;
-        if (a.c_f32) {
-          float* p = static_cast<float*>(a.C) + coff + cn;
-          *p = a.accumulate ? *p + v[e] : v[e];
-        } else {
-          c16[cn] = __float2bfloat16_rn(v[e]);
+          for (int e = 0; e < 16; ++e)
+            if (n0 + c0 + e < a.N) atomicAdd(accp + c0 + e, v[e]);
+        }
+      } else {
+        const int64_t coff = z1 * a.zc1 + z2 * a.zc2 + (rvalid ? side_offset(a.m, row, true) : 0);
+        const bool full_n = n0 + GN <= a.N;
+        __nv_bfloat16* c16 = static_cast<__nv_bfloat16*>(a.C) + coff;
+#pragma unroll 1
+        for (int c0 = 0; c0 < GN; c0 += 16) {
+          float v[16];
+          tmem_ld16(d + c0, v);
+          if (!rvalid) continue;
+          if (!a.c_f32 && full_n) {  // bf16 intermediate / output, no column tail
+            const int64_t cb = cn_t[c0];
+            if (cn_t[c0 + 15] - cb == 15 && ((coff + cb) & 7) == 0 &&
+                !(reinterpret_cast<uintptr_t>(a.C) & 15)) {
+              // 16 output-contiguous columns (the thread's row runs along y): two 16-byte stores
+              uint4 p0, p1;
+              p0.x = pack_bf16x2(v[0], v[1]);
+              p0.y = pack_bf16x2(v[2], v[3]);
+              p0.z = pack_bf16x2(v[4], v[5]);
+              p0.w = pack_bf16x2(v[6], v[7]);
+              p1.x = pack_bf16x2(v[8], v[9]);
+              p1.y = pack_bf16x2(v[10], v[11]);
+              p1.z = pack_bf16x2(v[12], v[13]);
+              p1.w = pack_bf16x2(v[14], v[15]);
+              uint4* dst = reinterpret_cast<uint4*>(c16 + cb);
+              dst[0] = p0;
+              dst[1] = p1;
+              continue;
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) c16[cn_t[c0 + e]] = __float2bfloat16_rn(v[e]);
+            continue;
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int64_t cn = cn_t[c0 + e];
+            if (cn < 0) continue;
+            if (a.c_f32) {
+              float* p = static_cast<float*>(a.C) + coff + cn;
+              *p = a.accumulate ? *p + v[e] : v[e];
+            } else {
+              c16[cn] = __float2bfloat16_rn(v[e]);
+            }
+          }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&tempty[acc]);
     }
   }
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<GN>(tmem);
+  if (warp == 0) tmem_dealloc<2 * GN>(tmem);
 }
 
 }  // namespace
 
-size_t tc_generic_smem() { return 1024 + 2 * (GA_STAGE + GB_STAGE) + GN * sizeof(int64_t) + 64; }
+size_t tc_generic_smem() { return 1024 + 2 * (GA_STAGE + GB_STAGE) + 2 * GN * sizeof(int64_t) + 64; }
 
 int launch_tc_generic(const TcgArgs& a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return 0;
   const int64_t tm = (a.M + GM - 1) / GM, tn = (a.N + GN - 1) / GN, zz = a.z1 * a.z2;
-  if (tm > 0x7fffffff || tn > 65535 || zz > 65535 || zz < 1 || a.M >= (1ll << 31) || a.N >= (1ll << 31))
+  if (tm > 0x7fffffff || tn > 0x7fffffff || zz < 1 || a.M >= (1ll << 31) || a.N >= (1ll << 31))
     return (int)cudaErrorInvalidValue;
   static AttrOnce attr;
   int attr_dev = 0;
@@ -272,12 +328,9 @@ int launch_tc_generic(const TcgArgs& a, cudaStream_t st) {
     b.cps = (nk + want - 1) / want;
     b.splits = (nk + b.cps - 1) / b.cps;
   }
-  if (zz * b.splits > 65535) {
-    b.splits = 1;
-    b.cps = nk;
-  }
-  cudaError_t e = launch_pdl(tc_generic_kernel, dim3((unsigned)tm, (unsigned)tn, (unsigned)(zz * b.splits)), dim3(GT),
-                             tc_generic_smem(), st, b);
+  const int64_t work = tiles * b.splits;
+  const unsigned grid = (unsigned)std::min<int64_t>(work, 2 * 148);  // two persistent CTAs per SM
+  cudaError_t e = launch_pdl(tc_generic_kernel, dim3(grid), dim3(GT_ALL), tc_generic_smem(), st, b, (int)tm, (int)tn);
   if (e != cudaSuccess || b.splits == 1) return (int)e;
   const int64_t total = zz * a.M * a.N;
   return (int)launch_pdl(finalize_kernel, dim3((unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8)), dim3(256),
