@@ -299,7 +299,10 @@ int launch_tc_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtens
                         int bn, int splits, cudaStream_t st) {
   switch (bn) {
     case 128:
-      return (args.ss_in || args.ss_fused) ? launch_pair<128, 6, true>(a, b, c, args, splits, st) : launch_pair<128, 6, false>(a, b, c, args, splits, st);
+#ifndef PAIR128_STAGES
+#define PAIR128_STAGES 7  // 7 x 24 KB ring: the N-split first steps (q 64.0, o 66.2 us)
+#endif
+      return (args.ss_in || args.ss_fused) ? launch_pair<128, PAIR128_STAGES, true>(a, b, c, args, splits, st) : launch_pair<128, PAIR128_STAGES, false>(a, b, c, args, splits, st);
     case 256:
       return (args.ss_in || args.ss_fused) ? launch_pair<256, 5, true>(a, b, c, args, splits, st) : launch_pair<256, 5, false>(a, b, c, args, splits, st);
     default:

@@ -1720,7 +1720,10 @@ static tnl_status tc_step_p(tnl_plan* P, const void* X, int64_t ldx, const void*
   // CTA pairs (M=256 MMAs, each CTA streams half of the weight tile) once there are two token
   // tiles and a wide enough weight tile; TNL_PAIR_GEMM=0 disables
   static const bool pair_env = !(getenv("TNL_PAIR_GEMM") && atoi(getenv("TNL_PAIR_GEMM")) == 0);
-  if (pair_env && M >= 256 && bn == 256) {
+  // 128-wide weight tiles (the N-split halves of the rank-256 first steps) too: half the weight
+  // bytes per CTA, a 7-deep ring (q 66.7 -> 64.0 us, o 70.4 -> 66.2 us; TNL_PAIR128=0 disables)
+  static const bool pair128_env = !(getenv("TNL_PAIR128") && atoi(getenv("TNL_PAIR128")) == 0);
+  if (pair_env && M >= 256 && (bn == 256 || (pair128_env && bn == 128 && !out_f32))) {
     CUtensorMap tbh;
     if ((err = get_tmap(P, &tbh, W, K, N, ldw, bn / 2)))
       return fail(TNL_ERR_CUDA, "tensor map (pair step) failed: %d", err);
