@@ -323,6 +323,22 @@ def ncu_graph_step_bytes():
         return None, "no graph-level ncu capture committed"
 
 
+def capture_steps(step, n, torch):
+    """n calls of `step` captured in one CUDA graph (after one eager warm call on the capture stream), so
+    per-call timings of host-driven paths are free of host launch jitter."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(n):
+            step()
+    return g
+
+
 def time_graph(replay, steps, warmup, torch, dist=None):
     for _ in range(warmup):
         replay()
@@ -621,7 +637,9 @@ def main():
                 pl.forward(xs[it[0] % 4], out=yp, ws=wsp)
                 it[0] += 1
 
-            ms_p = time_graph(pre_step, 20, 3, torch, None)
+            g_p = capture_steps(pre_step, 4, torch)  # one replay = 4 forwards over the 4 inputs
+            ms_p = time_graph(g_p.replay, 5, 1, torch, None) / 4
+            del g_p
             byts = 2 * (tnl.param_count(lay) + Mp * (rows_ + cols_))
             prefill[which] = {"layer": f"TT r64 {ms_}", "M": Mp, "ms": ms_p, "tokens_per_s": Mp / (ms_p / 1e3),
                               "alg_GBps": byts / (ms_p / 1e3) / 1e9, "frac_hbm": byts / (ms_p / 1e3) / 1e9 / hbm,
@@ -643,7 +661,9 @@ def main():
             blk.forward(xs[it[0] % 4], out=yp, ws=wsp)
             it[0] += 1
 
-        ms_b = time_graph(mlp_step, 20, 3, torch, None)
+        g_b = capture_steps(mlp_step, 4, torch)
+        ms_b = time_graph(g_b.replay, 5, 1, torch, None) / 4
+        del g_b
         P3 = sum(tnl.param_count(l_) for l_ in (g_, u_, d_))
         b_bytes = 2 * (P3 + Mp * (5120 + 5120))
         b_flops = Mp * sum(l_.chain_flops_per_token() for l_ in (g_, u_, d_))
