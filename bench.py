@@ -683,8 +683,8 @@ def main():
         del xs, yp
 
     # secondary (cfg5, N > 1 only): prefill of the cfg3 gate projection sharded over the ranks —
-    # output-mode sharded (each rank owns 25600/N rows of the leading output mode, one NCCL
-    # all-gather over NVLink assembles y) and token-sharded (no collective); max over ranks
+    # output-mode sharded (each rank owns 25600/N rows of the leading output mode and stores them into
+    # every peer's symmetric-memory y over NVLink) and token-sharded (no collective); max over ranks
     sharded = None
     if world > 1 and not args.no_prefill:
         try:
@@ -702,8 +702,11 @@ def main():
             sharded = {"layer": f"TT r64 {ms_}", "M": Mp, "world": world,
                        "output_sharded": {"ms": ms_o, "tokens_per_s": Mp / (ms_o / 1e3),
                                           "allgather_bytes_per_rank": 2 * Mp * 25600 // world,
-                                          "how": "row-restricted plan per rank + all_gather_into_tensor (NCCL) + "
-                                                 "[G][M][rows/G] -> (M, rows) placement; max over ranks"},
+                                          "how": "row-restricted plan per rank storing its slice of i0 straight into "
+                                                 "its columns of y (strided TMA store); NCCL groups: y in symmetric "
+                                                 "memory, P2P stores of the slice into every peer's y + one device "
+                                                 "barrier (no gather buffer, no permute); max over ranks; eager "
+                                                 "(host-driven exchange), not a graph replay"},
                        "token_sharded": {"ms": ms_t, "tokens_per_s": Mp / (ms_t / 1e3),
                                          "how": "M/N tokens per rank, full weights, no collective; max over ranks"}}
         except Exception as exc:  # report, never fail the headline run
