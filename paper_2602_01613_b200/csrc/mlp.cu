@@ -87,7 +87,11 @@ __device__ __forceinline__ float silu(float g) {
 __device__ __forceinline__ float silu_mul(float g, float u) {
   const float a = 0.5f * g;
   float t;
+#ifdef TNL_DIAG_NOTANH  // timing diagnostic only (wrong SiLU): no MUFU op
+  t = fminf(fmaxf(a, -1.f), 1.f);
+#else
   asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(a));
+#endif
   const float b = a * u;
   return fmaf(b, t, b);
 }

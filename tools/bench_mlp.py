@@ -12,13 +12,19 @@ layers = [S.make_layer(*S.CFG3_GATE, seed=30_100), S.make_layer(*S.CFG3_GATE, se
 xs = [torch.randn(M, 5120, device="cuda").to(torch.bfloat16) for _ in range(4)]
 
 def timeit(fn, iters=20):
+    # CUDA-graph replays of 4 calls (eager Python loops pick up host launch jitter)
     for i in range(3): fn(i)
     torch.cuda.synchronize()
+    s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(4): fn(i)
+    g.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for i in range(iters): fn(i)
+    for _ in range(iters // 4): g.replay()
     e1.record(); torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / iters
+    return e0.elapsed_time(e1) / (4 * (iters // 4))
 
 P = sum(tnl.param_count(l) for l in layers)
 F = sum(l.chain_flops_per_token() for l in layers) * M
