@@ -289,8 +289,11 @@ class ClockSampler:
 
 def ncu_traffic():
     """DRAM bytes per launch of the dominant kernel (dec_fused_kernel) from the committed
-    `ncu --set full` capture (profiles/r01/ncu_dec_fused.json); (None, reason) if absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_dec_fused.json")
+    `ncu --set full` capture (profiles/r02/ncu_dec_fused.json, tools/ncu_dec_summary.py); (None, reason) if absent."""
+    here = os.path.dirname(os.path.abspath(__file__))
+    path = os.path.join(here, "profiles", "r02", "ncu_dec_fused.json")  # HEAD build (r01: the first capture)
+    if not os.path.exists(path):
+        path = os.path.join(here, "profiles", "r01", "ncu_dec_fused.json")
     try:
         with open(path) as f:
             d = json.load(f)
