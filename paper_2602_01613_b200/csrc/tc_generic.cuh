@@ -29,7 +29,8 @@ struct TcgArgs {
   int64_t z1, z2;  // batch (grid.z = z1 * z2) and its strides
   int64_t za1, za2, zb1, zb2, zc1, zc2;
   // split-K (set by launch_tc_generic when the step has few output tiles and a long K): fp32
-  // partials into acc32 (dense [z][M][N], zero at rest; >= z1*z2*M*N floats), then one pass to C
+  // partials into acc32 (dense [z][M][N], zero at rest; >= z1*z2*M*N floats, which is below
+  // 74 * 128 * 64 whenever a step splits), then one pass to C
   float* acc32;
   int32_t splits, cps;
 };

@@ -1499,7 +1499,8 @@ static size_t ws_layout(const tnl_plan* P, int64_t M, size_t* o_f32, size_t* o_b
   if (P->tcg_out || P->tcg_full) {  // the bf16 chain's two intermediate states + split-K scratch
     const size_t s0 = take(2 * M * P->max_state);
     take(2 * M * P->max_state);
-    take(4 * M * std::max<int64_t>(P->max_state, std::max(P->rows, P->r_pad)));  // zero at rest
+    // split-K scratch (zero at rest): a step splits K only below 74 output tiles of 128 x 64
+    take(4 * std::min<int64_t>(M * std::max<int64_t>(P->max_state, std::max(P->rows, P->r_pad)), 74 * 128 * 64));
     if (o_s) *o_s = s0;
   }
   return bytes;
