@@ -103,3 +103,39 @@ def test_random_shape_all_plans(k):
             torch.cuda.synchronize()
             e = rel(O.forward_torch_orient(ref32, x), y.double().cpu().numpy())
             assert e <= 1e-5, (spec, flags, m, p.info["plan_large_name"], e)
+
+
+SHARD_SPECS = random_specs(24, seed=90_777)
+
+
+@pytest.mark.parametrize("k", range(len(SHARD_SPECS)),
+                         ids=[f"{s[0]}-{'x'.join(map(str, s[1]))}-rm{s[2]}" for s in SHARD_SPECS])
+def test_random_row_ranges_match_full_plan(k):
+    """Row-restricted plans (tnl_plan_create_rows, the output-mode sharding building block) at random
+    cut points: concatenated shard outputs equal the full plan's rows (bf16 and fp32, decode and
+    prefill token counts)."""
+    spec = SHARD_SPECS[k]
+    L = O.synthetic_layer(*spec, seed=95_000 + k)
+    rows, cols = L.matrix_shape
+    if rows < 3:
+        pytest.skip("fewer than three output rows")
+    rng = np.random.default_rng(95_100 + k)
+    cuts = sorted(set(int(c) for c in rng.integers(1, rows, size=2)))
+    bounds = [0] + cuts + [rows]
+    for dtype, tol in ((torch.bfloat16, 1e-2), (torch.float32, 1e-6)):
+        f = O.round_bf16 if dtype == torch.bfloat16 else (lambda a: np.asarray(a, np.float32))
+        kw = dict(family=L.family, mode_shape=L.mode_shape, row_mode_count=L.row_mode_count)
+        if L.family == "tucker":
+            kw.update(core=f(L.core), factors=[f(u) for u in L.factors])
+        else:
+            kw.update(cores=[f(c) for c in L.cores])
+        layer = tnl.CompressedLayer(**kw)
+        for m in (3, 150):
+            x = torch.tensor(f(O.synthetic_x(m, cols, seed=95_200 + m)), dtype=dtype, device=DEV)
+            full = layer.plan(dtype).forward(x).float()
+            parts = [layer.plan(dtype, row_range=(lo, hi)).forward(x).float() for lo, hi in zip(bounds, bounds[1:])]
+            torch.cuda.synchronize()
+            cat = torch.cat(parts, dim=1)
+            assert cat.shape == full.shape
+            d = float((cat - full).norm() / full.norm().clamp_min(1e-30))
+            assert d <= tol, (spec, dtype, m, bounds, d)
