@@ -621,16 +621,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP_PAIR_THREADS, 1)
   uint64_t* gu_empty = bars + 29;  // [3]  leader: G/U pair loaded by both CTAs' epilogues (8 warps)
   uint64_t* h_full = bars + 32;    // [3]  leader: h chunk written in both CTAs (8 warps)
   uint64_t* h_empty = bars + 35;   // [3]  per CTA (multicast commit of the D MMA)
-  uint64_t* td_done = bars + 38;   //      per CTA (multicast commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 39);
+  uint64_t* td_done = bars + 38;   //      per CTA (multicast commit): an item's T_d complete
+  uint64_t* t_copied = bars + 39;  //      per CTA: the item's T read out of sT by the 8 epilogue warps
+  uint64_t* t_free = bars + 40;    //      per CTA (multicast commit): the item's G/U MMAs done (TMEM T free)
+  uint64_t* td_empty = bars + 41;  //      leader: both CTAs' epilogues read the item's T_d (16 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
 
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  const int tile = blockIdx.x;
   const int total_ch = a.inter / CH;
-  const int c0 = blockIdx.y * a.chunks_per_slice;
-  const int nch = min(total_ch, c0 + a.chunks_per_slice) - c0;
   const uint32_t warp = warp_id();
+  // Work of this CTA pair: a contiguous range of the (token-pair tile, 64-column chunk) sequence.
+  // Slice mode: one token pair, chunk slice blockIdx.y. Balanced mode (a.per_pair > 0): per_pair
+  // chunk-units from the flattened sequence, split into items at token-pair boundaries, so every
+  // pair of the grid (74 on 148 SMs) does the same amount of work whatever the token count.
+  const int pair_id = blockIdx.x >> 1;
+  int64_t w_beg, w_end;
+  if (a.per_pair > 0) {
+    w_beg = (int64_t)pair_id * a.per_pair;
+    w_end = min((int64_t)a.tiles2 * total_ch, w_beg + a.per_pair);
+  } else {
+    w_beg = (int64_t)pair_id * total_ch + (int64_t)blockIdx.y * a.chunks_per_slice;
+    w_end = min((int64_t)(pair_id + 1) * total_ch, w_beg + a.chunks_per_slice);
+  }
+  auto next_item = [&](int64_t& w, int& tile, int& c0, int& nch) -> bool {
+    if (w >= w_end) return false;
+    const int tp = (int)(w / total_ch);
+    c0 = (int)(w % total_ch);
+    nch = (int)min(w_end - w, (int64_t)(total_ch - c0));
+    tile = 2 * tp + (int)rank;  // this CTA's 128-token tile of the pair
+    w += nch;
+    return true;
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmT);
@@ -650,6 +672,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP_PAIR_THREADS, 1)
       mbar_init(&h_empty[b], 1);
     }
     mbar_init(td_done, 1);
+    mbar_init(t_copied, 8);
+    mbar_init(t_free, 1);
+    mbar_init(td_empty, 16);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
@@ -661,63 +686,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP_PAIR_THREADS, 1)
   const uint32_t tT = tmem + L.t_col, tTD = tmem + L.td_col;
   pdl_launch_dependents();
 
-  if (nch > 0) {
+  if (w_beg < w_end) {
     if (warp == 0) {
       if (elect_one()) {
         Ring r;
         const int wrow = (int)rank * 32, drow = (int)rank * (a.rd / 2);
-        auto load_stage = [&](int i) {
+        int gi = 0;  // weight stages issued
+        auto load_stage = [&](int chunk) {
           const int s = r.idx;
+          if (gi >= S) mbar_wait(&empty[s], r.ph ^ 1);
           uint8_t* st = sR + (size_t)s * L.stage;
-          const int col = (c0 + i) * CH;
+          const int col = chunk * CH;
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * L.stage_tx);
           for (int k = 0; k < L.kg; ++k) tma_load_2d_pair(st + L.ag_off + k * HBLK, &tmAg, &full[s], k * 64, col + wrow);
           for (int k = 0; k < L.ku; ++k) tma_load_2d_pair(st + L.au_off + k * HBLK, &tmAu, &full[s], k * 64, col + wrow);
           tma_load_2d_pair(st + L.bd_off, &tmBd, &full[s], col, drow);
           r.next(S);
+          ++gi;
         };
-        const int npre = min(nch, S);
-        for (int i = 0; i < npre; ++i) load_stage(i);  // weights: before the dependency wait
-        pdl_wait();
-        mbar_arrive_expect_tx(tfull, (uint32_t)((L.kg + L.ku) * TBLK));
-        for (int k = 0; k < L.kg + L.ku; ++k) tma_load_2d(sT + k * TBLK, &tmT, tfull, k * 64, tile * 128);
-        for (int i = npre; i < nch; ++i) {
-          mbar_wait(&empty[r.idx], r.ph ^ 1);
-          load_stage(i);
+        int64_t w = w_beg;
+        int tile, c0, nch, k = 0;
+        while (next_item(w, tile, c0, nch)) {
+          int i = 0;
+          if (k == 0) {
+            for (; i < min(nch, S); ++i) load_stage(c0 + i);  // weights: before the dependency wait
+            pdl_wait();
+          } else {
+            mbar_wait(t_copied, (k - 1) & 1);  // the previous item's T has left sT
+          }
+          mbar_arrive_expect_tx(tfull, (uint32_t)((L.kg + L.ku) * TBLK));
+          for (int kb = 0; kb < L.kg + L.ku; ++kb) tma_load_2d(sT + kb * TBLK, &tmT, tfull, kb * 64, tile * 128);
+          for (; i < nch; ++i) load_stage(c0 + i);
+          ++k;
         }
       }
     } else if (warp == 1) {
       // G/U issuer: G_i = T_g A_g[chunk i]^T, U_i = T_u A_u[chunk i]^T into TMEM pair i % NB
       if (leader && elect_one()) {
         const uint32_t idesc_gu = idesc_bf16_f32(256, CH);
-        unsigned long long* tr = (a.trace && blockIdx.x == 0 && blockIdx.y == 0) ? a.trace : nullptr;
-        mbar_wait(t_tmem, 0);
-        tc_fence_after();
         Ring rf, rb;
-        for (int i = 0; i < nch; ++i) {
-          const int s = rf.idx, b = rb.idx;
-          mbar_wait(&full[s], rf.ph);
-          if (tr && i < 256) tr[i * 4 + 0] = globaltimer();
-          if (i >= NB) mbar_wait(&gu_empty[b], rb.ph ^ 1);
-          rf.next(S);
-          rb.next(NB);
+        int gi = 0;
+        int64_t w = w_beg;
+        int tile, c0, nch, k = 0;
+        while (next_item(w, tile, c0, nch)) {
+          mbar_wait(t_tmem, k & 1);
           tc_fence_after();
-          uint8_t* st = sR + (size_t)s * L.stage;
-          const uint32_t tG = tmem + b * 128, tU = tG + 64;
-          for (int k = 0; k < L.kg; ++k) {
-            const uint64_t bd = smem_desc_sw128(smem_u32(st + L.ag_off + k * HBLK));
+          for (int i = 0; i < nch; ++i, ++gi) {
+            const int s = rf.idx, b = rb.idx;
+            mbar_wait(&full[s], rf.ph);
+            if (gi >= NB) mbar_wait(&gu_empty[b], rb.ph ^ 1);
+            rf.next(S);
+            rb.next(NB);
+            tc_fence_after();
+            uint8_t* st = sR + (size_t)s * L.stage;
+            const uint32_t tG = tmem + b * 128, tU = tG + 64;
+            for (int kk = 0; kk < L.kg; ++kk) {
+              const uint64_t bd = smem_desc_sw128(smem_u32(st + L.ag_off + kk * HBLK));
 #pragma unroll
-            for (int q = 0; q < 4; ++q) mma_bf16_ts_pair(tG, tT + k * 32 + q * 8, bd + 2 * q, idesc_gu, (k | q) != 0);
-          }
-          for (int k = 0; k < L.ku; ++k) {
-            const uint64_t bd = smem_desc_sw128(smem_u32(st + L.au_off + k * HBLK));
+              for (int q = 0; q < 4; ++q) mma_bf16_ts_pair(tG, tT + kk * 32 + q * 8, bd + 2 * q, idesc_gu, (kk | q) != 0);
+            }
+            for (int kk = 0; kk < L.ku; ++kk) {
+              const uint64_t bd = smem_desc_sw128(smem_u32(st + L.au_off + kk * HBLK));
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              mma_bf16_ts_pair(tU, tT + (L.kg + k) * 32 + q * 8, bd + 2 * q, idesc_gu, (k | q) != 0);
+              for (int q = 0; q < 4; ++q)
+                mma_bf16_ts_pair(tU, tT + (L.kg + kk) * 32 + q * 8, bd + 2 * q, idesc_gu, (kk | q) != 0);
+            }
+            mma_commit_pair(&gu_full[b], 3);
+            mma_commit_pair(&empty[s], 3);
           }
-          mma_commit_pair(&gu_full[b], 3);
-          mma_commit_pair(&empty[s], 3);
-          if (tr && i < 256) tr[i * 4 + 1] = globaltimer();
+          mma_commit_pair(t_free, 3);  // every G/U MMA of this item has read the TMEM T tile
+          ++k;
         }
       }
       __syncwarp();
@@ -727,102 +765,123 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP_PAIR_THREADS, 1)
       if (leader && elect_one()) {
         const uint32_t idesc_d = idesc_bf16_f32(256, a.rd);
         Ring rf, rh;
-        for (int j = 0; j < nch; ++j) {
-          const int s = rf.idx, hb = rh.idx;
-          mbar_wait(&full[s], rf.ph);
-          mbar_wait(&h_full[hb], rh.ph);
-          rf.next(S);
-          rh.next(NH);
+        int64_t w = w_beg;
+        int tile, c0, nch, k = 0;
+        while (next_item(w, tile, c0, nch)) {
+          if (k > 0) mbar_wait_cluster(td_empty, (k - 1) & 1);  // previous item's T_d read out
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw128(smem_u32(sH + hb * TBLK));
-          const uint64_t bd = smem_desc_sw128(smem_u32(sR + (size_t)s * L.stage + L.bd_off));
+          for (int j = 0; j < nch; ++j) {
+            const int s = rf.idx, hb = rh.idx;
+            mbar_wait(&full[s], rf.ph);
+            mbar_wait(&h_full[hb], rh.ph);
+            rf.next(S);
+            rh.next(NH);
+            tc_fence_after();
+            const uint64_t ad = smem_desc_sw128(smem_u32(sH + hb * TBLK));
+            const uint64_t bd = smem_desc_sw128(smem_u32(sR + (size_t)s * L.stage + L.bd_off));
 #pragma unroll
-          for (int k = 0; k < 4; ++k) mma_bf16_ss_pair(tTD, ad + 2 * k, bd + 2 * k, idesc_d, (j > 0 || k > 0) ? 1u : 0u);
-          mma_commit_pair(&h_empty[hb], 3);
-          mma_commit_pair(&empty[s], 3);
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss_pair(tTD, ad + 2 * kk, bd + 2 * kk, idesc_d, (j > 0 || kk > 0) ? 1u : 0u);
+            mma_commit_pair(&h_empty[hb], 3);
+            mma_commit_pair(&empty[s], 3);
+          }
+          mma_commit_pair(td_done, 3);
+          ++k;
         }
-        mma_commit_pair(td_done, 3);
       }
       __syncwarp();
     } else {
       const uint32_t q = warp & 3, hh = (warp - 2) >> 2;
       const int lrow = q * 32 + lane_id();
       const uint32_t lane_base = (q * 32) << 16;
-      // T tile: smem (SW128, k-blocks of 64) -> TMEM (packed bf16 pairs, 32 columns per k-block)
-      mbar_wait(tfull, 0);
-      for (int kb = hh; kb < L.kg + L.ku; kb += 2) {
-        const uint8_t* rowp = sT + kb * TBLK + (lrow >> 3) * 1024 + (lrow & 7) * 128;
-        uint32_t r[32];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 v = lds128(smem_u32(rowp) + ((c ^ (lrow & 7)) << 4));
-          r[4 * c] = v.x;
-          r[4 * c + 1] = v.y;
-          r[4 * c + 2] = v.z;
-          r[4 * c + 3] = v.w;
-        }
-        tmem_st32(tT + lane_base + kb * 32, r);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive_remote(mapa_shared(t_tmem, 0));
-      unsigned long long* tr =
-          (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (warp == 2 || warp == 6) && lane_id() == 0) ? a.trace : nullptr;
-      // the two epilogue warps of a lane quarter take alternate chunks (all 64 columns each)
+      // the two epilogue warps of a lane quarter take alternate chunks of the CTA's chunk sequence
       Ring eb, ehb;
       eb.idx = hh;
       ehb.idx = hh;
-      for (int i = hh; i < nch; i += 2) {
-        const int b = eb.idx, hb = ehb.idx;
-        const uint32_t hph = ehb.ph;
-        mbar_wait(&gu_full[b], eb.ph);
-        eb.next2(NB);
-        ehb.next2(NH);
-        tc_fence_after();
-        if (tr && i < 256) tr[i * 4 + 2] = globaltimer();
-        const uint32_t tG = tmem + b * 128 + lane_base, tU = tG + 64;
-        uint32_t gr[64], ur[64];
-        tmem_ld32_nowait(tG, gr);
-        tmem_ld32_nowait(tU, ur);
-        tmem_ld32_nowait(tG + 32, gr + 32);
-        tmem_ld32_nowait(tU + 32, ur + 32);
-        tmem_wait_ld();
+      int g = 0;  // chunks of previous items
+      int64_t w = w_beg;
+      int tile, c0, nch, k = 0;
+      while (next_item(w, tile, c0, nch)) {
+        // T tile: smem (SW128, k-blocks of 64) -> TMEM (packed bf16 pairs, 32 columns per k-block)
+        mbar_wait(tfull, k & 1);
+        if (k > 0) mbar_wait(t_free, (k - 1) & 1);  // the previous item's G/U MMAs no longer read TMEM T
+        for (int kb = hh; kb < L.kg + L.ku; kb += 2) {
+          const uint8_t* rowp = sT + kb * TBLK + (lrow >> 3) * 1024 + (lrow & 7) * 128;
+          uint32_t r[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = lds128(smem_u32(rowp) + ((c ^ (lrow & 7)) << 4));
+            r[4 * c] = v.x;
+            r[4 * c + 1] = v.y;
+            r[4 * c + 2] = v.z;
+            r[4 * c + 3] = v.w;
+          }
+          tmem_st32(tT + lane_base + kb * 32, r);
+        }
+        tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane_id() == 0) mbar_arrive_remote(mapa_shared(&gu_empty[b], 0));  // pair b reusable
-        if (i >= NH) mbar_wait(&h_empty[hb], hph ^ 1);
-        uint8_t* rowp = sH + hb * TBLK + (lrow >> 3) * 1024 + (lrow & 7) * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 p;
-          p.x = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 0]), __uint_as_float(ur[8 * c + 0])),
-                            silu_mul(__uint_as_float(gr[8 * c + 1]), __uint_as_float(ur[8 * c + 1])));
-          p.y = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 2]), __uint_as_float(ur[8 * c + 2])),
-                            silu_mul(__uint_as_float(gr[8 * c + 3]), __uint_as_float(ur[8 * c + 3])));
-          p.z = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 4]), __uint_as_float(ur[8 * c + 4])),
-                            silu_mul(__uint_as_float(gr[8 * c + 5]), __uint_as_float(ur[8 * c + 5])));
-          p.w = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 6]), __uint_as_float(ur[8 * c + 6])),
-                            silu_mul(__uint_as_float(gr[8 * c + 7]), __uint_as_float(ur[8 * c + 7])));
-          sts128(smem_u32(rowp) + ((c ^ (lrow & 7)) << 4), p);
+        if (lane_id() == 0) {
+          mbar_arrive_remote(mapa_shared(t_tmem, 0));
+          mbar_arrive(t_copied);
         }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane_id() == 0) mbar_arrive_remote(mapa_shared(&h_full[hb], 0));
-        if (tr && i < 256) tr[i * 4 + 3] = globaltimer();
-      }
-      mbar_wait(td_done, 0);
-      tc_fence_after();
-      const int m = tile * 128 + lrow;
-      const int half = a.rd / 2;
-#pragma unroll 1
-      for (int c = hh * half; c < hh * half + half; c += 16) {
-        float v[16];
-        tmem_ld16(tTD + lane_base + c, v);
-        if (m >= a.M) continue;
-        float* o = a.td + (int64_t)m * a.ld_td + c;
+        for (int i = (int)((hh + g) & 1); i < nch; i += 2) {  // global chunk g + i has parity hh
+          const int gg = g + i;
+          const int b = eb.idx, hb = ehb.idx;
+          const uint32_t hph = ehb.ph;
+          mbar_wait(&gu_full[b], eb.ph);
+          eb.next2(NB);
+          ehb.next2(NH);
+          tc_fence_after();
+          const uint32_t tG = tmem + b * 128 + lane_base, tU = tG + 64;
+          uint32_t gr[64], ur[64];
+          tmem_ld32_nowait(tG, gr);
+          tmem_ld32_nowait(tU, ur);
+          tmem_ld32_nowait(tG + 32, gr + 32);
+          tmem_ld32_nowait(tU + 32, ur + 32);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive_remote(mapa_shared(&gu_empty[b], 0));  // pair b reusable
+          if (gg >= NH) mbar_wait(&h_empty[hb], hph ^ 1);
+          uint8_t* rowp = sH + hb * TBLK + (lrow >> 3) * 1024 + (lrow & 7) * 128;
 #pragma unroll
-        for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+          for (int c = 0; c < 8; ++c) {
+            uint4 p;
+            p.x = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 0]), __uint_as_float(ur[8 * c + 0])),
+                              silu_mul(__uint_as_float(gr[8 * c + 1]), __uint_as_float(ur[8 * c + 1])));
+            p.y = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 2]), __uint_as_float(ur[8 * c + 2])),
+                              silu_mul(__uint_as_float(gr[8 * c + 3]), __uint_as_float(ur[8 * c + 3])));
+            p.z = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 4]), __uint_as_float(ur[8 * c + 4])),
+                              silu_mul(__uint_as_float(gr[8 * c + 5]), __uint_as_float(ur[8 * c + 5])));
+            p.w = pack_bf16x2(silu_mul(__uint_as_float(gr[8 * c + 6]), __uint_as_float(ur[8 * c + 6])),
+                              silu_mul(__uint_as_float(gr[8 * c + 7]), __uint_as_float(ur[8 * c + 7])));
+            sts128(smem_u32(rowp) + ((c ^ (lrow & 7)) << 4), p);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive_remote(mapa_shared(&h_full[hb], 0));
+        }
+        g += nch;
+        // this item's T_d partial (the 128 rows of `tile`) -> fp32 reductions; then hand the TMEM
+        // accumulator back to the D issuer for the next item
+        mbar_wait(td_done, k & 1);
+        tc_fence_after();
+        const int m = tile * 128 + lrow;
+        const int half = a.rd / 2;
+#pragma unroll 1
+        for (int c = hh * half; c < hh * half + half; c += 16) {
+          float v[16];
+          tmem_ld16(tTD + lane_base + c, v);
+          if (m >= a.M) continue;
+          float* o = a.td + (int64_t)m * a.ld_td + c;
+#pragma unroll
+          for (int e = 0; e < 16; e += 4) red_add_v4(o + e, v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive_remote(mapa_shared(td_empty, 0));
+        ++k;
       }
     }
   }
@@ -898,7 +957,10 @@ int launch_mlp_mid_pair(const CUtensorMap& t, const CUtensorMap& ag, const CUten
   }
   const int tiles = (a.M + 127) / 128;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((tiles + 1) / 2 * 2, slices, 1);
+  // balanced mode: a.per_pair chunk-units per CTA pair over the flattened (token pair, chunk) sequence
+  const int64_t work = (int64_t)((tiles + 1) / 2) * (a.inter / CH);
+  cfg.gridDim = a.per_pair > 0 ? dim3((unsigned)(2 * ((work + a.per_pair - 1) / a.per_pair)), 1, 1)
+                               : dim3((tiles + 1) / 2 * 2, slices, 1);
   cfg.blockDim = dim3(MLP_PAIR_THREADS, 1, 1);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = st;

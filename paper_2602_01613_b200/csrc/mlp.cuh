@@ -13,6 +13,9 @@ struct MlpArgs {
   int32_t inter;       // intermediate width (gate/up rows == down cols), multiple of 64
   int32_t rg, ru, rd;  // padded cut ranks (multiples of 64; rg, ru <= 128, rd <= 256)
   int32_t chunks_per_slice;
+  int32_t tiles2;      // CTA-pair kernel: token-pair tiles ((M/128 + 1) / 2)
+  int64_t per_pair;    // CTA-pair kernel, balanced mode (> 0): chunk-units per pair of the flattened
+                       // (token pair, chunk) sequence; 0: slice mode (chunks_per_slice, grid.y slices)
   float* td;           // fp32 [M][ld_td] partial-sum target (zeroed by the caller)
   int64_t ld_td;
   unsigned long long* trace;  // optional: CTA 0 per-chunk %globaltimer stamps [chunk][4]

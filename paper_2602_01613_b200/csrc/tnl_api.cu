@@ -2792,6 +2792,15 @@ static tnl_status mlp_forward_impl(const tnl_mlp* Bc, const void* x, int64_t m, 
   }
   a.chunks_per_slice = (int32_t)((nchunks + slices - 1) / slices);
   slices = (int)((nchunks + a.chunks_per_slice - 1) / a.chunks_per_slice);
+  // CTA pairs, balanced: split the flattened (token pair, chunk) work evenly over 74 pairs (148 SMs)
+  // instead of whole slices per token pair (2 slices of 64 token pairs leave 20 SMs idle at M = 8192)
+  a.tiles2 = (int32_t)(tiles_m / 2);
+  a.per_pair = 0;
+  static const bool balance = !(getenv("TNL_MLP_BALANCE") && atoi(getenv("TNL_MLP_BALANCE")) == 0);
+  if (pair && balance) {
+    const int64_t work = (tiles_m / 2) * nchunks;
+    if (work >= 74 * 32) a.per_pair = (work + 73) / 74;
+  }
   a.td = td32;
   a.ld_td = B->rd;
   a.trace = B->g->trace;
