@@ -57,7 +57,7 @@ __device__ __forceinline__ float silu_mul(float g, float u) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
     dual_silu_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmG,
                      const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
-                     const DualArgs a, int tiles_n, int per) {
+                     const DualArgs a, int tiles_n, int per, int per_pair) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -69,14 +69,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
   uint64_t* tfull = empty + DSTAGES;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]  leader: 4 epilogue warps x 2 CTAs
   uint64_t* tload = tempty + 2;       //      leader: both CTAs' T tiles
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tload + 1);
+  uint64_t* t_free = tload + 1;       //      per CTA (multicast commit): an item's MMAs done, sT reusable
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_free + 1);
 
   const int kg = (a.kg + DBK - 1) / DBK, ku = (a.ku + DBK - 1) / DBK, nkb = kg + ku;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  const int tm = blockIdx.x;
-  const int tn0 = blockIdx.y * per, tn1 = min(tiles_n, tn0 + per);
   const uint32_t warp = warp_id();
+  // Work of this CTA pair: a contiguous range of the flattened (token-pair tile, output tile)
+  // sequence — one token pair's slice [y * per, (y+1) * per) of output tiles, or (balanced,
+  // per_pair > 0) an even share over the whole grid, cut into items at token-pair boundaries
+  // (each item reloads the resident T tile).
+  const int pair_id = blockIdx.x >> 1, tiles2 = (a.M + 2 * DBM - 1) / (2 * DBM);
+  int w_beg, w_end;
+  if (per_pair > 0) {
+    w_beg = pair_id * per_pair;
+    w_end = min(tiles2 * tiles_n, w_beg + per_pair);
+  } else {
+    w_beg = pair_id * tiles_n + blockIdx.y * per;
+    w_end = min((pair_id + 1) * tiles_n, w_beg + per);
+  }
+  auto next_item = [&](int& w, int& tm, int& tn0, int& tn1) -> bool {
+    if (w >= w_end) return false;
+    const int tp = w / tiles_n;
+    tn0 = w % tiles_n;
+    tn1 = min(tiles_n, tn0 + (w_end - w));
+    tm = 2 * tp + (int)rank;
+    w += tn1 - tn0;
+    return true;
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmT);
@@ -92,6 +113,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
       mbar_init(&tempty[b], 16);  // 8 epilogue warps x 2 CTAs
     }
     mbar_init(tload, 1);
+    mbar_init(t_free, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
@@ -114,20 +136,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
         tma_load_2d_pair(sB + s * D_HBLK, up ? &tmU : &tmG, &full[s], (up ? kb - kg : kb) * DBK, tn * DBN + hrow);
         ++it;
       };
-      const int pre = min(DSTAGES, (tn1 - tn0) * nkb);
-      for (int i = 0; i < pre; ++i) load_b(tn0 + i / nkb, i % nkb);  // weights before the wait
-      pdl_wait();
-      if (leader) mbar_arrive_expect_tx(tload, 2 * nkb * D_BLK);
-      for (int kb = 0; kb < nkb; ++kb)
-        tma_load_2d_pair(sT + kb * D_BLK, &tmT, tload, (kb >= kg ? a.u_off + (kb - kg) * DBK : kb * DBK), tm * DBM);
-      for (int i = pre; i < (tn1 - tn0) * nkb; ++i) load_b(tn0 + i / nkb, i % nkb);
+      int w = w_beg, tm, tn0, tn1, k = 0;
+      while (next_item(w, tm, tn0, tn1)) {
+        const int n = (tn1 - tn0) * nkb;
+        const int pre = min(DSTAGES, n);
+        for (int i = 0; i < pre; ++i) load_b(tn0 + i / nkb, i % nkb);  // weights before the T wait
+        if (k == 0)
+          pdl_wait();
+        else
+          mbar_wait(t_free, (k - 1) & 1);  // the previous item's MMAs no longer read sT
+        if (leader) mbar_arrive_expect_tx(tload, 2 * nkb * D_BLK);
+        for (int kb = 0; kb < nkb; ++kb)
+          tma_load_2d_pair(sT + kb * D_BLK, &tmT, tload, (kb >= kg ? a.u_off + (kb - kg) * DBK : kb * DBK), tm * DBM);
+        for (int i = pre; i < n; ++i) load_b(tn0 + i / nkb, i % nkb);
+        ++k;
+      }
     }
   } else if (warp == 1) {
     if (leader && elect_one()) {
       constexpr uint32_t idesc = idesc_bf16_f32(2 * DBM, DBN);
-      mbar_wait(tload, 0);
-      tc_fence_after();
       int it = 0, lt = 0;
+      int w = w_beg, tm, tn0, tn1, k = 0;
+      while (next_item(w, tm, tn0, tn1)) {
+      mbar_wait(tload, k & 1);
+      tc_fence_after();
       for (int tn = tn0; tn < tn1; ++tn, ++lt) {
         const int acc = lt & 1;
         if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
@@ -148,6 +180,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
         }
         mma_commit_pair(&tfull[acc], 3);
       }
+      mma_commit_pair(t_free, 3);  // every MMA of this item has read the resident T tile
+      ++k;
+      }
     }
     __syncwarp();
   } else {
@@ -157,6 +192,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
     const int lrow = q * 32 + lane_id();
     uint8_t* stage = sC + hf * D_CHUNK;
     int lt = 0;
+    int w = w_beg, tm, tn0, tn1;
+    while (next_item(w, tm, tn0, tn1))
     for (int tn = tn0; tn < tn1; ++tn, ++lt) {
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
@@ -239,8 +276,12 @@ int launch_dual_silu(const CUtensorMap& t, const CUtensorMap& g, const CUtensorM
   if (env_slices > 0) slices = env_slices < tiles_n ? env_slices : tiles_n;
   const int per = (tiles_n + slices - 1) / slices;
   slices = (tiles_n + per - 1) / per;
+  // balanced: the flattened (token pair, output tile) work split evenly over 74 CTA pairs
+  static const bool balance = !(getenv("TNL_DUAL_BALANCE") && atoi(getenv("TNL_DUAL_BALANCE")) == 0);  // A/B
+  const int work = tiles_m / 2 * tiles_n;
+  const int per_pair = (balance && env_slices <= 0 && work >= 74 * 8) ? (work + 73) / 74 : 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles_m, slices, 1);
+  cfg.gridDim = per_pair ? dim3(2 * ((work + per_pair - 1) / per_pair), 1, 1) : dim3(tiles_m, slices, 1);
   cfg.blockDim = dim3(DUAL_THREADS, 1, 1);
   cfg.dynamicSmemBytes = D_SMEM;
   cfg.stream = st;
@@ -249,7 +290,7 @@ int launch_dual_silu(const CUtensorMap& t, const CUtensorMap& g, const CUtensorM
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dual_silu_kernel, t, g, u, h, a, tiles_n, per);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dual_silu_kernel, t, g, u, h, a, tiles_n, per, per_pair);
   count_launch();
   return (int)e;
 }
